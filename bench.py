@@ -1,0 +1,350 @@
+"""bench.py -- node.velocity updates/s of the palindromic PDG step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl product|reference]
+
+One "step" is one palindromic step M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
+over the whole workload (all rows of SURVEY §8(a)).  The default workload is
+BASELINE config 5 (3-D isothermal, 256^3 cells, p=2, D3Q6 x 4 components: 10.9 G
+node.velocity updates per step; f = 87 GB in place, far larger than L2, so no L2
+flush is needed between steps).  Multi-GPU (torchrun): velocities are sharded
+evenly and one NCCL sum of the moments per step feeds the local relaxation
+(strong scaling: total work fixed).
+
+The JSON line adds:
+  roofline     : the dominant kernel's algorithmic bytes / its CUDA-event time (on the
+                 library stream), against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline : the CPU oracle (oracle/, as it stands) timed on this host on a bounded
+                 sample of the same workload (N=64 sub-box of config 5, same p, nu, model).
+  e2e          : the same metric through the public C-ABI with HOST buffers: per step,
+                 pdg_set_equilibrium(host w0, pinned) + pdg_step(1) + pdg_moments(host w).
+  clocks       : nvidia-smi samples taken during the timed region.
+--impl reference times the oracle (the base contract's reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "node·velocity updates/s per palindromic PDG step (fp64), % of HBM roofline"
+UNIT = "node·velocity updates/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N=1) and the --impl reference arm
+# ----------------------------------------------------------------------------
+def oracle_sample_cfg(cfg, N_sub):
+    return cfg.resized(N_sub, name=f"{cfg.name}@N{N_sub}")
+
+
+def oracle_prepare(cfg, N_sub):
+    import numpy as np
+    from oracle import oracle as O
+    from pdg_inputs import w0_grid, wb_grid
+    sub = oracle_sample_cfg(cfg, N_sub)
+    pb = O.Problem.from_config(sub)
+    w0 = w0_grid(sub)
+    f0, fb = O.initial_data(pb, w0.numpy(), wb_grid(sub, w0).numpy())
+    fc = pb.grid_to_cells(f0)
+    fbc = pb.grid_to_cells(fb)
+    return sub, pb, fc, fbc, np
+
+
+def oracle_step(pb, fc, fbc):
+    from oracle import oracle as O
+    O.t2_all(pb, 0.5 * pb.dt, fc, fbc)
+    O.collide(pb, fc, pb.dt)
+    O.t2_all(pb, 0.5 * pb.dt, fc, fbc)
+
+
+def omp_threads():
+    try:
+        return int(os.environ.get("OMP_NUM_THREADS", "")) or os.cpu_count()
+    except ValueError:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, N_sub=64):
+    sub, pb, fc, fbc, _ = oracle_prepare(cfg, N_sub)
+    t0 = time.perf_counter()
+    oracle_step(pb, fc, fbc)
+    dt = time.perf_counter() - t0
+    ups = sub.updates_per_step / dt
+    return {"value": ups, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
+            "sample": f"1 M2 step of the {N_sub}^{cfg.dim}-cell sub-box of {cfg.name} (same p, lambda, nu, model; "
+                      f"{sub.updates_per_step} node.velocity updates, {dt:.2f} s), oracle/pdg_oracle.c -O2 "
+                      f"-ffp-contract=off, OpenMP over velocities/nodes"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    N_sub = args.ref_cells
+    sub, pb, fc, fbc, _ = oracle_prepare(cfg, N_sub)
+    for _ in range(args.warmup):
+        oracle_step(pb, fc, fbc)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(pb, fc, fbc)
+    dt = time.perf_counter() - t0
+    ups = sub.updates_per_step * args.steps / dt
+    sample = (f"each step = 1 M2 step of the {N_sub}^{cfg.dim}-cell sub-box of {cfg.name} (same p, lambda, nu, "
+              f"model; {sub.updates_per_step} node.velocity updates)")
+    line = {"impl": "reference", "metric": METRIC, "value": ups, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, pdg_inputs)",
+            "config": config_block(cfg, args.gpus),
+            "cpu_baseline": {"value": ups, "unit": UNIT, "cores": omp_threads(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": ups, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, G):
+    return {"workload": cfg.name, "dim": cfg.dim, "cells_per_axis": cfg.N, "degree": cfg.p, "m": cfg.m,
+            "nv": cfg.nv, "lambda": cfg.lam, "dt": cfg.dt, "nodes": cfg.nnodes,
+            "updates_per_step": cfg.updates_per_step, "f_bytes": 8 * cfg.nv * cfg.nnodes,
+            "l2": "inputs larger than L2 (f = %.1f GB >> 126 MB); no flush" % (8e-9 * cfg.nv * cfg.nnodes)
+            if 8 * cfg.nv * cfg.nnodes > 4 * 126e6 else "f fits in L2: HBM fraction not meaningful",
+            "parallelism": f"velocity-sharded x{G}" + (" + NCCL allreduce of w" if G > 1 else ""),
+            "scheme": "M2 = T2(dt/2) C2(dt) T2(dt/2), consecutive half-steps swept in one pass"}
+
+
+# ----------------------------------------------------------------------------
+# product arm
+# ----------------------------------------------------------------------------
+def fill_w0(cfg, w_flat, device):
+    """Seeded w0 on the device, generated in z-slabs straight into w_flat ([m][nodes])."""
+    import torch
+    from pdg_inputs import w0_grid
+    w = w_flat.view((cfg.m,) + cfg.grid_shape)
+    if cfg.dim == 2:
+        w.copy_(w0_grid(cfg, device=device))
+        return
+    L = cfg.N * cfg.n
+    slab = max(1, min(L, (1 << 25) // (L * L)))
+    for z0 in range(0, L, slab):
+        z1 = min(L, z0 + slab)
+        w[:, z0:z1].copy_(w0_grid(cfg, device=device, zslab=(z0, z1)))
+    torch.cuda.synchronize(device)
+
+
+def run_product(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_00169_b200 import pdg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        idt = torch.zeros(128, dtype=torch.uint8, device=device)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(pdg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    stream = torch.cuda.Stream(device)
+    with torch.cuda.stream(stream):
+        pb = pdg.problem_from_config(cfg, rank=rank, nranks=world, nccl_id=nccl_id, flags=pdg.PDG_PROFILE,
+                                     stream=stream.cuda_stream)
+        S = pdg.Solver(pb, device=device)
+        fill_w0(cfg, S.w, device)
+        S.set_equilibrium(S.w)
+        S.step(args.warmup)
+        S.profile_read()  # discard warm-up launches
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(device)
+        e0.record(stream)
+        S.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        ms = e0.elapsed_time(e1)
+        clk = clocks.stop()
+        prof = S.profile_read()
+        if world > 1:
+            dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        value = cfg.updates_per_step * args.steps / (ms * 1e-3)
+
+        # dominant kernel roofline (per launch = its algorithmic bytes / its event time)
+        peak, peak_src = peaks()
+        dom = max((k for k in prof if prof[k][1] > 0), key=lambda k: prof[k][0])
+        dms, dn, db = prof[dom]
+        achieved = db / (dms * 1e-3) / 1e9
+        launches = int(sum(v[1] for k, v in prof.items() if k != "allreduce"))
+        kernels = {k: {"ms_total": v[0], "launches": v[1], "alg_GB": v[2] / 1e9,
+                       "GB_per_s": (v[2] / (v[0] * 1e-3) / 1e9) if v[0] > 0 else None} for k, v in prof.items()
+                   if v[1] > 0}
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": dom, "peak_source": peak_src,
+                    "alg_bytes_per_launch": db / dn,
+                    "step_frac_48B_model": value * 48.0 / (peak * 1e9 * world)}
+
+        # end to end through the C-ABI with host buffers
+        e2e = None
+        if not args.no_e2e:
+            n_e2e = max(1, min(args.steps, args.e2e_steps))
+            w_host = torch.empty(S.sizes.w_elems, dtype=torch.float64, pin_memory=True)
+            w_out = torch.empty(S.sizes.w_elems, dtype=torch.float64, pin_memory=True)
+            fill_w0(cfg, S.w, device)
+            w_host.copy_(S.w)
+            torch.cuda.synchronize(device)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(n_e2e):
+                S.set_equilibrium(w_host)       # H2D of the step's input (pinned host)
+                S.step(1)
+                S.moments(w_out)                # D2H of the step's result
+            a1.record(stream)
+            torch.cuda.synchronize(device)
+            ems = a0.elapsed_time(a1)
+            wall = time.perf_counter() - t0
+            te = torch.tensor([ems], dtype=torch.float64, device=device)
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            ems = float(te.item())
+            e2e = {"value": cfg.updates_per_step * n_e2e / (ems * 1e-3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(8 * S.sizes.w_elems), "d2h_bytes_per_step": int(8 * S.sizes.w_elems),
+                   "steps": n_e2e, "ms_per_step": ems / n_e2e, "wall_s": wall,
+                   "call": "pdg_set_equilibrium(host w0) + pdg_step(1) + pdg_moments(host w) per step"}
+            S.profile_read()
+            del w_host, w_out
+
+        cpu = None
+        if world == 1 and rank == 0 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, args.cpu_cells)
+
+        if rank == 0:
+            line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                    "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic (seeded pdg_inputs recipe of the config)",
+                    "config": config_block(cfg, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                    "gpu_launches": launches, "clocks": clk, "kernels": kernels,
+                    "hbm_roofline_frac_48B": value * 48.0 / (peak * 1e9 * world)}
+            print(json.dumps(line), flush=True)
+        S.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=64)
+    ap.add_argument("--ref-cells", type=int, default=32)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "product":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    from pdg_inputs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_product(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,232 @@
+/*
+ * include/pdg.h -- C-ABI of libpdg, the B200-native hot path of the
+ * Palindromic Discontinuous Galerkin (PDG) method, arxiv 1702.00169.
+ *
+ * One call of pdg_step() advances a vectorial kinetic BGK system (P:110-138,
+ * eq kin_bgk, with tau = 0 and no source) by the palindromic step
+ *
+ *     M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
+ *
+ * where T2 is the Crank-Nicolson upwind-DG transport of every velocity
+ * (P:440-444 eq transport_cn, solved by the downwind sweep of P:622-637) and
+ * C2 is the relaxation f <- 2 f^eq(w) - f with w = P f.
+ * "P:n" = line n of the paper's LaTeX source.  Readings of silent or
+ * garbled passages are listed in DESIGN.md ("readings C1..C19").
+ *
+ * Conventions (all entry points):
+ *  - fp64 everywhere; every pointer is owned by the caller.  Host arrays are
+ *    read/written during the call only.  Device buffers given to pdg_create stay
+ *    bound to the context until pdg_destroy.  The library never allocates
+ *    device memory.
+ *  - Errors are returned as pdg_status codes; nothing aborts or throws.  A
+ *    human-readable detail of the last failure on the calling thread is
+ *    available from pdg_last_error().  After PDG_E_CUDA the context must be
+ *    destroyed.  Kernel faults are asynchronous and surface at the next
+ *    synchronising call (or immediately with PDG_SYNC_ERRORS).
+ *  - All device work is enqueued on the stream given in pdg_problem.cuda_stream
+ *    (a cudaStream_t, NULL = legacy default stream); pdg_step/pdg_transport/
+ *    pdg_collide are asynchronous and CUDA-graph capturable when nranks == 1.
+ *  - One context per device; calls on one context are serialised by the caller.
+ *
+ * Canonical layouts (row-major, last index fastest):
+ *  - node grid: for an N_0 x N_1 (x N_2) cell box of degree p, n = p+1 nodes per
+ *    cell and axis; node index (Z, Y, X) with X = c_x*n + a_x (a_x = local GL
+ *    node along x), same for Y, Z.  nnodes = prod_d (N_d * n).
+ *  - f:  [nv_local][Z][Y][X]   (local velocities of this rank, see pdg_sizes)
+ *  - fb: [nv_local][plane_stride]; velocity i (axis k_i) stores its inflow
+ *        plane = the node grid with axis k_i removed, in the same order
+ *        (e.g. axis y in 3-D: [Z][X]); plane_stride = max over axes.
+ *  - w:  [m][Z][Y][X]
+ *
+ * Velocity set: the vectorial D2Q4 / D3Q6-per-component set (reading C6):
+ *   velocity i = c*2D + 2k + s has v_i = (s ? -lambda : +lambda) e_k and
+ *   belongs to component c (P = block sums).  Any other set is rejected with
+ *   PDG_E_VELOCITY_SET.
+ */
+#ifndef PDG_H
+#define PDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pdg_ctx pdg_ctx; /* opaque, owned by the library */
+
+typedef enum {
+    PDG_OK = 0,
+    PDG_E_INVALID_ARGUMENT = 1, /* NULL pointer, bad size, dt == 0, lambda <= 0, tau < 0, nv % nranks != 0 */
+    PDG_E_DIMENSION = 2,        /* dim not in {2, 3}                                   (SPEC DimensionOutOfRange) */
+    PDG_E_DEGREE = 3,           /* degree not in the compiled set {1, 2, 3}            (SPEC DegreeOutOfRange) */
+    PDG_E_VELOCITY_SET = 4,     /* velocities not the canonical +-lambda e_k per component set, or comp[] wrong */
+    PDG_E_FLUX_MODEL = 5,       /* unknown flux kind, wrong m for it, or bad parameters */
+    PDG_E_STATE_NOT_SET = 6,    /* pdg_step / pdg_transport / pdg_collide before a set_state call */
+    PDG_E_NONPHYSICAL = 7,      /* (PDG_CHECK_STATE) rho <= 0 or non-finite value seen after the call;
+                                   the state WAS advanced                              (SPEC NonpositiveDensity) */
+    PDG_E_CUDA = 8,             /* a CUDA runtime error (launch or asynchronous fault) */
+    PDG_E_NCCL = 9,             /* NCCL unavailable or a collective failed (nranks > 1) */
+    PDG_E_BUFFER = 10,          /* a caller buffer is NULL or too small for pdg_sizes */
+    PDG_E_UNSUPPORTED = 11      /* valid request outside what this build implements */
+} pdg_status;
+
+typedef enum {
+    PDG_FLUX_LINEAR_ADVECTION = 0, /* m = 1:      q^k = a_k w;                      flux_params = a[dim] */
+    PDG_FLUX_EULER = 1,            /* m = dim+2:  compressible Euler, w = (rho, rho u, E); flux_params = {gamma} */
+    PDG_FLUX_ISOTHERMAL = 2        /* m = dim+1:  w = (rho, rho u), p = c^2 rho;    flux_params = {c} */
+} pdg_flux;
+
+typedef enum {
+    PDG_SCHEME_M2 = 0,    /* T2(dt/2) C2(dt) T2(dt/2), the hot path */
+    PDG_SCHEME_M2KIN = 1  /* T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) */
+} pdg_scheme;
+
+/* pdg_problem.flags */
+#define PDG_CHECK_STATE 0x1u  /* after each pdg_step, count nodes with rho <= 0 or non-finite f (one extra pass) */
+#define PDG_SYNC_ERRORS 0x2u  /* synchronise the stream after every call and report asynchronous faults there */
+#define PDG_NO_FUSION   0x4u  /* do not fuse step n's trailing T2(dt/2) with step n+1's leading one
+                                 (results agree to rounding; the fused form is two sweeps in one pass, not the
+                                 "collapsed" scheme of P:1173-1177) */
+#define PDG_PROFILE     0x8u  /* bracket every kernel launch with CUDA events on the context stream (read with
+                                 pdg_profile_read; not for use under CUDA-graph capture) */
+
+/* kernel kinds reported by pdg_profile_read */
+typedef enum {
+    PDG_K_SWEEP_STRIDED = 0, /* T2 sweeps of velocities along y/z (one or two sweeps per pass) */
+    PDG_K_SWEEP_X = 1,       /* T2 sweeps of velocities along x (warp-scan) */
+    PDG_K_RELAX = 2,         /* collision fused with moments (nranks == 1) */
+    PDG_K_PARTIAL = 3,       /* partial moments (nranks > 1, pdg_moments) */
+    PDG_K_RELAX_W = 4,       /* collision from reduced moments (nranks > 1) */
+    PDG_K_ALLREDUCE = 5,     /* NCCL sum of w */
+    PDG_K_OTHER = 6,         /* initialisation / checks */
+    PDG_NUM_KERNEL_KINDS = 7
+} pdg_kernel_kind;
+
+typedef struct {
+    int32_t dim;                 /* D in {2, 3} */
+    int64_t ncell[3];            /* cells per axis (x, y, z); ncell[d] = 1 for d >= dim */
+    double lo[3], hi[3];         /* box [lo, hi] (affine cells) */
+    int32_t degree;              /* p: (p+1)^D Gauss-Lobatto nodes per cell */
+    int32_t m;                   /* number of conservative variables w */
+    int32_t nv;                  /* number of velocities */
+    const double *vel;           /* host, nv*3 (row i = v_i, unused components 0); copied */
+    const int32_t *comp;         /* host, nv: P[c][i] = (comp[i] == c); copied */
+    double lambda;               /* lattice speed, |v_i| = lambda */
+    int32_t flux;                /* pdg_flux: the flux q(w) defining f^eq */
+    const double *flux_params;   /* host, n_flux_params values (see pdg_flux); copied */
+    int32_t n_flux_params;
+    double tau;                  /* relaxation time; 0 => f <- 2 f^eq - f */
+    double dt;                   /* time step of one palindromic step (may be negative) */
+    int32_t scheme;              /* pdg_scheme */
+    int32_t rank, nranks;        /* velocity shard: contiguous block of nv/nranks velocity indices */
+    const void *nccl_id;         /* 128-byte ncclUniqueId (identical on all ranks).  NULL with nranks > 1
+                                    creates a communicator-less shard: pdg_collide/pdg_moments then return
+                                    PDG_E_NCCL and the caller reduces w_dev itself between
+                                    pdg_partial_moments and pdg_relax_from_w */
+    void *cuda_stream;           /* cudaStream_t for every launch of this context */
+    uint32_t flags;              /* PDG_CHECK_STATE | PDG_SYNC_ERRORS | PDG_NO_FUSION */
+} pdg_problem;
+
+typedef struct {
+    size_t f_elems;        /* doubles in f_dev  = nv_local * nnodes */
+    size_t fb_elems;       /* doubles in fb_dev = nv_local * plane_stride */
+    size_t w_elems;        /* doubles in w_dev  = m * nnodes (moments / sharded exchange / equilibrium init) */
+    size_t work_bytes;     /* bytes of work_dev (device scratch: counters) */
+    int64_t nnodes;        /* nodes of the full grid */
+    int64_t plane_stride;  /* doubles per velocity in fb */
+    int32_t nv_local;      /* velocities owned by this rank */
+    int32_t v_begin;       /* first owned velocity index */
+} pdg_sizes;
+
+/* Validate *p and return the buffer sizes of this rank.  Host-only: needs no GPU.
+ * Errors: PDG_E_INVALID_ARGUMENT, PDG_E_DIMENSION, PDG_E_DEGREE, PDG_E_VELOCITY_SET, PDG_E_FLUX_MODEL. */
+pdg_status pdg_query_sizes(const pdg_problem *p, pdg_sizes *out);
+
+/* Create a context bound to caller-owned device buffers sized by pdg_query_sizes
+ * (f_dev, fb_dev, w_dev, work_dev: 256-byte aligned device pointers on the current
+ * device).  Precomputes the per-axis cell blocks (the KLU refactorisation of P:769-777
+ * becomes a tiny precomputed inverse: dt and v are constant).  With nranks > 1 it
+ * also creates an NCCL communicator from nccl_id (collective over all ranks).
+ * Errors: as pdg_query_sizes, plus PDG_E_BUFFER, PDG_E_CUDA, PDG_E_NCCL. */
+pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, double *w_dev, void *work_dev,
+                      pdg_ctx **out);
+
+/* Load the kinetic state.  f: f_elems doubles in the canonical layout; fb:
+ * fb_elems doubles (inflow planes, constant in time: P:183-184).
+ * Either may be NULL to keep the bound buffer's content.  on_device != 0:
+ * pointers are device memory, else host (copied on the context stream, then
+ * the stream is synchronised before returning). */
+pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_device);
+
+/* Equilibrium initialisation (readings C12, C13): f_i = f^eq_i(w) at every node and
+ * fb_i = f^eq_i(wb) on the inflow plane of velocity i.  w, wb: [m][nodes] (w_elems
+ * doubles); wb == NULL means wb = w.  Host pointers are staged through w_dev. */
+pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, int on_device);
+
+/* Copy the current f (f_elems doubles, canonical layout) out (checkpoint/readback). */
+pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
+
+/* Advance nsteps palindromic steps (scheme of pdg_problem; nsteps == 0 is a no-op).
+ * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE. */
+pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
+
+/* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):
+ * f <- (I + dtp/2 L_h)(I - dtp/2 L_h)^{-1} f with fictitious inflow cells f^b. */
+pdg_status pdg_transport(pdg_ctx *c, double dtp);
+
+/* One collision operator C2(dt) on every node (row a2): w = P f, f^eq(w),
+ * f <- ((2 tau - dt) f + 2 dt f^eq)/(2 tau + dt)   (= 2 f^eq - f at tau = 0).
+ * With nranks > 1: partial moments, NCCL sum, then relaxation of local velocities. */
+pdg_status pdg_collide(pdg_ctx *c, double dt);
+
+/* The two halves of the sharded collision (row a4), exposed for testing:
+ * pdg_partial_moments writes w_dev = sum over LOCAL velocities of each component
+ * (zeros for components without local velocities); pdg_relax_from_w applies C2(dt)
+ * to the local velocities from the (already reduced) w_dev. */
+pdg_status pdg_partial_moments(pdg_ctx *c);
+pdg_status pdg_relax_from_w(pdg_ctx *c, double dt);
+
+/* Moments w = P f of the full state ([m][nodes], w_elems doubles) into w (host or
+ * device); with nranks > 1 the partial sums are reduced over ranks (every rank gets w). */
+pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device);
+
+/* Number of nodes with rho <= 0 or a non-finite f seen in the local state
+ * (synchronising).  Component 0 of w is the density for the Euler/isothermal models. */
+pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad);
+
+/* The precomputed 1-D cell block of the T2(dtp) sweep along `axis` (reading C18):
+ * f_new = M f_old + g s_in, s_out = f_old[n-1] + f_new[n-1], nodes in flow order;
+ * M: n*n row-major, g: n, beta = g[n-1].  Host outputs.  For inspection/pins. */
+pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, double *g, double *beta);
+
+/* Block until all work enqueued by this context has finished; reports asynchronous faults. */
+pdg_status pdg_synchronize(pdg_ctx *c);
+
+/* Destroy the context (NULL-safe); destroys the NCCL communicator if any. Does not free caller buffers. */
+void pdg_destroy(pdg_ctx *c);
+
+/* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls it and broadcasts).
+ * Errors: PDG_E_NCCL if libnccl.so.2 cannot be loaded. */
+pdg_status pdg_nccl_unique_id(void *out);
+
+/* Static description of a status code. */
+const char *pdg_status_string(pdg_status s);
+
+/* Detail of the last error reported on the calling thread ("" if none). */
+const char *pdg_last_error(void);
+
+/* (PDG_PROFILE) Synchronise, then return per kernel kind the summed device time in ms,
+ * the number of launches and the algorithmic bytes moved since the last read, and reset.
+ * Each array has PDG_NUM_KERNEL_KINDS entries (any may be NULL).  Algorithmic bytes =
+ * one fp64 read + one write of every value a launch updates, plus its side inputs
+ * (inflow planes, moments), i.e. the traffic of a perfect single pass. */
+pdg_status pdg_profile_read(pdg_ctx *c, double *ms, int64_t *launches, double *alg_bytes);
+
+/* Library version string ("pdg-b200 <version> sm_100a"). */
+const char *pdg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDG_H */

@@ -1,0 +1,40 @@
+"""Build libpdg.so in-tree for sm_100a (B200) with nvcc.  No JIT, no fallback."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libpdg.so")
+SOURCES = [os.path.join(SRC, "pdg_api.cu")]
+DEPS = SOURCES + [os.path.join(SRC, f) for f in ("pdg_kernels.cuh", "pdg_tables.hpp", "pdg_comm.hpp")] + \
+    [os.path.join(os.path.dirname(HERE), "include", "pdg.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc_cmd(out=LIB, extra=()):
+    return [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
+            "--expt-relaxed-constexpr", *extra, "-o", out, *SOURCES, "-ldl"]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or needs_build():
+        tmp = LIB + f".tmp{os.getpid()}"
+        cmd = nvcc_cmd(tmp, ("-Xptxas", "-v") if verbose else ())
+        subprocess.check_call(cmd, stdout=sys.stderr if verbose else subprocess.DEVNULL)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,745 @@
+// libpdg: C-ABI of the B200-native PDG hot path (declared in include/pdg.h).
+//
+// The host side validates the problem statement, precomputes the cell
+// blocks (pdg_tables.hpp) and enqueues the sm_100a kernels of pdg_kernels.cuh on the
+// caller's stream.  No device allocation, no host fallback: every arithmetic step of
+// the hot path runs in these kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pdg.h"
+#include "pdg_comm.hpp"
+#include "pdg_kernels.cuh"
+#include "pdg_tables.hpp"
+
+#ifndef PDG_VERSION
+#define PDG_VERSION "0.1.0"
+#endif
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pdg_status fail(pdg_status s, const std::string &msg)
+{
+    g_last_error = msg;
+    return s;
+}
+
+#define PDG_CUDA_TRY(expr)                                                                             \
+    do {                                                                                               \
+        cudaError_t e_ = (expr);                                                                       \
+        if (e_ != cudaSuccess)                                                                         \
+            return fail(PDG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));               \
+    } while (0)
+
+struct Geometry {
+    int dim = 0, p = 0, n = 0, m = 0, nv = 0, nvl = 0, v0 = 0;
+    int64_t ncell[3] = {1, 1, 1};
+    int64_t L[3] = {1, 1, 1};      // nodes per axis
+    int64_t stride[3] = {1, 1, 1}; // element stride of each axis in the node grid
+    int64_t nnodes = 0, plane_stride = 0;
+    double h[3] = {1, 1, 1};
+};
+
+pdg_status validate(const pdg_problem *p, Geometry *g)
+{
+    if (!p) return fail(PDG_E_INVALID_ARGUMENT, "problem is NULL");
+    if (p->dim != 2 && p->dim != 3) return fail(PDG_E_DIMENSION, "dim must be 2 or 3");
+    if (p->degree < 1 || p->degree > 3) return fail(PDG_E_DEGREE, "degree must be 1, 2 or 3");
+    if (!(p->lambda > 0.0) || !std::isfinite(p->lambda)) return fail(PDG_E_INVALID_ARGUMENT, "lambda must be > 0");
+    if (!(p->dt != 0.0) || !std::isfinite(p->dt)) return fail(PDG_E_INVALID_ARGUMENT, "dt must be finite and != 0");
+    if (!(p->tau >= 0.0) || !std::isfinite(p->tau)) return fail(PDG_E_INVALID_ARGUMENT, "tau must be >= 0");
+    if (p->scheme != PDG_SCHEME_M2 && p->scheme != PDG_SCHEME_M2KIN)
+        return fail(PDG_E_INVALID_ARGUMENT, "unknown scheme");
+    if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
+    g->dim = p->dim;
+    g->p = p->degree;
+    g->n = p->degree + 1;
+    for (int d = 0; d < 3; ++d) {
+        const int64_t nc = p->ncell[d];
+        if (d < p->dim) {
+            if (nc < 1) return fail(PDG_E_INVALID_ARGUMENT, "ncell must be >= 1");
+            if (!(p->hi[d] > p->lo[d])) return fail(PDG_E_INVALID_ARGUMENT, "hi must be > lo");
+            g->ncell[d] = nc;
+            g->L[d] = nc * g->n;
+            g->h[d] = (p->hi[d] - p->lo[d]) / (double)nc;
+        } else {
+            g->ncell[d] = 1;
+            g->L[d] = 1;
+        }
+    }
+    // x-sweep line length must fit the int32 cell counter
+    if (g->ncell[0] > (int64_t)1 << 30 || g->ncell[1] > (int64_t)1 << 30 || g->ncell[2] > (int64_t)1 << 30)
+        return fail(PDG_E_INVALID_ARGUMENT, "too many cells along an axis");
+    g->stride[0] = 1;
+    g->stride[1] = g->L[0];
+    g->stride[2] = g->L[0] * g->L[1];
+    g->nnodes = g->L[0] * g->L[1] * g->L[2];
+    int64_t ps = 0;
+    for (int d = 0; d < p->dim; ++d) ps = std::max(ps, g->nnodes / g->L[d]);
+    g->plane_stride = ps;
+
+    // flux model and m
+    int m_expect = 0;
+    if (p->flux == PDG_FLUX_LINEAR_ADVECTION) {
+        m_expect = 1;
+        if (!p->flux_params || p->n_flux_params < p->dim)
+            return fail(PDG_E_FLUX_MODEL, "advection needs flux_params = a[dim]");
+    } else if (p->flux == PDG_FLUX_EULER) {
+        m_expect = p->dim + 2;
+        if (!p->flux_params || p->n_flux_params < 1 || !(p->flux_params[0] > 1.0))
+            return fail(PDG_E_FLUX_MODEL, "Euler needs flux_params = {gamma > 1}");
+    } else if (p->flux == PDG_FLUX_ISOTHERMAL) {
+        m_expect = p->dim + 1;
+        if (!p->flux_params || p->n_flux_params < 1 || !(p->flux_params[0] > 0.0))
+            return fail(PDG_E_FLUX_MODEL, "isothermal needs flux_params = {c > 0}");
+    } else {
+        return fail(PDG_E_FLUX_MODEL, "unknown flux model");
+    }
+    if (p->m != m_expect) return fail(PDG_E_FLUX_MODEL, "m does not match the flux model");
+    g->m = p->m;
+
+    // velocity set: canonical vectorial D2Q4 / D3Q6 per component (reading C6)
+    if (p->nv != p->m * 2 * p->dim) return fail(PDG_E_VELOCITY_SET, "nv must be m * 2 * dim");
+    if (p->nv > pdg::kMaxVel) return fail(PDG_E_VELOCITY_SET, "too many velocities");
+    if (!p->vel || !p->comp) return fail(PDG_E_INVALID_ARGUMENT, "vel/comp are NULL");
+    for (int i = 0; i < p->nv; ++i) {
+        const int c = i / (2 * p->dim), k = (i % (2 * p->dim)) / 2, s = i % 2;
+        if (p->comp[i] != c) return fail(PDG_E_VELOCITY_SET, "comp[i] must be i / (2 dim)");
+        for (int d = 0; d < 3; ++d) {
+            const double expect = (d == k) ? (s ? -p->lambda : p->lambda) : 0.0;
+            if (p->vel[3 * i + d] != expect)
+                return fail(PDG_E_VELOCITY_SET, "velocity " + std::to_string(i) +
+                                                    " must be (s ? -lambda : lambda) e_k, i = c*2D + 2k + s");
+        }
+    }
+    g->nv = p->nv;
+    if (p->nv % p->nranks != 0) return fail(PDG_E_INVALID_ARGUMENT, "nv must be divisible by nranks");
+    g->nvl = p->nv / p->nranks;
+    g->v0 = p->rank * g->nvl;
+    return PDG_OK;
+}
+
+void fill_sizes(const Geometry &g, pdg_sizes *out)
+{
+    out->f_elems = (size_t)g.nvl * (size_t)g.nnodes;
+    out->fb_elems = (size_t)g.nvl * (size_t)g.plane_stride;
+    out->w_elems = (size_t)g.m * (size_t)g.nnodes;
+    out->work_bytes = 256;
+    out->nnodes = g.nnodes;
+    out->plane_stride = g.plane_stride;
+    out->nv_local = g.nvl;
+    out->v_begin = g.v0;
+}
+
+struct ProfRec {
+    int kind;
+    int ev;        // index of the start event; stop = ev + 1
+    double bytes;  // algorithmic bytes of the launch
+};
+
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<ProfRec> recs;
+    int next = 0;
+};
+
+}  // namespace
+
+struct pdg_ctx {
+    Geometry g;
+    pdg_problem prob;
+    std::vector<double> vel;
+    std::vector<int32_t> comp;
+    double fparams[3] = {0, 0, 0};
+    double *f = nullptr, *fb = nullptr, *w = nullptr;
+    unsigned long long *counter = nullptr;
+    cudaStream_t stream = nullptr;
+    bool state_set = false;
+    pdg::ModelParams mp{};
+    pdg::SweepParams x_params{};        // velocities along x
+    pdg::SweepParams yz_params{};       // velocities along y / z
+    pdg::SweepParams all_params{};      // every local velocity (inflow initialisation)
+    pdg::NcclComm comm;
+    int device = 0;
+    Profiler prof;
+};
+
+namespace {
+
+pdg_status post_launch(pdg_ctx *c, const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PDG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    if (c->prob.flags & PDG_SYNC_ERRORS) {
+        e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) return fail(PDG_E_CUDA, std::string(what) + " (async): " + cudaGetErrorString(e));
+    }
+    return PDG_OK;
+}
+
+// PDG_PROFILE: CUDA events bracketing each launch on the context stream.
+int prof_begin(pdg_ctx *c)
+{
+    if (!c->prof.on || c->prof.next + 2 > (int)c->prof.ev.size()) return -1;
+    const int i = c->prof.next;
+    c->prof.next += 2;
+    cudaEventRecord(c->prof.ev[i], c->stream);
+    return i;
+}
+
+void prof_end(pdg_ctx *c, int i, int kind, double bytes)
+{
+    if (i < 0) return;
+    cudaEventRecord(c->prof.ev[i + 1], c->stream);
+    c->prof.recs.push_back({kind, i, bytes});
+}
+
+int grid_for(int64_t work, int threads)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+bool fill_blocks(pdg_ctx *c, double dtp, pdg::DevBlock blk[3])
+{
+    for (int d = 0; d < 3; ++d) {
+        pdg::CellBlock cb;
+        const double hd = (d < c->g.dim) ? c->g.h[d] : c->g.h[0];
+        const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)hd;
+        if (!pdg::cell_block(c->g.p, kappa, &cb)) return false;
+        std::memset(&blk[d], 0, sizeof(blk[d]));
+        for (int i = 0; i < cb.n * cb.n; ++i) blk[d].M[i] = cb.M[i];
+        for (int i = 0; i < cb.n; ++i) blk[d].g[i] = cb.g[i];
+    }
+    return true;
+}
+
+double sweep_bytes(const pdg_ctx *c, const pdg::SweepParams &sp)
+{
+    double b = 0.0;
+    for (int i = 0; i < sp.nvel; ++i) b += 16.0 * (double)c->g.nnodes + 8.0 * (double)sp.v[i].nlines;
+    return b;
+}
+
+template <int N, int NPASS>
+void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParams &yzp)
+{
+    if (yzp.nvel > 0) {
+        int64_t maxl = 0;
+        for (int i = 0; i < yzp.nvel; ++i) maxl = std::max(maxl, yzp.v[i].nlines);
+        dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
+        const int e = prof_begin(c);
+        pdg::sweep_strided_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
+        prof_end(c, e, PDG_K_SWEEP_STRIDED, sweep_bytes(c, yzp));
+    }
+    if (xp.nvel > 0) {
+        int64_t maxl = 0;
+        for (int i = 0; i < xp.nvel; ++i) maxl = std::max(maxl, xp.v[i].nlines);
+        dim3 grid((unsigned)((maxl + pdg::kXsWarps - 1) / pdg::kXsWarps), (unsigned)xp.nvel);
+        const int e = prof_begin(c);
+        pdg::sweep_x_kernel<N, NPASS><<<grid, pdg::kXsWarps * 32, 0, c->stream>>>(xp);
+        prof_end(c, e, PDG_K_SWEEP_X, sweep_bytes(c, xp));
+    }
+}
+
+// One pass over f applying T2(dtp) npass times (npass in {1, 2}).
+pdg_status transport_pass(pdg_ctx *c, double dtp, int npass)
+{
+    pdg::SweepParams xp = c->x_params, yzp = c->yz_params;
+    pdg::DevBlock blk[3];
+    if (!fill_blocks(c, dtp, blk)) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block for this dt");
+    std::memcpy(xp.blk, blk, sizeof(blk));
+    std::memcpy(yzp.blk, blk, sizeof(blk));
+    const int n = c->g.n;
+    if (npass == 1) {
+        if (n == 2) launch_sweeps<2, 1>(c, xp, yzp);
+        else if (n == 3) launch_sweeps<3, 1>(c, xp, yzp);
+        else launch_sweeps<4, 1>(c, xp, yzp);
+    } else {
+        if (n == 2) launch_sweeps<2, 2>(c, xp, yzp);
+        else if (n == 3) launch_sweeps<3, 2>(c, xp, yzp);
+        else launch_sweeps<4, 2>(c, xp, yzp);
+    }
+    return post_launch(c, "sweep");
+}
+
+template <int DIM, int MODEL>
+void launch_relax_t(pdg_ctx *c, double ca, double cb)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::relax_kernel<DIM, MODEL><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->mp, ca, cb);
+    prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
+}
+
+template <int DIM, int MODEL>
+void launch_partial_t(pdg_ctx *c)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::partial_moments_kernel<DIM, pdg::Model<DIM, MODEL>::M>
+        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl);
+    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)c->g.nnodes);
+}
+
+template <int DIM, int MODEL>
+void launch_relax_from_w_t(pdg_ctx *c, double ca, double cb)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::relax_from_w_kernel<DIM, MODEL>
+        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp, ca, cb);
+    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)c->g.nnodes);
+}
+
+template <int DIM, int MODEL>
+void launch_equilibrium_t(pdg_ctx *c, const double *w, const double *wb)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    pdg::equilibrium_kernel<DIM, MODEL><<<grid, 256, 0, c->stream>>>(c->f, w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp);
+    int64_t maxl = 0;
+    for (int i = 0; i < c->all_params.nvel; ++i) maxl = std::max(maxl, c->all_params.v[i].nlines);
+    dim3 g2((unsigned)((maxl + 255) / 256), (unsigned)c->all_params.nvel);
+    pdg::inflow_equilibrium_kernel<DIM, MODEL>
+        <<<g2, 256, 0, c->stream>>>(c->fb, wb, c->g.nnodes, c->all_params, c->g.n, c->mp);
+}
+
+// dispatch on (dim, flux model)
+#define PDG_DISPATCH(FN, ...)                                                                       \
+    do {                                                                                            \
+        const int dim_ = c->g.dim, mod_ = c->prob.flux;                                             \
+        if (dim_ == 2 && mod_ == 0) FN<2, pdg::MODEL_ADV>(__VA_ARGS__);                             \
+        else if (dim_ == 2 && mod_ == 1) FN<2, pdg::MODEL_EULER>(__VA_ARGS__);                      \
+        else if (dim_ == 2 && mod_ == 2) FN<2, pdg::MODEL_ISO>(__VA_ARGS__);                        \
+        else if (dim_ == 3 && mod_ == 0) FN<3, pdg::MODEL_ADV>(__VA_ARGS__);                        \
+        else if (dim_ == 3 && mod_ == 1) FN<3, pdg::MODEL_EULER>(__VA_ARGS__);                      \
+        else FN<3, pdg::MODEL_ISO>(__VA_ARGS__);                                                    \
+    } while (0)
+
+void collision_coeffs(const pdg_ctx *c, double dt, double *ca, double *cb)
+{
+    const double tau = c->prob.tau;
+    if (tau == 0.0) {  // over-relaxation f <- 2 f^eq - f
+        *ca = -1.0;
+        *cb = 2.0;
+    } else {           // eq collision_cn
+        *ca = (2.0 * tau - dt) / (2.0 * tau + dt);
+        *cb = 2.0 * dt / (2.0 * tau + dt);
+    }
+}
+
+pdg_status partial_and_reduce(pdg_ctx *c)
+{
+    PDG_DISPATCH(launch_partial_t, c);
+    pdg_status s = post_launch(c, "partial_moments");
+    if (s != PDG_OK) return s;
+    if (c->prob.nranks > 1) {
+        std::string err;
+        if (!c->comm.comm) return fail(PDG_E_NCCL, "communicator-less shard context: reduce w_dev yourself "
+                                                   "between pdg_partial_moments and pdg_relax_from_w");
+        const int e = prof_begin(c);
+        if (!c->comm.allreduce_sum(c->w, (size_t)c->g.m * (size_t)c->g.nnodes, c->stream, &err))
+            return fail(PDG_E_NCCL, err);
+        prof_end(c, e, PDG_K_ALLREDUCE, 8.0 * (double)c->g.m * (double)c->g.nnodes);
+    }
+    return PDG_OK;
+}
+
+pdg_status collide(pdg_ctx *c, double dt)
+{
+    double ca, cb;
+    collision_coeffs(c, dt, &ca, &cb);
+    if (c->prob.nranks == 1) {
+        PDG_DISPATCH(launch_relax_t, c, ca, cb);
+        return post_launch(c, "relax");
+    }
+    pdg_status s = partial_and_reduce(c);
+    if (s != PDG_OK) return s;
+    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    return post_launch(c, "relax_from_w");
+}
+
+void build_sweep_params(pdg_ctx *c)
+{
+    const Geometry &g = c->g;
+    std::memset(&c->x_params, 0, sizeof(c->x_params));
+    std::memset(&c->yz_params, 0, sizeof(c->yz_params));
+    std::memset(&c->all_params, 0, sizeof(c->all_params));
+    for (auto *sp : {&c->x_params, &c->yz_params, &c->all_params}) {
+        sp->f = c->f;
+        sp->fb = c->fb;
+    }
+    for (int j = 0; j < g.nvl; ++j) {
+        const int i = g.v0 + j;
+        const int k = (i % (2 * g.dim)) / 2;
+        const int s = i % 2;
+        pdg::SweepVel V{};
+        V.f_off = (int64_t)j * g.nnodes;
+        V.fb_off = (int64_t)j * g.plane_stride;
+        V.inner = g.stride[k];
+        V.nlines = g.nnodes / g.L[k];
+        V.ncells = (int32_t)g.ncell[k];
+        V.sign = s ? -1 : 1;
+        V.axis = k;
+        V.vel = i;
+        c->all_params.v[c->all_params.nvel++] = V;
+        if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
+        else c->yz_params.v[c->yz_params.nvel++] = V;
+    }
+}
+
+bool is_device_pointer(const void *p)
+{
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+pdg_status pdg_query_sizes(const pdg_problem *p, pdg_sizes *out)
+{
+    if (!out) return fail(PDG_E_INVALID_ARGUMENT, "out is NULL");
+    Geometry g;
+    pdg_status s = validate(p, &g);
+    if (s != PDG_OK) return s;
+    fill_sizes(g, out);
+    return PDG_OK;
+}
+
+pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, double *w_dev, void *work_dev,
+                      pdg_ctx **out)
+{
+    if (!out) return fail(PDG_E_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    Geometry g;
+    pdg_status s = validate(p, &g);
+    if (s != PDG_OK) return s;
+    if (!f_dev || !fb_dev || !w_dev || !work_dev) return fail(PDG_E_BUFFER, "device buffers must be non-NULL");
+    for (const void *ptr : {(const void *)f_dev, (const void *)fb_dev, (const void *)w_dev, (const void *)work_dev})
+        if (!is_device_pointer(ptr)) return fail(PDG_E_BUFFER, "buffers must be device memory");
+    pdg_ctx *c = new pdg_ctx();
+    c->g = g;
+    c->prob = *p;
+    c->vel.assign(p->vel, p->vel + 3 * p->nv);
+    c->comp.assign(p->comp, p->comp + p->nv);
+    for (int i = 0; i < p->n_flux_params && i < 3; ++i) c->fparams[i] = p->flux_params[i];
+    c->prob.vel = c->vel.data();
+    c->prob.comp = c->comp.data();
+    c->prob.flux_params = c->fparams;
+    c->prob.nccl_id = nullptr;
+    c->f = f_dev;
+    c->fb = fb_dev;
+    c->w = w_dev;
+    c->counter = (unsigned long long *)work_dev;
+    c->stream = (cudaStream_t)p->cuda_stream;
+    cudaGetDevice(&c->device);
+    std::memset(&c->mp, 0, sizeof(c->mp));
+    if (p->flux == PDG_FLUX_LINEAR_ADVECTION)
+        for (int d = 0; d < p->dim; ++d) c->mp.a[d] = p->flux_params[d];
+    if (p->flux == PDG_FLUX_EULER) c->mp.gamma = p->flux_params[0];
+    if (p->flux == PDG_FLUX_ISOTHERMAL) c->mp.c2 = p->flux_params[0] * p->flux_params[0];
+    c->mp.inv2D = 1.0 / (2.0 * p->dim);
+    c->mp.inv2lam = 1.0 / (2.0 * p->lambda);
+    build_sweep_params(c);
+    if (p->flags & PDG_PROFILE) {
+        c->prof.on = true;
+        c->prof.ev.resize(2 * 4096);
+        for (auto &e : c->prof.ev) {
+            if (cudaEventCreate(&e) != cudaSuccess) {
+                e = nullptr;
+                c->prof.on = false;
+            }
+        }
+        if (!c->prof.on) {
+            for (auto &e : c->prof.ev)
+                if (e) cudaEventDestroy(e);
+            delete c;
+            return fail(PDG_E_CUDA, "cudaEventCreate failed");
+        }
+    }
+    if (p->nranks > 1 && p->nccl_id) {
+        std::string err;
+        if (!c->comm.init(p->nccl_id, p->nranks, p->rank, &err)) {
+            delete c;
+            return fail(PDG_E_NCCL, err);
+        }
+    }
+    *out = c;
+    return PDG_OK;
+}
+
+pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_device)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (f) PDG_CUDA_TRY(cudaMemcpyAsync(c->f, f, sizeof(double) * c->g.nvl * c->g.nnodes, kind, c->stream));
+    if (fb)
+        PDG_CUDA_TRY(cudaMemcpyAsync(c->fb, fb, sizeof(double) * c->g.nvl * c->g.plane_stride, kind, c->stream));
+    if (!on_device || (c->prob.flags & PDG_SYNC_ERRORS)) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->state_set = true;
+    return PDG_OK;
+}
+
+pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, int on_device)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!w) return fail(PDG_E_INVALID_ARGUMENT, "w is NULL");
+    const size_t wbytes = sizeof(double) * c->g.m * c->g.nnodes;
+    if (!on_device) {
+        // stage through w_dev: inflow data first (from wb), then the interior (from w)
+        PDG_CUDA_TRY(cudaMemcpyAsync(c->w, wb ? wb : w, wbytes, cudaMemcpyHostToDevice, c->stream));
+        PDG_DISPATCH(launch_equilibrium_t, c, c->w, c->w);
+        pdg_status s = post_launch(c, "equilibrium(wb)");
+        if (s != PDG_OK) return s;
+        if (wb) {
+            PDG_CUDA_TRY(cudaMemcpyAsync(c->w, w, wbytes, cudaMemcpyHostToDevice, c->stream));
+            const int grid = grid_for(c->g.nnodes, 256);
+            const int dim = c->g.dim, mod = c->prob.flux;
+#define PDG_EQ_ONLY(D, MO) pdg::equilibrium_kernel<D, MO><<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp)
+            if (dim == 2 && mod == 0) PDG_EQ_ONLY(2, pdg::MODEL_ADV);
+            else if (dim == 2 && mod == 1) PDG_EQ_ONLY(2, pdg::MODEL_EULER);
+            else if (dim == 2 && mod == 2) PDG_EQ_ONLY(2, pdg::MODEL_ISO);
+            else if (dim == 3 && mod == 0) PDG_EQ_ONLY(3, pdg::MODEL_ADV);
+            else if (dim == 3 && mod == 1) PDG_EQ_ONLY(3, pdg::MODEL_EULER);
+            else PDG_EQ_ONLY(3, pdg::MODEL_ISO);
+#undef PDG_EQ_ONLY
+            s = post_launch(c, "equilibrium(w)");
+            if (s != PDG_OK) return s;
+        }
+        PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    } else {
+        PDG_DISPATCH(launch_equilibrium_t, c, w, wb ? wb : w);
+        pdg_status s = post_launch(c, "equilibrium");
+        if (s != PDG_OK) return s;
+    }
+    c->state_set = true;
+    return PDG_OK;
+}
+
+pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device)
+{
+    if (!c || !f) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
+    PDG_CUDA_TRY(cudaMemcpyAsync(f, c->f, sizeof(double) * c->g.nvl * c->g.nnodes,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    if (!on_device) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return PDG_OK;
+}
+
+pdg_status pdg_transport(pdg_ctx *c, double dtp)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
+    if (!std::isfinite(dtp)) return fail(PDG_E_INVALID_ARGUMENT, "dtp must be finite");
+    return transport_pass(c, dtp, 1);
+}
+
+pdg_status pdg_collide(pdg_ctx *c, double dt)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
+    return collide(c, dt);
+}
+
+pdg_status pdg_partial_moments(pdg_ctx *c)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    PDG_DISPATCH(launch_partial_t, c);
+    return post_launch(c, "partial_moments");
+}
+
+pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    double ca, cb;
+    collision_coeffs(c, dt, &ca, &cb);
+    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    return post_launch(c, "relax_from_w");
+}
+
+pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
+    if (nsteps == 0) return PDG_OK;
+    if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
+    const double dt = c->prob.dt;
+    const bool fuse = !(c->prob.flags & PDG_NO_FUSION);
+    pdg_status s = PDG_OK;
+    if (c->prob.scheme == PDG_SCHEME_M2) {
+        // M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
+        s = transport_pass(c, 0.5 * dt, 1);
+        for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
+            s = collide(c, dt);
+            if (s != PDG_OK) break;
+            if (k + 1 < nsteps && fuse) s = transport_pass(c, 0.5 * dt, 2);  // T2(dt/2) then T2(dt/2), one pass
+            else if (k + 1 < nsteps) {
+                s = transport_pass(c, 0.5 * dt, 1);
+                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
+            } else s = transport_pass(c, 0.5 * dt, 1);
+        }
+    } else {
+        // M2kin(dt) = T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4)
+        s = transport_pass(c, 0.25 * dt, 1);
+        for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
+            s = collide(c, 0.5 * dt);
+            if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
+            if (s == PDG_OK) s = collide(c, 0.5 * dt);
+            if (s != PDG_OK) break;
+            if (k + 1 < nsteps && fuse) s = transport_pass(c, 0.25 * dt, 2);
+            else if (k + 1 < nsteps) {
+                s = transport_pass(c, 0.25 * dt, 1);
+                if (s == PDG_OK) s = transport_pass(c, 0.25 * dt, 1);
+            } else s = transport_pass(c, 0.25 * dt, 1);
+        }
+    }
+    if (s != PDG_OK) return s;
+    if (c->prob.flags & PDG_CHECK_STATE) {
+        int64_t bad = 0;
+        s = pdg_check_state(c, &bad);
+        if (s != PDG_OK) return s;
+        if (bad > 0) return fail(PDG_E_NONPHYSICAL, std::to_string(bad) + " nodes with rho <= 0 or non-finite f");
+    }
+    return PDG_OK;
+}
+
+pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device)
+{
+    if (!c || !w) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
+    pdg_status s = partial_and_reduce(c);
+    if (s != PDG_OK) return s;
+    const size_t bytes = sizeof(double) * c->g.m * c->g.nnodes;
+    if (w != c->w)
+        PDG_CUDA_TRY(cudaMemcpyAsync(w, c->w, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                     c->stream));
+    if (!on_device) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return PDG_OK;
+}
+
+pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad)
+{
+    if (!c || !n_bad) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
+    PDG_CUDA_TRY(cudaMemsetAsync(c->counter, 0, sizeof(unsigned long long), c->stream));
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int check_rho = (c->prob.flux != PDG_FLUX_LINEAR_ADVECTION && c->prob.nranks == 1) ? 1 : 0;
+    if (c->g.dim == 2)
+        pdg::check_state_kernel<2><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, check_rho,
+                                                                c->counter);
+    else
+        pdg::check_state_kernel<3><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, check_rho,
+                                                                c->counter);
+    pdg_status s = post_launch(c, "check_state");
+    if (s != PDG_OK) return s;
+    unsigned long long h = 0;
+    PDG_CUDA_TRY(cudaMemcpyAsync(&h, c->counter, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *n_bad = (int64_t)h;
+    return PDG_OK;
+}
+
+pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, double *g, double *beta)
+{
+    if (!c || !M || !g || !beta) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
+    if (axis < 0 || axis >= c->g.dim) return fail(PDG_E_INVALID_ARGUMENT, "bad axis");
+    pdg::CellBlock cb;
+    const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)c->g.h[axis];
+    if (!pdg::cell_block(c->g.p, kappa, &cb)) return fail(PDG_E_INVALID_ARGUMENT, "singular block");
+    for (int i = 0; i < cb.n * cb.n; ++i) M[i] = cb.M[i];
+    for (int i = 0; i < cb.n; ++i) g[i] = cb.g[i];
+    *beta = cb.beta;
+    return PDG_OK;
+}
+
+pdg_status pdg_synchronize(pdg_ctx *c)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return PDG_OK;
+}
+
+void pdg_destroy(pdg_ctx *c)
+{
+    if (!c) return;
+    c->comm.destroy();
+    for (auto &e : c->prof.ev)
+        if (e) cudaEventDestroy(e);
+    delete c;
+}
+
+pdg_status pdg_nccl_unique_id(void *out)
+{
+    if (!out) return fail(PDG_E_INVALID_ARGUMENT, "out is NULL");
+    std::string err;
+    if (!pdg::NcclComm::unique_id(out, &err)) return fail(PDG_E_NCCL, err);
+    return PDG_OK;
+}
+
+pdg_status pdg_profile_read(pdg_ctx *c, double *ms, int64_t *launches, double *alg_bytes)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    double t[PDG_NUM_KERNEL_KINDS] = {0}, b[PDG_NUM_KERNEL_KINDS] = {0};
+    int64_t n[PDG_NUM_KERNEL_KINDS] = {0};
+    PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (const ProfRec &r : c->prof.recs) {
+        float e = 0.f;
+        PDG_CUDA_TRY(cudaEventElapsedTime(&e, c->prof.ev[r.ev], c->prof.ev[r.ev + 1]));
+        t[r.kind] += e;
+        b[r.kind] += r.bytes;
+        n[r.kind] += 1;
+    }
+    c->prof.recs.clear();
+    c->prof.next = 0;
+    for (int k = 0; k < PDG_NUM_KERNEL_KINDS; ++k) {
+        if (ms) ms[k] = t[k];
+        if (launches) launches[k] = n[k];
+        if (alg_bytes) alg_bytes[k] = b[k];
+    }
+    return PDG_OK;
+}
+
+const char *pdg_status_string(pdg_status s)
+{
+    switch (s) {
+    case PDG_OK: return "PDG_OK";
+    case PDG_E_INVALID_ARGUMENT: return "PDG_E_INVALID_ARGUMENT";
+    case PDG_E_DIMENSION: return "PDG_E_DIMENSION";
+    case PDG_E_DEGREE: return "PDG_E_DEGREE";
+    case PDG_E_VELOCITY_SET: return "PDG_E_VELOCITY_SET";
+    case PDG_E_FLUX_MODEL: return "PDG_E_FLUX_MODEL";
+    case PDG_E_STATE_NOT_SET: return "PDG_E_STATE_NOT_SET";
+    case PDG_E_NONPHYSICAL: return "PDG_E_NONPHYSICAL";
+    case PDG_E_CUDA: return "PDG_E_CUDA";
+    case PDG_E_NCCL: return "PDG_E_NCCL";
+    case PDG_E_BUFFER: return "PDG_E_BUFFER";
+    case PDG_E_UNSUPPORTED: return "PDG_E_UNSUPPORTED";
+    }
+    return "PDG_E_UNKNOWN";
+}
+
+const char *pdg_last_error(void) { return g_last_error.c_str(); }
+
+const char *pdg_version(void) { return "pdg-b200 " PDG_VERSION " sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,433 @@
+// sm_100a kernels of the PDG hot path (arxiv 1702.00169).  See DESIGN.md for the
+// roofline of each kernel and the data layout.
+//
+//  * sweep_strided_kernel : T2(dt') for velocities along a
+//    non-contiguous axis (y, z).  One thread owns one node line along the velocity
+//    axis and walks it downwind carrying the scalar upwind trace s (register carry);
+//    consecutive threads own consecutive X columns -> 256-byte coalesced warp
+//    accesses.  Loads of future cells do not depend on the carry and are software-
+//    prefetched PF cells ahead.
+//  * sweep_x_kernel : T2(dt') for velocities along the contiguous axis x.  One warp
+//    owns one line; lanes are 32 consecutive cells of a chunk staged through shared
+//    memory with coalesced loads.  The carry recurrence s_l = a_l + beta s_{l-1} is
+//    solved by a 5-step warp-shuffle affine scan; lane 31 chains chunks.
+//  * relax_kernel : collision C2 fused with the moment reduction: per
+//    node read the n_v SoA streams, w = P f, q(w), f^eq, f <- ca f + cb f^eq.
+//  * NPASS = 2 variants apply T2 twice in one pass over memory (step n's trailing
+//    and step n+1's leading T2(dt/2): two sweeps, identical arithmetic, not the
+//    collapsed scheme of P:1173-1177).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pdg {
+
+constexpr int kMaxVel = 32;
+
+struct DevBlock {
+    double M[16];
+    double g[4];
+};
+
+struct SweepVel {
+    int64_t f_off;    // element offset of this velocity's node grid in f
+    int64_t fb_off;   // element offset of its inflow plane in fb
+    int64_t inner;    // element stride along the velocity axis
+    int64_t nlines;   // lines along the axis
+    int32_t ncells;   // cells along the axis
+    int32_t sign;     // +1: walk upward, -1: walk downward
+    int32_t axis;
+    int32_t vel;      // global velocity index
+};
+
+struct SweepParams {
+    double *f;
+    const double *fb;
+    DevBlock blk[3];  // per axis (kappa_k = lambda dt' / h_k)
+    int32_t nvel;
+    SweepVel v[kMaxVel];
+};
+
+enum { MODEL_ADV = 0, MODEL_EULER = 1, MODEL_ISO = 2 };
+
+struct ModelParams {
+    double a[3];      // advection speeds
+    double gamma;     // Euler
+    double c2;        // isothermal c^2
+    double inv2D;     // 1/(2D)
+    double inv2lam;   // 1/(2 lambda)
+};
+
+template <int DIM, int MODEL>
+struct Model;
+
+template <int DIM>
+struct Model<DIM, MODEL_ADV> {
+    static constexpr int M = 1;
+    __device__ __forceinline__ static void flux(const double *w, double (&q)[DIM][M], const ModelParams &P)
+    {
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) q[k][0] = P.a[k] * w[0];
+    }
+    __device__ __forceinline__ static double density(const double *w) { return 1.0; }
+};
+
+template <int DIM>
+struct Model<DIM, MODEL_EULER> {
+    static constexpr int M = DIM + 2;
+    __device__ __forceinline__ static void flux(const double *w, double (&q)[DIM][M], const ModelParams &P)
+    {
+        const double rho = w[0];
+        const double inv = 1.0 / rho;
+        double u[DIM];
+        double ke = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+            u[d] = w[1 + d] * inv;
+            ke += w[1 + d] * u[d];
+        }
+        const double E = w[DIM + 1];
+        const double p = (P.gamma - 1.0) * (E - 0.5 * ke);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            q[k][0] = w[1 + k];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) q[k][1 + d] = w[1 + k] * u[d] + (d == k ? p : 0.0);
+            q[k][DIM + 1] = (E + p) * u[k];
+        }
+    }
+    __device__ __forceinline__ static double density(const double *w) { return w[0]; }
+};
+
+template <int DIM>
+struct Model<DIM, MODEL_ISO> {
+    static constexpr int M = DIM + 1;
+    __device__ __forceinline__ static void flux(const double *w, double (&q)[DIM][M], const ModelParams &P)
+    {
+        const double rho = w[0];
+        const double inv = 1.0 / rho;
+        double u[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) u[d] = w[1 + d] * inv;
+        const double prs = P.c2 * rho;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            q[k][0] = w[1 + k];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) q[k][1 + d] = w[1 + k] * u[d] + (d == k ? prs : 0.0);
+        }
+    }
+    __device__ __forceinline__ static double density(const double *w) { return w[0]; }
+};
+
+// f^eq of velocity i = c*2D + 2k + s (reading C6): w_c/(2D) +- q^k_c/(2 lambda)
+template <int DIM, int M>
+__device__ __forceinline__ double feq_of(int i, const double *w, const double (&q)[DIM][M], const ModelParams &P)
+{
+    const int c = i / (2 * DIM);
+    const int k = (i % (2 * DIM)) >> 1;
+    const double sq = (i & 1) ? -q[k][c] : q[k][c];
+    return fma(sq, P.inv2lam, w[c] * P.inv2D);
+}
+
+// ---------------------------------------------------------------------------
+// T2 sweep along a strided axis (y or z): thread per line, register carry.
+// ---------------------------------------------------------------------------
+template <int N, int NPASS, int PF>
+__global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
+{
+    const SweepVel V = P.v[blockIdx.y];
+    const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= V.nlines) return;
+    const int64_t Lk = (int64_t)V.ncells * N;
+    const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
+    const int64_t step = (V.sign > 0) ? V.inner : -V.inner;
+    double *p = P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+
+    double M[N * N], g[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
+
+    double carry[NPASS];
+    const double s0 = 2.0 * P.fb[V.fb_off + line];  // ghost cell: f^b old + f^b new (reading C5)
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+
+    // ring of PF prefetched cells (values in flow order)
+    double ring[PF][N];
+#pragma unroll
+    for (int k = 0; k < PF; ++k)
+        if (k < V.ncells) {
+#pragma unroll
+            for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(p + (int64_t)(k * N + a) * step);
+        }
+
+    for (int c0 = 0; c0 < V.ncells; c0 += PF) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int c = c0 + k;
+            if (c < V.ncells) {
+                double fo[N];
+#pragma unroll
+                for (int a = 0; a < N; ++a) fo[a] = ring[k][a];
+                const int cn = c + PF;
+                if (cn < V.ncells) {
+#pragma unroll
+                    for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(p + ((int64_t)cn * N + a) * step);
+                }
+#pragma unroll
+                for (int q = 0; q < NPASS; ++q) {
+                    double fn[N];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        double acc = g[a] * carry[q];
+#pragma unroll
+                        for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
+                        fn[a] = acc;
+                    }
+                    carry[q] = fo[N - 1] + fn[N - 1];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) fo[a] = fn[a];
+                }
+#pragma unroll
+                for (int a = 0; a < N; ++a) __stcs(p + ((int64_t)c * N + a) * step, fo[a]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// T2 sweep along x (contiguous): warp per line, lanes = cells, affine warp scan.
+// ---------------------------------------------------------------------------
+constexpr int kXsWarps = 8;
+
+template <int N, int NPASS>
+__global__ void __launch_bounds__(kXsWarps * 32) sweep_x_kernel(const SweepParams P)
+{
+    constexpr int S = (N % 2) ? N : N + 1;  // odd smem stride: conflict-free 8-byte lane reads
+    __shared__ double sbuf[kXsWarps][32 * S];
+    const SweepVel V = P.v[blockIdx.y];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t line = (int64_t)blockIdx.x * kXsWarps + warp;
+    if (line >= V.nlines) return;  // warp-uniform
+    double *row = P.f + V.f_off + line * (int64_t)V.ncells * N;
+    double *buf = sbuf[warp];
+    const unsigned FULL = 0xffffffffu;
+
+    double M[N * N], g[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[0].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[0].g[i];
+    const double beta = g[N - 1];
+
+    double carry[NPASS];
+    const double s0 = 2.0 * P.fb[V.fb_off + line];
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+
+    const int nchunks = (V.ncells + 31) >> 5;
+    const bool up = V.sign > 0;
+    const int pos = up ? lane : 31 - lane;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int region = up ? ch * 32 : V.ncells - 32 * (ch + 1);
+#pragma unroll
+        for (int t = lane; t < 32 * N; t += 32) {
+            const int co = t / N, a = t - co * N;
+            const int cell = region + co;
+            if (cell >= 0 && cell < V.ncells) buf[co * S + a] = __ldcs(row + (int64_t)cell * N + a);
+        }
+        __syncwarp();
+        const int mycell = region + pos;
+        const bool valid = mycell >= 0 && mycell < V.ncells;
+        double fo[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) fo[a] = valid ? buf[pos * S + (up ? a : N - 1 - a)] : 0.0;
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) {
+            double f0[N];
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+                double acc = 0.0;
+#pragma unroll
+                for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
+                f0[a] = acc;
+            }
+            double A = valid ? fo[N - 1] + f0[N - 1] : 0.0;
+            double B = valid ? beta : 1.0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double Ap = __shfl_up_sync(FULL, A, off);
+                const double Bp = __shfl_up_sync(FULL, B, off);
+                if (lane >= off) {
+                    A = fma(B, Ap, A);
+                    B *= Bp;
+                }
+            }
+            const double s_incl = fma(B, carry[q], A);
+            double s_prev = __shfl_up_sync(FULL, s_incl, 1);
+            if (lane == 0) s_prev = carry[q];
+#pragma unroll
+            for (int a = 0; a < N; ++a) fo[a] = fma(g[a], s_prev, f0[a]);
+            carry[q] = __shfl_sync(FULL, s_incl, 31);
+        }
+        if (valid) {
+#pragma unroll
+            for (int a = 0; a < N; ++a) buf[pos * S + (up ? a : N - 1 - a)] = fo[a];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = lane; t < 32 * N; t += 32) {
+            const int co = t / N, a = t - co * N;
+            const int cell = region + co;
+            if (cell >= 0 && cell < V.ncells) __stcs(row + (int64_t)cell * N + a, buf[co * S + a]);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Relaxation fused with the moment reduction (G = 1): all n_v velocities local.
+// ---------------------------------------------------------------------------
+template <int DIM, int MODEL>
+__global__ void __launch_bounds__(256) relax_kernel(double *__restrict__ f, int64_t nnodes, ModelParams P,
+                                                    double ca, double cb)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
+        double w[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            double s = fv[c * 2 * DIM];
+#pragma unroll
+            for (int j = 1; j < 2 * DIM; ++j) s += fv[c * 2 * DIM + j];
+            w[c] = s;
+        }
+        double q[DIM][M];
+        Md::flux(w, q, P);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const double feq = feq_of<DIM, M>(i, w, q, P);
+            __stcs(f + (int64_t)i * nnodes + x, fma(cb, feq, ca * fv[i]));
+        }
+    }
+}
+
+// Partial moments of the local velocity block [v0, v0 + nvl): w_c = sum of local f_i in c.
+template <int DIM, int M>
+__global__ void __launch_bounds__(256) partial_moments_kernel(const double *__restrict__ f, double *__restrict__ w,
+                                                              int64_t nnodes, int v0, int nvl)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double acc[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[c] = 0.0;
+        for (int j = 0; j < nvl; ++j) {
+            const int c = (v0 + j) / (2 * DIM);
+            const double v = f[(int64_t)j * nnodes + x];
+#pragma unroll
+            for (int cc = 0; cc < M; ++cc)
+                if (cc == c) acc[cc] += v;
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) w[(int64_t)c * nnodes + x] = acc[c];
+    }
+}
+
+// Collision of the local velocities from reduced moments w (sharded path, row a4).
+template <int DIM, int MODEL>
+__global__ void __launch_bounds__(256) relax_from_w_kernel(double *__restrict__ f, const double *__restrict__ w,
+                                                           int64_t nnodes, int v0, int nvl, ModelParams P,
+                                                           double ca, double cb)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double wl[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) wl[c] = w[(int64_t)c * nnodes + x];
+        double q[DIM][M];
+        Md::flux(wl, q, P);
+        for (int j = 0; j < nvl; ++j) {
+            const double feq = feq_of<DIM, M>(v0 + j, wl, q, P);
+            double *fi = f + (int64_t)j * nnodes + x;
+            *fi = fma(cb, feq, ca * *fi);
+        }
+    }
+}
+
+// f_i = f^eq_i(w) at every node for the local velocities.
+template <int DIM, int MODEL>
+__global__ void __launch_bounds__(256) equilibrium_kernel(double *__restrict__ f, const double *__restrict__ w,
+                                                          int64_t nnodes, int v0, int nvl, ModelParams P)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double wl[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) wl[c] = w[(int64_t)c * nnodes + x];
+        double q[DIM][M];
+        Md::flux(wl, q, P);
+        for (int j = 0; j < nvl; ++j) f[(int64_t)j * nnodes + x] = feq_of<DIM, M>(v0 + j, wl, q, P);
+    }
+}
+
+// fb_i = f^eq_i(wb) on the inflow plane of each local velocity (line enumeration of the sweeps:
+// plane index == line index, the inflow node is the first node of the line in flow order).
+template <int DIM, int MODEL>
+__global__ void __launch_bounds__(256) inflow_equilibrium_kernel(double *__restrict__ fb, const double *__restrict__ wb,
+                                                                 int64_t nnodes, const SweepParams S, int n,
+                                                                 ModelParams P)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    const SweepVel V = S.v[blockIdx.y];
+    const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= V.nlines) return;
+    const int64_t Lk = (int64_t)V.ncells * n;
+    const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
+    const int64_t node = base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    double wl[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) wl[c] = wb[(int64_t)c * nnodes + node];
+    double q[DIM][M];
+    Md::flux(wl, q, P);
+    fb[V.fb_off + line] = feq_of<DIM, M>(V.vel, wl, q, P);
+}
+
+// Count nodes with rho <= 0 (component-0 block sum) or a non-finite local f.
+template <int DIM>
+__global__ void __launch_bounds__(256) check_state_kernel(const double *__restrict__ f, int64_t nnodes, int v0,
+                                                          int nvl, int check_rho, unsigned long long *count)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long bad = 0;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double rho = 0.0;
+        bool ok = true;
+        for (int j = 0; j < nvl; ++j) {
+            const double v = f[(int64_t)j * nnodes + x];
+            ok = ok && isfinite(v);
+            if (v0 + j < 2 * DIM) rho += v;
+        }
+        if (check_rho && !(rho > 0.0)) ok = false;
+        bad += ok ? 0 : 1;
+    }
+    for (int off = 16; off > 0; off >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, off);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
+}  // namespace pdg

@@ -1,0 +1,132 @@
+// Host-side tables of the B200 sweep: the 1-D Gauss-Lobatto upwind-DG cell block.
+//
+// For an axis-aligned velocity v = +-lambda e_k the (p+1)^D x (p+1)^D local block of
+// eq. DG_reduit is I (x) B_1D (reading C18), so the implicit CN solve of
+// a cell factors into independent 1-D solves along the velocity axis.
+// With the n = p+1 nodes of a line ordered in the flow direction and
+// kappa = lambda * dt' / h (theta = dt'/2, eq transport_cn; reading C1):
+//
+//   G  = W^{-1} (D^T W - e_out e_out^T),   D_ab = l_b'(x_a), W = diag(omega)
+//   A  = I - kappa G
+//   f_new = M f_old + g s_in,  M = A^{-1}(I + kappa G),  g = A^{-1} (kappa/omega_0) e_in
+//   s_out = f_old[n-1] + f_new[n-1]      (upwind trace, old + new: reading C4)
+//
+// and the carry obeys s_out = a + beta s_in with beta = g[n-1].  The paper refactorises
+// a KLU system per step; dt and v are constant, so one precomputed block
+// per (axis, dt') is the same linear algebra.
+//
+// Computed in long double and rounded once to double.  Independent of oracle/.
+#pragma once
+#include <cmath>
+#include <cstring>
+
+namespace pdg {
+
+constexpr int kMaxN = 4;  // p <= 3
+
+struct CellBlock {
+    double M[kMaxN * kMaxN];
+    double g[kMaxN];
+    double beta;
+    int n;
+};
+
+// Gauss-Lobatto nodes / weights on [-1, 1] for p = 1..3.
+inline bool gl_nodes(int p, long double *x, long double *w)
+{
+    if (p == 1) {
+        x[0] = -1.0L; x[1] = 1.0L;
+        w[0] = 1.0L; w[1] = 1.0L;
+        return true;
+    }
+    if (p == 2) {
+        x[0] = -1.0L; x[1] = 0.0L; x[2] = 1.0L;
+        w[0] = 1.0L / 3.0L; w[1] = 4.0L / 3.0L; w[2] = 1.0L / 3.0L;
+        return true;
+    }
+    if (p == 3) {
+        const long double r = 1.0L / sqrtl(5.0L);
+        x[0] = -1.0L; x[1] = -r; x[2] = r; x[3] = 1.0L;
+        w[0] = 1.0L / 6.0L; w[1] = 5.0L / 6.0L; w[2] = 5.0L / 6.0L; w[3] = 1.0L / 6.0L;
+        return true;
+    }
+    return false;
+}
+
+// Lagrange derivative matrix D_ab = l_b'(x_a) in barycentric form.
+inline void lagrange_derivative(int n, const long double *x, long double *D)
+{
+    long double bw[kMaxN];
+    for (int b = 0; b < n; ++b) {
+        long double prod = 1.0L;
+        for (int j = 0; j < n; ++j)
+            if (j != b) prod *= (x[b] - x[j]);
+        bw[b] = 1.0L / prod;
+    }
+    for (int a = 0; a < n; ++a) {
+        long double diag = 0.0L;
+        for (int b = 0; b < n; ++b) {
+            if (b == a) continue;
+            D[a * n + b] = (bw[b] / bw[a]) / (x[a] - x[b]);
+            diag -= D[a * n + b];
+        }
+        D[a * n + a] = diag;
+    }
+}
+
+// Gauss-Jordan inverse with partial pivoting; false if singular.
+inline bool invert(int n, const long double *A, long double *Ainv)
+{
+    long double T[kMaxN][2 * kMaxN];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < 2 * n; ++j) T[i][j] = (j < n) ? A[i * n + j] : ((j - n == i) ? 1.0L : 0.0L);
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r)
+            if (fabsl(T[r][c]) > fabsl(T[piv][c])) piv = r;
+        if (T[piv][c] == 0.0L) return false;
+        if (piv != c)
+            for (int j = 0; j < 2 * n; ++j) { long double t = T[c][j]; T[c][j] = T[piv][j]; T[piv][j] = t; }
+        const long double d = T[c][c];
+        for (int j = 0; j < 2 * n; ++j) T[c][j] /= d;
+        for (int r = 0; r < n; ++r) {
+            if (r == c || T[r][c] == 0.0L) continue;
+            const long double fac = T[r][c];
+            for (int j = 0; j < 2 * n; ++j) T[r][j] -= fac * T[c][j];
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) Ainv[i * n + j] = T[i][n + j];
+    return true;
+}
+
+// The cell block for degree p and CN parameter kappa (any sign).
+inline bool cell_block(int p, long double kappa, CellBlock *out)
+{
+    long double x[kMaxN], w[kMaxN], D[kMaxN * kMaxN], G[kMaxN * kMaxN], A[kMaxN * kMaxN], Ai[kMaxN * kMaxN];
+    if (!gl_nodes(p, x, w)) return false;
+    const int n = p + 1;
+    lagrange_derivative(n, x, D);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            long double v = D[j * n + i] * w[j];                // (D^T W)_ij
+            if (i == n - 1 && j == n - 1) v -= 1.0L;            // - e_out e_out^T
+            G[i * n + j] = v / w[i];                            // W^{-1} (...)
+            A[i * n + j] = ((i == j) ? 1.0L : 0.0L) - kappa * G[i * n + j];
+        }
+    if (!invert(n, A, Ai)) return false;
+    std::memset(out, 0, sizeof(*out));
+    out->n = n;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            long double acc = 0.0L;  // A^{-1} (I + kappa G)
+            for (int k = 0; k < n; ++k) acc += Ai[i * n + k] * (((k == j) ? 1.0L : 0.0L) + kappa * G[k * n + j]);
+            out->M[i * n + j] = (double)acc;
+        }
+        out->g[i] = (double)(Ai[i * n + 0] * kappa / w[0]);
+    }
+    out->beta = out->g[n - 1];
+    return true;
+}
+
+}  // namespace pdg

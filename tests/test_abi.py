@@ -1,0 +1,88 @@
+"""CPU checks of the boundary: the library loads, exports every symbol declared in
+include/pdg.h, and validates problem statements host-side (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1702_00169_b200 import pdg
+from pdg_inputs import CONFIGS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "pdg.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pdg_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported():
+    lib = pdg.load()
+    names = declared_symbols()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(pdg.EXPORTED)
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in pdg.version()
+    assert pdg.status_string(pdg.PDG_E_VELOCITY_SET) == "PDG_E_VELOCITY_SET"
+
+
+@pytest.mark.parametrize("key", [1, 2, 3, 4, 5])
+def test_query_sizes_configs(key):
+    cfg = CONFIGS[key]
+    s = pdg.query_sizes(pdg.problem_from_config(cfg))
+    assert s.nnodes == cfg.nnodes
+    assert s.f_elems == cfg.nv * cfg.nnodes
+    assert s.w_elems == cfg.m * cfg.nnodes
+    assert s.plane_stride == (cfg.N * cfg.n) ** (cfg.dim - 1)
+    assert s.nv_local == cfg.nv and s.v_begin == 0
+
+
+def test_query_sizes_sharded():
+    cfg = CONFIGS[5]
+    for G in (2, 4, 8):
+        for r in range(G):
+            s = pdg.query_sizes(pdg.problem_from_config(cfg, rank=r, nranks=G))
+            assert s.nv_local == 24 // G and s.v_begin == r * (24 // G)
+            assert s.f_elems == (24 // G) * cfg.nnodes
+
+
+def _bad(cfg, **over):
+    vel, comp = cfg.velocities()
+    kw = dict(dim=cfg.dim, ncell=cfg.N, degree=cfg.p, m=cfg.m, vel=vel, comp=comp, lam=cfg.lam, flux=cfg.flux,
+              flux_params=list(cfg.fparams), dt=cfg.dt)
+    kw.update(over)
+    with pytest.raises(pdg.PdgError) as e:
+        pdg.query_sizes(pdg.make_problem(**kw))
+    return e.value.status
+
+
+def test_validation_errors():
+    cfg = CONFIGS[3]
+    assert _bad(cfg, dim=4) == pdg.PDG_E_DIMENSION
+    assert _bad(cfg, degree=5) == pdg.PDG_E_DEGREE
+    assert _bad(cfg, lam=-1.0) == pdg.PDG_E_INVALID_ARGUMENT
+    assert _bad(cfg, dt=0.0) == pdg.PDG_E_INVALID_ARGUMENT
+    assert _bad(cfg, m=3) == pdg.PDG_E_FLUX_MODEL
+    assert _bad(cfg, flux=7) == pdg.PDG_E_FLUX_MODEL
+    vel, comp = cfg.velocities()
+    vel2 = [list(v) for v in vel]
+    vel2[3][1] = 1.0  # not axis-aligned
+    assert _bad(cfg, vel=vel2) == pdg.PDG_E_VELOCITY_SET
+    comp2 = list(comp)
+    comp2[0] = 1
+    assert _bad(cfg, comp=comp2) == pdg.PDG_E_VELOCITY_SET
+    assert _bad(cfg, ncell=0) == pdg.PDG_E_INVALID_ARGUMENT
+
+
+def test_solver_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        pdg.Solver(pdg.problem_from_config(CONFIGS[1]))

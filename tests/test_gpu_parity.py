@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: relative max-norm (reading C17) <= 1e-12 for the palindromic step (north
+star), <= 1e-13 for a single transport / collision operator.  Sizes span
+several x-chunks (32 cells), ragged tails and every axis/sign; full config
+sizes are checked on sampled cells through dependency cones
+(test_gpu_fullsize.py).
+"""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from pdg_inputs import CONFIGS, random_state, w0_grid, wb_grid
+from gpu_helpers import (full_grid_to_planes, make_solver, oracle_problem, planes_to_full_grid, rel_maxnorm,
+                               to_dev, to_np)
+
+pytestmark = pytest.mark.gpu
+
+TOL_OP = 1e-13
+TOL_STEP = 1e-12
+
+
+def random_inputs(cfg, seed, scale=0.5):
+    f = random_state(cfg, seed, scale).numpy()
+    rng = np.random.default_rng(seed + 1)
+    fb_full = planes_to_full_grid(cfg, rng.random((cfg.nv, (cfg.N * cfg.n) ** (cfg.dim - 1))) / cfg.nv)
+    return f, fb_full
+
+
+def gpu_with_state(cfg, f, fb_full, **kw):
+    S = make_solver(cfg, **kw)
+    planes = full_grid_to_planes(cfg, fb_full, S.sizes.plane_stride)
+    S.set_state(to_dev(f), to_dev(planes))
+    return S
+
+
+def small_cases():
+    return [
+        CONFIGS[1],                                   # 8x8, p=2, advection
+        CONFIGS[1].resized(37, name="adv37"),         # 2 x-chunks + ragged tail
+        CONFIGS[2].resized(40, name="euler40"),       # Euler, ragged 40 = 32 + 8
+        CONFIGS[3].resized(5, name="iso5"),           # 3-D, p=2
+        CONFIGS[4].resized(4, name="iso4p3"),         # 3-D, p=3, kappa=2
+        replace(CONFIGS[3].resized(3), p=1, name="iso3p1"),  # p=1
+    ]
+
+
+# --------------------------------------------------------------------------
+# Cell block (setup of row a5) against the oracle's single-cell solve
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("p,kappa", [(1, 0.25), (2, 0.125), (2, 1.0), (3, 2.0), (3, -0.5), (2, 7.0)])
+def test_cell_block_matches_oracle(p, kappa):
+    cfg = replace(CONFIGS[3].resized(2), p=p)
+    S = make_solver(cfg)
+    dtp = kappa * cfg.h / cfg.lam
+    M, g, beta = S.cell_block(0, dtp)
+    pb = O.Problem(1, 1, p, [[1.0, 0, 0]], [0], 1, 1.0, 0, [1.0], dt=1.0)
+    n = p + 1
+    Mo = np.zeros((n, n))
+    for j in range(n):
+        f = np.zeros((1, n))
+        f[0, j] = 1.0
+        O.t2_velocity(pb, pb.vel[0], kappa, f, np.zeros((1, n)))
+        Mo[:, j] = f[0]
+    f = np.zeros((1, n))
+    O.t2_velocity(pb, pb.vel[0], kappa, f, np.full((1, n), 0.5))
+    assert rel_maxnorm(np.array(M), Mo) < 1e-14
+    assert rel_maxnorm(np.array(g), f[0]) < 1e-14
+    assert abs(beta - f[0][-1]) < 1e-15
+
+
+# --------------------------------------------------------------------------
+# Row a1/a3: one transport operator T2(dt') on every velocity
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("npass_dt", [0.5, -0.05, 1.3])
+def test_transport_parity(case, npass_dt):
+    cfg = small_cases()[case]
+    f, fb_full = random_inputs(cfg, 100 + case)
+    dtp = npass_dt * cfg.dt
+    S = gpu_with_state(cfg, f, fb_full)
+    S.transport(dtp)
+    got = to_np(S.get_state(), f.shape)
+    pb = oracle_problem(cfg)
+    fc = pb.grid_to_cells(f)
+    O.t2_all(pb, dtp, fc, pb.grid_to_cells(fb_full))
+    assert rel_maxnorm(got, pb.cells_to_grid(fc)) < TOL_OP
+
+
+# --------------------------------------------------------------------------
+# Row a2: collision fused with moments, every model, tau = 0 and tau > 0
+# --------------------------------------------------------------------------
+MODEL_CASES = [
+    ("adv2", CONFIGS[1]), ("euler2", CONFIGS[2].resized(6)), ("iso3", CONFIGS[3].resized(3)),
+    ("adv3", replace(CONFIGS[3].resized(3), m=1, flux=0, fparams=(1.0, -0.5, 0.25))),
+    ("euler3", replace(CONFIGS[3].resized(3), m=5, flux=1, fparams=(1.4,))),
+    ("iso2", replace(CONFIGS[2].resized(6), m=3, flux=2, fparams=(0.7,))),
+]
+
+
+@pytest.mark.parametrize("name,cfg", MODEL_CASES)
+@pytest.mark.parametrize("tau", [0.0, 0.01])
+def test_collision_parity(name, cfg, tau):
+    f, fb_full = random_inputs(cfg, 7)
+    S = gpu_with_state(cfg, f, fb_full, tau=tau)
+    S.collide(cfg.dt)
+    got = to_np(S.get_state(), f.shape)
+    pb = oracle_problem(cfg, tau=tau)
+    ref = np.ascontiguousarray(f.copy())
+    O.collide(pb, ref, cfg.dt, tau=tau)
+    assert rel_maxnorm(got, ref) < TOL_OP
+    w = to_np(S.moments(), (cfg.m,) + cfg.grid_shape)
+    assert rel_maxnorm(w, O.moments(pb, ref)) < TOL_OP
+
+
+# --------------------------------------------------------------------------
+# Equilibrium initialisation (readings C12, C13)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("key", [1, 2, 3])
+@pytest.mark.parametrize("host", [True, False])
+def test_set_equilibrium_parity(key, host):
+    cfg = CONFIGS[key] if key == 1 else CONFIGS[key].resized(6)
+    w0 = w0_grid(cfg)
+    wb = wb_grid(cfg, w0)
+    S = make_solver(cfg)
+    if host:
+        S.set_equilibrium(w0.reshape(-1), wb.reshape(-1) if cfg.wb_zero else None)
+    else:
+        S.set_equilibrium(w0.reshape(-1).cuda(), wb.reshape(-1).cuda())
+    pb = oracle_problem(cfg)
+    f0, fbg = O.initial_data(pb, w0.numpy(), wb.numpy())
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), f0) < TOL_OP
+    planes = to_np(S.fb, (cfg.nv, S.sizes.plane_stride))
+    assert rel_maxnorm(planes, full_grid_to_planes(cfg, fbg, S.sizes.plane_stride)) < TOL_OP
+
+
+# --------------------------------------------------------------------------
+# The palindromic step M2 (rows a1-a3 + a5)
+# --------------------------------------------------------------------------
+def seeded_equilibrium(cfg):
+    w0 = w0_grid(cfg)
+    wb = wb_grid(cfg, w0)
+    pb = oracle_problem(cfg)
+    f0, fbg = O.initial_data(pb, w0.numpy(), wb.numpy())
+    return pb, f0, fbg
+
+
+def test_config1_free_running_full():
+    """Config 1 exactly as written: 10 free-running steps, f and w <= 1e-12."""
+    cfg = CONFIGS[1]
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    S.step(cfg.steps)
+    got = to_np(S.get_state(), f0.shape)
+    ref = O.m2_run(pb, f0, fbg, cfg.steps)
+    assert rel_maxnorm(got, ref) < TOL_STEP
+    w = to_np(S.moments(), (cfg.m,) + cfg.grid_shape)
+    assert rel_maxnorm(w, O.moments(pb, ref)) < TOL_STEP
+
+
+@pytest.mark.parametrize("key,N,steps", [(2, 24, 6), (3, 6, 5), (4, 4, 4), (5, 8, 4)])
+def test_m2_resynced_each_step(key, N, steps):
+    """One-step parity re-synced from the oracle's f^n (parity protocol step 1)."""
+    cfg = CONFIGS[key].resized(N)
+    pb, f, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f, fbg)
+    for s in range(steps):
+        ref = O.m2_run(pb, f, fbg, 1)
+        S.set_state(to_dev(f))
+        S.step(1)
+        got = to_np(S.get_state(), f.shape)
+        assert rel_maxnorm(got, ref) < TOL_STEP, s
+        f = ref
+
+
+@pytest.mark.parametrize("key,N,steps", [(2, 20, 10), (3, 6, 8), (4, 4, 6), (5, 8, 6)])
+def test_m2_stabilised_twin_free_running(key, N, steps):
+    """Stabilised twins (lambda = 3.5, same nu) free-running: <= 1e-12 (protocol step 3)."""
+    cfg = CONFIGS[key].resized(N, steps=steps).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    S.step(steps)
+    got = to_np(S.get_state(), f0.shape)
+    ref = O.m2_run(pb, f0, fbg, steps)
+    assert rel_maxnorm(got, ref) < TOL_STEP
+
+
+def test_fused_equals_unfused():
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(6).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    A = gpu_with_state(cfg, f0, fbg)
+    B = gpu_with_state(cfg, f0, fbg, flags=pdg.PDG_NO_FUSION)
+    A.step(5)
+    B.step(5)
+    a = to_np(A.get_state(), f0.shape)
+    b = to_np(B.get_state(), f0.shape)
+    assert rel_maxnorm(a, b) < 1e-14
+
+
+def test_m2kin_scheme():
+    """M2kin = T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) vs oracle composition."""
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[2].resized(12).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg, scheme=pdg.PDG_SCHEME_M2KIN)
+    S.step(3)
+    fc = pb.grid_to_cells(f0)
+    fbc = pb.grid_to_cells(fbg)
+    for _ in range(3):
+        O.t2_all(pb, cfg.dt / 4, fc, fbc)
+        O.collide(pb, fc, cfg.dt / 2)
+        O.t2_all(pb, cfg.dt / 2, fc, fbc)
+        O.collide(pb, fc, cfg.dt / 2)
+        O.t2_all(pb, cfg.dt / 4, fc, fbc)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), pb.cells_to_grid(fc)) < TOL_STEP
+
+
+# --------------------------------------------------------------------------
+# Row a4 on one GPU: sharded collision halves with the reduction done by torch
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_sharded_collision_standin(G):
+    cfg = CONFIGS[3].resized(4)
+    f, fb_full = random_inputs(cfg, 3)
+    nvl = cfg.nv // G
+    shards = []
+    for r in range(G):
+        S = make_solver(cfg, rank=r, nranks=G)
+        assert S.sizes.nv_local == nvl and S.sizes.v_begin == r * nvl
+        planes = full_grid_to_planes(cfg, fb_full[r * nvl:(r + 1) * nvl], S.sizes.plane_stride, v_begin=r * nvl)
+        S.set_state(to_dev(f[r * nvl:(r + 1) * nvl]), to_dev(planes))
+        S.partial_moments()
+        shards.append(S)
+    wsum = sum(S.w for S in shards)
+    for S in shards:
+        S.w.copy_(wsum)
+        S.relax_from_w(cfg.dt)
+    got = np.concatenate([to_np(S.get_state(), (nvl,) + cfg.grid_shape) for S in shards])
+    pb = oracle_problem(cfg)
+    ref = np.ascontiguousarray(f.copy())
+    O.collide(pb, ref, cfg.dt)
+    assert rel_maxnorm(got, ref) < TOL_OP
+    with pytest.raises(Exception):
+        shards[0].collide(cfg.dt)  # no communicator: must fail loudly, not fall back
+
+
+# --------------------------------------------------------------------------
+# Edge cases and error behaviour
+# --------------------------------------------------------------------------
+def test_single_cell_and_zero_steps():
+    cfg = CONFIGS[3].resized(1).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    S.step(0)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), f0) == 0.0
+    S.step(2)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), O.m2_run(pb, f0, fbg, 2)) < TOL_STEP
+
+
+def test_gpu_time_symmetry():
+    """T2(-dt') T2(dt') = I on the GPU path too (eq prop_sym), small nu."""
+    cfg = CONFIGS[2].resized(4)
+    f, fb_full = random_inputs(cfg, 5)
+    S = gpu_with_state(cfg, f, fb_full)
+    S.transport(0.05 * cfg.dt)
+    S.transport(-0.05 * cfg.dt)
+    assert rel_maxnorm(to_np(S.get_state(), f.shape), f) < 1e-12
+
+
+def test_errors_are_reported():
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[1]
+    S = make_solver(cfg)
+    with pytest.raises(pdg.PdgError) as e:
+        S.step(1)
+    assert e.value.status == pdg.PDG_E_STATE_NOT_SET
+    with pytest.raises(pdg.PdgError) as e:
+        S.step(-1)
+    assert e.value.status == pdg.PDG_E_INVALID_ARGUMENT
+
+
+def test_check_state_flags_nonphysical():
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(3)
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    assert S.check_state() == 0
+    bad = f0.copy()
+    bad[0, 0, 0, 0] = np.nan
+    bad[:6, 1, 1, 1] = -1.0
+    S.set_state(to_dev(bad))
+    assert S.check_state() == 2
+    S2 = gpu_with_state(cfg, bad, fbg, flags=pdg.PDG_CHECK_STATE)
+    with pytest.raises(pdg.PdgError) as e:
+        S2.step(1)
+    assert e.value.status == pdg.PDG_E_NONPHYSICAL
+
+
+def test_cuda_graph_capture_of_step():
+    """pdg_step is capturable: replaying the graph equals eager steps."""
+    cfg = CONFIGS[3].resized(6).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        S = gpu_with_state(cfg, f0, fbg)
+        S.set_state(to_dev(f0))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            S.step(2)
+        S.set_state(to_dev(f0))
+        g.replay()
+        g.replay()
+        stream.synchronize()
+    ref = O.m2_run(pb, f0, fbg, 4)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP
