@@ -100,7 +100,8 @@ typedef enum {
     PDG_K_RELAX_W = 4,       /* collision from reduced moments (nranks > 1) */
     PDG_K_ALLREDUCE = 5,     /* NCCL sum of w */
     PDG_K_OTHER = 6,         /* initialisation / checks */
-    PDG_NUM_KERNEL_KINDS = 7
+    PDG_K_RELAX_X = 7,       /* collision fused with moments and the following x-velocity sweep(s) */
+    PDG_NUM_KERNEL_KINDS = 8
 } pdg_kernel_kind;
 
 typedef struct {

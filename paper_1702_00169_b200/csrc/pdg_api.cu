@@ -170,6 +170,7 @@ struct pdg_ctx {
     pdg::NcclComm comm;
     int device = 0;
     Profiler prof;
+    bool yz_pairs = false;  // two columns per thread in the strided sweeps
 };
 
 namespace {
@@ -235,18 +236,25 @@ double sweep_bytes(const pdg_ctx *c, const pdg::SweepParams &sp)
     return b;
 }
 
+enum { SWEEP_ALL = 0, SWEEP_YZ = 1, SWEEP_X = 2 };
+
 template <int N, int NPASS>
-void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParams &yzp)
+void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParams &yzp, int which)
 {
-    if (yzp.nvel > 0) {
+    if (yzp.nvel > 0 && which != SWEEP_X) {
         int64_t maxl = 0;
         for (int i = 0; i < yzp.nvel; ++i) maxl = std::max(maxl, yzp.v[i].nlines);
-        dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
         const int e = prof_begin(c);
-        pdg::sweep_strided_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
+        if (c->yz_pairs) {
+            dim3 grid((unsigned)((maxl / 2 + 255) / 256), (unsigned)yzp.nvel);
+            pdg::sweep_strided2_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
+        } else {
+            dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
+            pdg::sweep_strided_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
+        }
         prof_end(c, e, PDG_K_SWEEP_STRIDED, sweep_bytes(c, yzp));
     }
-    if (xp.nvel > 0) {
+    if (xp.nvel > 0 && which != SWEEP_YZ) {
         int64_t maxl = 0;
         for (int i = 0; i < xp.nvel; ++i) maxl = std::max(maxl, xp.v[i].nlines);
         dim3 grid((unsigned)((maxl + pdg::kXsWarps - 1) / pdg::kXsWarps), (unsigned)xp.nvel);
@@ -256,8 +264,8 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
     }
 }
 
-// One pass over f applying T2(dtp) npass times (npass in {1, 2}).
-pdg_status transport_pass(pdg_ctx *c, double dtp, int npass)
+// One pass over f applying T2(dtp) npass times (npass in {1, 2}) to the selected velocities.
+pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_ALL)
 {
     pdg::SweepParams xp = c->x_params, yzp = c->yz_params;
     pdg::DevBlock blk[3];
@@ -266,15 +274,69 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass)
     std::memcpy(yzp.blk, blk, sizeof(blk));
     const int n = c->g.n;
     if (npass == 1) {
-        if (n == 2) launch_sweeps<2, 1>(c, xp, yzp);
-        else if (n == 3) launch_sweeps<3, 1>(c, xp, yzp);
-        else launch_sweeps<4, 1>(c, xp, yzp);
+        if (n == 2) launch_sweeps<2, 1>(c, xp, yzp, which);
+        else if (n == 3) launch_sweeps<3, 1>(c, xp, yzp, which);
+        else launch_sweeps<4, 1>(c, xp, yzp, which);
     } else {
-        if (n == 2) launch_sweeps<2, 2>(c, xp, yzp);
-        else if (n == 3) launch_sweeps<3, 2>(c, xp, yzp);
-        else launch_sweeps<4, 2>(c, xp, yzp);
+        if (n == 2) launch_sweeps<2, 2>(c, xp, yzp, which);
+        else if (n == 3) launch_sweeps<3, 2>(c, xp, yzp, which);
+        else launch_sweeps<4, 2>(c, xp, yzp, which);
     }
     return post_launch(c, "sweep");
+}
+
+// ---- collision fused with the x-velocity sweeps (nranks == 1) ----------------------------
+int relax_x_K(int ncx)
+{
+    if (ncx <= 64) return 2;
+    if (ncx <= 128) return 4;
+    return 8;
+}
+
+size_t relax_x_smem(const pdg_ctx *c)
+{
+    const int K = relax_x_K((int)c->g.ncell[0]);
+    const int n = c->g.n;
+    const int64_t L = c->g.ncell[0] * n;
+    const int64_t Lp = L + L / (K * n) + 1;
+    return sizeof(double) * (size_t)(2 * c->g.m) * (size_t)Lp;
+}
+
+template <int DIM, int MODEL, int N, int NPASS, int K>
+void launch_relax_x_k(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
+{
+    static bool attr_set = false;
+    auto kern = pdg::relax_xsweep_kernel<DIM, MODEL, N, NPASS, K>;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    const unsigned nlines = (unsigned)(c->g.nnodes / (c->g.ncell[0] * N));
+    kern<<<nlines, 256, smem, c->stream>>>(P);
+}
+
+template <int DIM, int MODEL, int N, int NPASS>
+void launch_relax_x_n(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
+{
+    const int K = relax_x_K(P.ncx);
+    if (K == 2) launch_relax_x_k<DIM, MODEL, N, NPASS, 2>(c, P, smem);
+    else if (K == 4) launch_relax_x_k<DIM, MODEL, N, NPASS, 4>(c, P, smem);
+    else launch_relax_x_k<DIM, MODEL, N, NPASS, 8>(c, P, smem);
+}
+
+template <int DIM, int MODEL>
+void launch_relax_x_t(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem, int npass)
+{
+    const int n = c->g.n;
+    if (npass == 1) {
+        if (n == 2) launch_relax_x_n<DIM, MODEL, 2, 1>(c, P, smem);
+        else if (n == 3) launch_relax_x_n<DIM, MODEL, 3, 1>(c, P, smem);
+        else launch_relax_x_n<DIM, MODEL, 4, 1>(c, P, smem);
+    } else {
+        if (n == 2) launch_relax_x_n<DIM, MODEL, 2, 2>(c, P, smem);
+        else if (n == 3) launch_relax_x_n<DIM, MODEL, 3, 2>(c, P, smem);
+        else launch_relax_x_n<DIM, MODEL, 4, 2>(c, P, smem);
+    }
 }
 
 template <int DIM, int MODEL>
@@ -373,6 +435,38 @@ pdg_status collide(pdg_ctx *c, double dt)
     return post_launch(c, "relax_from_w");
 }
 
+// C2(dt) followed by npass sweeps T2(dtp) of the x-velocities, in one pass over f.
+pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
+{
+    double ca, cb;
+    collision_coeffs(c, dt, &ca, &cb);
+    pdg::DevBlock blk[3];
+    if (!fill_blocks(c, dtp, blk)) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block for this dt");
+    pdg::RelaxXParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.f = c->f;
+    P.fb = c->fb;
+    P.nnodes = c->g.nnodes;
+    P.plane_stride = c->g.plane_stride;
+    P.ncx = (int32_t)c->g.ncell[0];
+    P.blk = blk[0];
+    P.mp = c->mp;
+    P.ca = ca;
+    P.cb = cb;
+    const size_t smem = relax_x_smem(c);
+    const int e = prof_begin(c);
+    PDG_DISPATCH(launch_relax_x_t, c, P, smem, npass);
+    prof_end(c, e, PDG_K_RELAX_X,
+             16.0 * (double)c->g.nvl * (double)c->g.nnodes + 8.0 * (double)c->x_params.nvel * (double)c->x_params.v[0].nlines);
+    return post_launch(c, "relax_xsweep");
+}
+
+bool use_relax_x(const pdg_ctx *c)
+{
+    return c->prob.nranks == 1 && !(c->prob.flags & PDG_NO_FUSION) && relax_x_smem(c) <= 110 * 1024 &&
+           c->g.nnodes / (c->g.ncell[0] * c->g.n) < (int64_t)1 << 31;
+}
+
 void build_sweep_params(pdg_ctx *c)
 {
     const Geometry &g = c->g;
@@ -400,6 +494,10 @@ void build_sweep_params(pdg_ctx *c)
         if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
         else c->yz_params.v[c->yz_params.nvel++] = V;
     }
+    bool pairs = (g.nnodes % 2 == 0) && (g.plane_stride % 2 == 0);
+    for (int i = 0; i < c->yz_params.nvel; ++i)
+        pairs = pairs && (c->yz_params.v[i].inner % 2 == 0) && (c->yz_params.v[i].nlines % 2 == 0);
+    c->yz_pairs = pairs;
 }
 
 bool is_device_pointer(const void *p)
@@ -588,28 +686,46 @@ pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
     const double dt = c->prob.dt;
     const bool fuse = !(c->prob.flags & PDG_NO_FUSION);
     pdg_status s = PDG_OK;
+    const bool fx = use_relax_x(c);
     if (c->prob.scheme == PDG_SCHEME_M2) {
-        // M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
+        // M2(dt) = T2(dt/2) C2(dt) T2(dt/2); the trailing T2(dt/2) of step k and the
+        // leading T2(dt/2) of step k+1 are swept in one pass (two sweeps, no collapse).
         s = transport_pass(c, 0.5 * dt, 1);
         for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
-            s = collide(c, dt);
-            if (s != PDG_OK) break;
-            if (k + 1 < nsteps && fuse) s = transport_pass(c, 0.5 * dt, 2);  // T2(dt/2) then T2(dt/2), one pass
-            else if (k + 1 < nsteps) {
-                s = transport_pass(c, 0.5 * dt, 1);
-                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
-            } else s = transport_pass(c, 0.5 * dt, 1);
+            const bool last = (k + 1 == nsteps);
+            if (fx) {
+                const int np = last ? 1 : 2;
+                s = collide_xsweep(c, dt, 0.5 * dt, np);
+                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, np, SWEEP_YZ);
+            } else {
+                s = collide(c, dt);
+                if (s != PDG_OK) break;
+                if (!last && fuse) s = transport_pass(c, 0.5 * dt, 2);
+                else if (!last) {
+                    s = transport_pass(c, 0.5 * dt, 1);
+                    if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
+                } else s = transport_pass(c, 0.5 * dt, 1);
+            }
         }
     } else {
         // M2kin(dt) = T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4)
         s = transport_pass(c, 0.25 * dt, 1);
         for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
+            const bool last = (k + 1 == nsteps);
+            if (fx) {
+                s = collide_xsweep(c, 0.5 * dt, 0.5 * dt, 1);
+                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1, SWEEP_YZ);
+                const int np = last ? 1 : 2;
+                if (s == PDG_OK) s = collide_xsweep(c, 0.5 * dt, 0.25 * dt, np);
+                if (s == PDG_OK) s = transport_pass(c, 0.25 * dt, np, SWEEP_YZ);
+                continue;
+            }
             s = collide(c, 0.5 * dt);
             if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
             if (s == PDG_OK) s = collide(c, 0.5 * dt);
             if (s != PDG_OK) break;
-            if (k + 1 < nsteps && fuse) s = transport_pass(c, 0.25 * dt, 2);
-            else if (k + 1 < nsteps) {
+            if (!last && fuse) s = transport_pass(c, 0.25 * dt, 2);
+            else if (!last) {
                 s = transport_pass(c, 0.25 * dt, 1);
                 if (s == PDG_OK) s = transport_pass(c, 0.25 * dt, 1);
             } else s = transport_pass(c, 0.25 * dt, 1);

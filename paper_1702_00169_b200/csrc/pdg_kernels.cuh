@@ -199,6 +199,282 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
 }
 
 // ---------------------------------------------------------------------------
+// T2 sweep along a strided axis, two adjacent columns per thread (16-byte accesses).
+// Requires an even stride along the axis, even velocity offsets and even plane offsets.
+// Same arithmetic per column as sweep_strided_kernel; half the instructions per byte.
+// ---------------------------------------------------------------------------
+template <int N, int NPASS, int PF>
+__global__ void __launch_bounds__(256) sweep_strided2_kernel(const SweepParams P)
+{
+    const SweepVel V = P.v[blockIdx.y];
+    const int64_t line = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (line >= V.nlines) return;
+    const int64_t Lk = (int64_t)V.ncells * N;
+    const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
+    const int64_t step = ((V.sign > 0) ? V.inner : -V.inner) >> 1;  // in double2 units
+    const double2 *ld = reinterpret_cast<const double2 *>(P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner));
+    double2 *st = reinterpret_cast<double2 *>(P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner));
+
+    double M[N * N], g[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
+
+    const double2 fbv = *reinterpret_cast<const double2 *>(P.fb + V.fb_off + line);
+    double cx[NPASS], cy[NPASS];
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) {
+        cx[q] = 2.0 * fbv.x;  // ghost: f^b old + f^b new (reading C5)
+        cy[q] = 2.0 * fbv.y;
+    }
+
+    double2 ring[PF][N];
+#pragma unroll
+    for (int k = 0; k < PF; ++k)
+        if (k < V.ncells) {
+#pragma unroll
+            for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(ld + a * step);
+            ld += N * step;
+        }
+
+    for (int c0 = 0; c0 < V.ncells; c0 += PF) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int c = c0 + k;
+            if (c < V.ncells) {
+                double ox[N], oy[N];
+#pragma unroll
+                for (int a = 0; a < N; ++a) {
+                    ox[a] = ring[k][a].x;
+                    oy[a] = ring[k][a].y;
+                }
+                if (c + PF < V.ncells) {
+#pragma unroll
+                    for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(ld + a * step);
+                    ld += N * step;
+                }
+#pragma unroll
+                for (int q = 0; q < NPASS; ++q) {
+                    double nx[N], ny[N];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        double accx = g[a] * cx[q], accy = g[a] * cy[q];
+#pragma unroll
+                        for (int b = 0; b < N; ++b) {
+                            accx = fma(M[a * N + b], ox[b], accx);
+                            accy = fma(M[a * N + b], oy[b], accy);
+                        }
+                        nx[a] = accx;
+                        ny[a] = accy;
+                    }
+                    cx[q] = ox[N - 1] + nx[N - 1];
+                    cy[q] = oy[N - 1] + ny[N - 1];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        ox[a] = nx[a];
+                        oy[a] = ny[a];
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < N; ++a) __stcs(st + a * step, make_double2(ox[a], oy[a]));
+                st += N * step;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp sweep of one line held in shared memory: lane = segment of K consecutive cells
+// (flow order).  Per pass: zero-inflow carry of each segment (s_out = A + B s_in,
+// B = beta^cells), a 5-step warp-shuffle affine scan for the true segment inflows,
+// then the sequential cell recurrence f_new = M f_old + g s with the true inflow.
+// `row` uses padded indexing: element X lives at X + X / (K N).
+// ---------------------------------------------------------------------------
+template <int N, int NPASS, int K>
+__device__ __forceinline__ void warp_line_sweep(double *row, int ncells, bool up, const double (&M)[N * N],
+                                                const double (&g)[N], double s0, int lane)
+{
+    constexpr int SEG = K * N;
+    const unsigned FULL = 0xffffffffu;
+    const double beta = g[N - 1];
+    double carry[NPASS];
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+    for (int sc0 = 0; sc0 < ncells; sc0 += 32 * K) {
+        const int f0 = sc0 + lane * K;
+        const int cnt = max(0, min(K, ncells - f0));
+        double v[K][N];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+            if (kk < cnt) {
+                const int fc = f0 + kk;
+                const int mc = up ? fc : ncells - 1 - fc;
+#pragma unroll
+                for (int a = 0; a < N; ++a) {
+                    const int X = mc * N + (up ? a : N - 1 - a);
+                    v[kk][a] = row[X + X / SEG];
+                }
+            } else {
+#pragma unroll
+                for (int a = 0; a < N; ++a) v[kk][a] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) {
+            double A = 0.0, B = 1.0;  // zero-inflow carry of the segment: s_out = A + B s_in
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                if (kk < cnt) {
+                    double r = v[kk][N - 1];
+#pragma unroll
+                    for (int b = 0; b < N; ++b) r = fma(M[(N - 1) * N + b], v[kk][b], r);
+                    A = fma(beta, A, r);
+                    B *= beta;
+                }
+            }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double Ap = __shfl_up_sync(FULL, A, off);
+                const double Bp = __shfl_up_sync(FULL, B, off);
+                if (lane >= off) {
+                    A = fma(B, Ap, A);
+                    B *= Bp;
+                }
+            }
+            double Ae = __shfl_up_sync(FULL, A, 1);
+            double Be = __shfl_up_sync(FULL, B, 1);
+            if (lane == 0) {
+                Ae = 0.0;
+                Be = 1.0;
+            }
+            double s = fma(Be, carry[q], Ae);
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                if (kk < cnt) {
+                    double fn[N];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        double acc = g[a] * s;
+#pragma unroll
+                        for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], v[kk][b], acc);
+                        fn[a] = acc;
+                    }
+                    s = v[kk][N - 1] + fn[N - 1];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) v[kk][a] = fn[a];
+                }
+            }
+            carry[q] = __shfl_sync(FULL, fma(B, carry[q], A), 31);
+        }
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+            if (kk < cnt) {
+                const int fc = f0 + kk;
+                const int mc = up ? fc : ncells - 1 - fc;
+#pragma unroll
+                for (int a = 0; a < N; ++a) {
+                    const int X = mc * N + (up ? a : N - 1 - a);
+                    row[X + X / SEG] = v[kk][a];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Collision fused with the moment reduction AND the following T2 sweep(s) of the
+// x-velocities (G = 1).  One CTA per x-line (fixed y, z):
+//   phase 1: per node, w = P f, f^eq(w), f <- ca f + cb f^eq for all n_v velocities;
+//            y/z velocities go straight back to HBM, x velocities to shared memory;
+//   phase 2: one warp per x velocity sweeps the line in shared memory (NPASS times);
+//   phase 3: coalesced store of the x velocities.
+// HBM traffic = one read + one write of every value (16 B per node.velocity).
+// ---------------------------------------------------------------------------
+struct RelaxXParams {
+    double *f;
+    const double *fb;
+    int64_t nnodes;
+    int64_t plane_stride;
+    int32_t ncx;  // cells along x
+    DevBlock blk; // x-axis block of the sweeps that follow the collision
+    ModelParams mp;
+    double ca, cb;
+};
+
+template <int N, int K>
+__host__ __device__ constexpr int relax_x_row_len(int ncx)
+{
+    return ncx * N + (ncx * N) / (K * N) + 1;
+}
+
+template <int DIM, int MODEL, int N, int NPASS, int K>
+__global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
+    constexpr int SEG = K * N;
+    extern __shared__ double sx[];
+    const int Lx = P.ncx * N;
+    const int Lp = relax_x_row_len<N, K>(P.ncx);
+    const int64_t line = blockIdx.x;
+    const int64_t base = line * Lx;
+    const int64_t nn = P.nnodes;
+
+    // phase 1: collision at every node of the line
+    for (int X = threadIdx.x; X < Lx; X += blockDim.x) {
+        const double *src = P.f + base + X;
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = __ldcs(src + i * nn);
+        double w[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+            double s = fv[c * 2 * DIM];
+#pragma unroll
+            for (int j = 1; j < 2 * DIM; ++j) s += fv[c * 2 * DIM + j];
+            w[c] = s;
+        }
+        double q[DIM][M];
+        Md::flux(w, q, P.mp);
+        const int xs = X + X / SEG;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const double val = fma(P.cb, feq_of<DIM, M>(i, w, q, P.mp), P.ca * fv[i]);
+            const int c = i / (2 * DIM), k = (i % (2 * DIM)) >> 1, s = i & 1;
+            if (k == 0) sx[(2 * c + s) * Lp + xs] = val;
+            else __stcs(P.f + base + X + i * nn, val);
+        }
+    }
+    __syncthreads();
+
+    // phase 2: T2 sweep(s) of the 2M x-velocities, one warp per velocity
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    double Mb[N * N], gb[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) Mb[i] = P.blk.M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) gb[i] = P.blk.g[i];
+    for (int v = warp; v < 2 * M; v += nwarps) {
+        const int c = v >> 1, s = v & 1;
+        const int i = c * 2 * DIM + s;
+        const double s0 = 2.0 * P.fb[i * P.plane_stride + line];  // ghost: f^b old + new
+        warp_line_sweep<N, NPASS, K>(sx + v * Lp, P.ncx, s == 0, Mb, gb, s0, lane);
+    }
+    __syncthreads();
+
+    // phase 3: store the x-velocities
+    for (int v = 0; v < 2 * M; ++v) {
+        const int c = v >> 1, s = v & 1;
+        const int i = c * 2 * DIM + s;
+        double *dst = P.f + base + i * nn;
+        const double *srow = sx + v * Lp;
+        for (int X = threadIdx.x; X < Lx; X += blockDim.x) __stcs(dst + X, srow[X + X / SEG]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // T2 sweep along x (contiguous): warp per line, lanes = cells, affine warp scan.
 // ---------------------------------------------------------------------------
 constexpr int kXsWarps = 8;

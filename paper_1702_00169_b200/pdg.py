@@ -36,7 +36,8 @@ PDG_CHECK_STATE = 0x1
 PDG_SYNC_ERRORS = 0x2
 PDG_NO_FUSION = 0x4
 PDG_PROFILE = 0x8
-KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other"]
+KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other",
+                "relax_xsweep"]
 
 EXPORTED = [
     "pdg_query_sizes", "pdg_create", "pdg_set_state", "pdg_set_equilibrium", "pdg_get_state", "pdg_step",

@@ -318,3 +318,24 @@ def test_cuda_graph_capture_of_step():
         stream.synchronize()
     ref = O.m2_run(pb, f0, fbg, 4)
     assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP
+
+
+@pytest.mark.parametrize("N", [3, 37, 100, 300])
+def test_m2_fused_relax_xsweep_line_lengths(N):
+    """The fused collision + x-sweep kernel over segment sizes K = 2, 4, 8 and a
+    line longer than one 32K-cell super-chunk (N = 300), ragged tails included."""
+    cfg = CONFIGS[1].resized(N, steps=3)
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    S.step(3)
+    ref = O.m2_run(pb, f0, fbg, 3)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP
+
+
+def test_odd_line_count_uses_scalar_strided_sweep():
+    """p=2 with an odd cell count gives odd node rows: the one-column strided kernel."""
+    cfg = CONFIGS[3].resized(5).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg)
+    S.step(3)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), O.m2_run(pb, f0, fbg, 3)) < TOL_STEP
