@@ -170,7 +170,6 @@ struct pdg_ctx {
     pdg::NcclComm comm;
     int device = 0;
     Profiler prof;
-    bool yz_pairs = false;  // two columns per thread in the strided sweeps
 };
 
 namespace {
@@ -245,13 +244,10 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
         int64_t maxl = 0;
         for (int i = 0; i < yzp.nvel; ++i) maxl = std::max(maxl, yzp.v[i].nlines);
         const int e = prof_begin(c);
-        if (c->yz_pairs) {
-            dim3 grid((unsigned)((maxl / 2 + 255) / 256), (unsigned)yzp.nvel);
-            pdg::sweep_strided2_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
-        } else {
-            dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
-            pdg::sweep_strided_kernel<N, NPASS, 4><<<grid, 256, 0, c->stream>>>(yzp);
-        }
+        // prefetch depth tuned on B200 (tools/microbench_strided.cu): n=3 -> 2, n=4 -> 3 (one sweep) / 1 (two)
+        constexpr int PF = (N == 4) ? (NPASS == 1 ? 3 : 1) : 2;
+        dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
+        pdg::sweep_strided_kernel<N, NPASS, PF><<<grid, 256, 0, c->stream>>>(yzp);
         prof_end(c, e, PDG_K_SWEEP_STRIDED, sweep_bytes(c, yzp));
     }
     if (xp.nvel > 0 && which != SWEEP_YZ) {
@@ -494,10 +490,6 @@ void build_sweep_params(pdg_ctx *c)
         if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
         else c->yz_params.v[c->yz_params.nvel++] = V;
     }
-    bool pairs = (g.nnodes % 2 == 0) && (g.plane_stride % 2 == 0);
-    for (int i = 0; i < c->yz_params.nvel; ++i)
-        pairs = pairs && (c->yz_params.v[i].inner % 2 == 0) && (c->yz_params.v[i].nlines % 2 == 0);
-    c->yz_pairs = pairs;
 }
 
 bool is_device_pointer(const void *p)

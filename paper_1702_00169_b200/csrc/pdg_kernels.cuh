@@ -6,7 +6,8 @@
 //    axis and walks it downwind carrying the scalar upwind trace s (register carry);
 //    consecutive threads own consecutive X columns -> 256-byte coalesced warp
 //    accesses.  Loads of future cells do not depend on the carry and are software-
-//    prefetched PF cells ahead.
+//    prefetched PF cells ahead (PF = 2 for n = 3 measured best on B200: occupancy beats
+//    per-thread depth; tools/microbench_strided.cu).
 //  * sweep_x_kernel : T2(dt') for velocities along the contiguous axis x.  One warp
 //    owns one line; lanes are 32 consecutive cells of a chunk staged through shared
 //    memory with coalesced loads.  The carry recurrence s_l = a_l + beta s_{l-1} is
@@ -193,92 +194,6 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
                 }
 #pragma unroll
                 for (int a = 0; a < N; ++a) __stcs(p + ((int64_t)c * N + a) * step, fo[a]);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// T2 sweep along a strided axis, two adjacent columns per thread (16-byte accesses).
-// Requires an even stride along the axis, even velocity offsets and even plane offsets.
-// Same arithmetic per column as sweep_strided_kernel; half the instructions per byte.
-// ---------------------------------------------------------------------------
-template <int N, int NPASS, int PF>
-__global__ void __launch_bounds__(256) sweep_strided2_kernel(const SweepParams P)
-{
-    const SweepVel V = P.v[blockIdx.y];
-    const int64_t line = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-    if (line >= V.nlines) return;
-    const int64_t Lk = (int64_t)V.ncells * N;
-    const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
-    const int64_t step = ((V.sign > 0) ? V.inner : -V.inner) >> 1;  // in double2 units
-    const double2 *ld = reinterpret_cast<const double2 *>(P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner));
-    double2 *st = reinterpret_cast<double2 *>(P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner));
-
-    double M[N * N], g[N];
-#pragma unroll
-    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
-#pragma unroll
-    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
-
-    const double2 fbv = *reinterpret_cast<const double2 *>(P.fb + V.fb_off + line);
-    double cx[NPASS], cy[NPASS];
-#pragma unroll
-    for (int q = 0; q < NPASS; ++q) {
-        cx[q] = 2.0 * fbv.x;  // ghost: f^b old + f^b new (reading C5)
-        cy[q] = 2.0 * fbv.y;
-    }
-
-    double2 ring[PF][N];
-#pragma unroll
-    for (int k = 0; k < PF; ++k)
-        if (k < V.ncells) {
-#pragma unroll
-            for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(ld + a * step);
-            ld += N * step;
-        }
-
-    for (int c0 = 0; c0 < V.ncells; c0 += PF) {
-#pragma unroll
-        for (int k = 0; k < PF; ++k) {
-            const int c = c0 + k;
-            if (c < V.ncells) {
-                double ox[N], oy[N];
-#pragma unroll
-                for (int a = 0; a < N; ++a) {
-                    ox[a] = ring[k][a].x;
-                    oy[a] = ring[k][a].y;
-                }
-                if (c + PF < V.ncells) {
-#pragma unroll
-                    for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(ld + a * step);
-                    ld += N * step;
-                }
-#pragma unroll
-                for (int q = 0; q < NPASS; ++q) {
-                    double nx[N], ny[N];
-#pragma unroll
-                    for (int a = 0; a < N; ++a) {
-                        double accx = g[a] * cx[q], accy = g[a] * cy[q];
-#pragma unroll
-                        for (int b = 0; b < N; ++b) {
-                            accx = fma(M[a * N + b], ox[b], accx);
-                            accy = fma(M[a * N + b], oy[b], accy);
-                        }
-                        nx[a] = accx;
-                        ny[a] = accy;
-                    }
-                    cx[q] = ox[N - 1] + nx[N - 1];
-                    cy[q] = oy[N - 1] + ny[N - 1];
-#pragma unroll
-                    for (int a = 0; a < N; ++a) {
-                        ox[a] = nx[a];
-                        oy[a] = ny[a];
-                    }
-                }
-#pragma unroll
-                for (int a = 0; a < N; ++a) __stcs(st + a * step, make_double2(ox[a], oy[a]));
-                st += N * step;
             }
         }
     }

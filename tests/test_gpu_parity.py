@@ -332,8 +332,8 @@ def test_m2_fused_relax_xsweep_line_lengths(N):
     assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP
 
 
-def test_odd_line_count_uses_scalar_strided_sweep():
-    """p=2 with an odd cell count gives odd node rows: the one-column strided kernel."""
+def test_odd_line_count():
+    """p=2 with an odd cell count gives odd node rows and odd line counts."""
     cfg = CONFIGS[3].resized(5).stabilised()
     pb, f0, fbg = seeded_equilibrium(cfg)
     S = gpu_with_state(cfg, f0, fbg)
