@@ -50,6 +50,19 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(cfg, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary of this workload."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        if t.get("workload") == cfg.name and kernel in t["kernels"]:
+            return float(t["kernels"][kernel]["dram_bytes_per_launch"]), t.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
 # ----------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ----------------------------------------------------------------------------
@@ -210,6 +223,7 @@ def run_product(args, cfg):
     import torch
     import torch.distributed as dist
 
+    from paper_1702_00169_b200 import dist as pdist
     from paper_1702_00169_b200 import pdg
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -217,19 +231,11 @@ def run_product(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-        idt = torch.zeros(128, dtype=torch.uint8, device=device)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(pdg.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
-        pb = pdg.problem_from_config(cfg, rank=rank, nranks=world, nccl_id=nccl_id, flags=pdg.PDG_PROFILE,
-                                     stream=stream.cuda_stream)
-        S = pdg.Solver(pb, device=device)
+        S = pdist.sharded_solver(cfg, device, flags=pdg.PDG_PROFILE, stream=stream.cuda_stream)
         fill_w0(cfg, S.w, device)
         S.set_equilibrium(S.w)
         S.step(args.warmup)
@@ -251,10 +257,7 @@ def run_product(args, cfg):
         prof = S.profile_read()
         if world > 1:
             dist.barrier()
-        t = torch.tensor([ms], dtype=torch.float64, device=device)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = pdist.max_over_ranks(ms, device=device)
         value = cfg.updates_per_step * args.steps / (ms * 1e-3)
 
         # dominant kernel roofline (per launch = its algorithmic bytes / its event time)
@@ -266,8 +269,9 @@ def run_product(args, cfg):
         kernels = {k: {"ms_total": v[0], "launches": v[1], "alg_GB": v[2] / 1e9,
                        "GB_per_s": (v[2] / (v[0] * 1e-3) / 1e9) if v[0] > 0 else None} for k, v in prof.items()
                    if v[1] > 0}
+        traffic, traffic_src = ncu_traffic(cfg, dom)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom, "peak_source": peak_src,
+                    "traffic": traffic, "traffic_source": traffic_src, "kernel": dom, "peak_source": peak_src,
                     "alg_bytes_per_launch": db / dn,
                     "step_frac_48B_model": value * 48.0 / (peak * 1e9 * world)}
 
@@ -294,10 +298,7 @@ def run_product(args, cfg):
             torch.cuda.synchronize(device)
             ems = a0.elapsed_time(a1)
             wall = time.perf_counter() - t0
-            te = torch.tensor([ems], dtype=torch.float64, device=device)
-            if world > 1:
-                dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            ems = float(te.item())
+            ems = pdist.max_over_ranks(ems, device=device)
             e2e = {"value": cfg.updates_per_step * n_e2e / (ems * 1e-3), "unit": UNIT,
                    "h2d_bytes_per_step": int(8 * S.sizes.w_elems), "d2h_bytes_per_step": int(8 * S.sizes.w_elems),
                    "steps": n_e2e, "ms_per_step": ems / n_e2e, "wall_s": wall,

@@ -348,29 +348,36 @@ def m2_cone_plan(pb: Problem, sample_cells):
     return {"S": S, "R": R, "second": second, "first": first}
 
 
-def m2_cone_step(pb: Problem, plan, f0_of_cells, fb_of_cells):
+def m2_cone_step(pb: Problem, plan, f0_of_cells, fb_of_cells, threads: int | None = None):
     """Evaluate one M2 step at plan['S'].
     f0_of_cells(i, cells) -> [len(cells), Nd] initial f_i on those cells;
     fb_of_cells(i, cells) -> [len(cells), Nd] boundary data of velocity i.
-    Returns f at S: [nv, len(S), Nd]."""
+    Velocities are independent in transport, so they run on a thread pool
+    (the C solver releases the GIL).  Returns f at S: [nv, len(S), Nd]."""
+    from concurrent.futures import ThreadPoolExecutor
     R = plan["R"]
-    posR = {int(c): k for k, c in enumerate(R)}
     fR = np.zeros((pb.nv, R.size, pb.Nd))
-    for i in range(pb.nv):
+    threads = threads or min(pb.nv, os.cpu_count() or 1)
+
+    def first(i):
         cells = plan["first"][i]
         f = np.ascontiguousarray(f0_of_cells(i, cells), dtype=np.float64)
         fb = np.ascontiguousarray(fb_of_cells(i, cells), dtype=np.float64)
         t2_velocity(pb, pb.vel[i], 0.5 * pb.dt, f, fb, cells)
-        idx = np.searchsorted(cells, R)
-        fR[i] = f[idx]
+        fR[i] = f[np.searchsorted(cells, R)]
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(first, range(pb.nv)))
     collide(pb, fR, pb.dt)
     out = np.zeros((pb.nv, plan["S"].size, pb.Nd))
-    for i in range(pb.nv):
+
+    def second(i):
         cells = plan["second"][i]
-        idx = np.searchsorted(R, cells)
-        f = np.ascontiguousarray(fR[i][idx])
+        f = np.ascontiguousarray(fR[i][np.searchsorted(R, cells)])
         fb = np.ascontiguousarray(fb_of_cells(i, cells), dtype=np.float64)
         t2_velocity(pb, pb.vel[i], 0.5 * pb.dt, f, fb, cells)
         out[i] = f[np.searchsorted(cells, plan["S"])]
-    del posR
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(second, range(pb.nv)))
     return out

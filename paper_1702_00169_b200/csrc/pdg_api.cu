@@ -349,7 +349,7 @@ void launch_partial_t(pdg_ctx *c)
 {
     const int grid = grid_for(c->g.nnodes, 256);
     const int e = prof_begin(c);
-    pdg::partial_moments_kernel<DIM, pdg::Model<DIM, MODEL>::M>
+    pdg::partial_moments_kernel<DIM, MODEL>
         <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl);
     prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)c->g.nnodes);
 }

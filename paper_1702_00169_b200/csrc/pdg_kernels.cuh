@@ -514,24 +514,24 @@ __global__ void __launch_bounds__(256) relax_kernel(double *__restrict__ f, int6
 }
 
 // Partial moments of the local velocity block [v0, v0 + nvl): w_c = sum of local f_i in c.
-template <int DIM, int M>
+// Velocity loops run over the compile-time n_v with a range test, so every index is static
+// (no local-memory arrays).
+template <int DIM, int MODEL>
 __global__ void __launch_bounds__(256) partial_moments_kernel(const double *__restrict__ f, double *__restrict__ w,
                                                               int64_t nnodes, int v0, int nvl)
 {
+    constexpr int M = Model<DIM, MODEL>::M;
+    constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
         double acc[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) acc[c] = 0.0;
-        for (int j = 0; j < nvl; ++j) {
-            const int c = (v0 + j) / (2 * DIM);
-            const double v = f[(int64_t)j * nnodes + x];
 #pragma unroll
-            for (int cc = 0; cc < M; ++cc)
-                if (cc == c) acc[cc] += v;
-        }
+        for (int i = 0; i < NV; ++i)
+            if (i >= v0 && i < v0 + nvl) acc[i / (2 * DIM)] += __ldcs(f + (int64_t)(i - v0) * nnodes + x);
 #pragma unroll
-        for (int c = 0; c < M; ++c) w[(int64_t)c * nnodes + x] = acc[c];
+        for (int c = 0; c < M; ++c) __stcs(w + (int64_t)c * nnodes + x, acc[c]);
     }
 }
 
@@ -543,17 +543,20 @@ __global__ void __launch_bounds__(256) relax_from_w_kernel(double *__restrict__ 
 {
     using Md = Model<DIM, MODEL>;
     constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
         double wl[M];
 #pragma unroll
-        for (int c = 0; c < M; ++c) wl[c] = w[(int64_t)c * nnodes + x];
+        for (int c = 0; c < M; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
         double q[DIM][M];
         Md::flux(wl, q, P);
-        for (int j = 0; j < nvl; ++j) {
-            const double feq = feq_of<DIM, M>(v0 + j, wl, q, P);
-            double *fi = f + (int64_t)j * nnodes + x;
-            *fi = fma(cb, feq, ca * *fi);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            if (i >= v0 && i < v0 + nvl) {
+                double *fi = f + (int64_t)(i - v0) * nnodes + x;
+                __stcs(fi, fma(cb, feq_of<DIM, M>(i, wl, q, P), ca * __ldcs(fi)));
+            }
         }
     }
 }
@@ -565,6 +568,7 @@ __global__ void __launch_bounds__(256) equilibrium_kernel(double *__restrict__ f
 {
     using Md = Model<DIM, MODEL>;
     constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
         double wl[M];
@@ -572,7 +576,9 @@ __global__ void __launch_bounds__(256) equilibrium_kernel(double *__restrict__ f
         for (int c = 0; c < M; ++c) wl[c] = w[(int64_t)c * nnodes + x];
         double q[DIM][M];
         Md::flux(wl, q, P);
-        for (int j = 0; j < nvl; ++j) f[(int64_t)j * nnodes + x] = feq_of<DIM, M>(v0 + j, wl, q, P);
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (i >= v0 && i < v0 + nvl) __stcs(f + (int64_t)(i - v0) * nnodes + x, feq_of<DIM, M>(i, wl, q, P));
     }
 }
 

@@ -1,0 +1,122 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+* One M2 step from the seeded equilibrium of configs 2-5 at full size: the CUDA
+  result is compared with the oracle on sampled cells, the oracle evaluating each
+  sample exactly on its dependency cone (oracle.m2_cone_step: closures of the
+  upwind graph), from the same seeded w0.
+* The fused multi-step pass structure bench.py times (consecutive T2(dt/2) swept in
+  one pass, collision fused with the x-sweeps) equals separate single-step calls:
+  a property that holds at any size.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from pdg_inputs import CONFIGS
+from gpu_helpers import make_solver, rel_maxnorm
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def fill_w0(cfg, w_flat):
+    from pdg_inputs import w0_grid
+    w = w_flat.view((cfg.m,) + cfg.grid_shape)
+    if cfg.dim == 2:
+        w.copy_(w0_grid(cfg, device=w_flat.device))
+        return
+    L = cfg.N * cfg.n
+    slab = max(1, min(L, (1 << 24) // (L * L)))
+    for z0 in range(0, L, slab):
+        w[:, z0:z0 + slab].copy_(w0_grid(cfg, device=w_flat.device, zslab=(z0, min(L, z0 + slab))))
+
+
+def cell_node_index(cfg, cells: np.ndarray) -> torch.Tensor:
+    """Grid node indices [len(cells), Nd] of the nodes of `cells` (cell-blocked order)."""
+    n, N, D = cfg.n, cfg.N, cfg.dim
+    L = N * n
+    cells = torch.as_tensor(cells, dtype=torch.int64)
+    cc = []
+    r = cells.clone()
+    for _ in range(D):
+        cc.append(r % N)
+        r = r // N
+    a = torch.arange(n ** D, dtype=torch.int64)
+    aa = []
+    r = a.clone()
+    for _ in range(D):
+        aa.append(r % n)
+        r = r // n
+    idx = torch.zeros((cells.numel(), n ** D), dtype=torch.int64)
+    stride = 1
+    for d in range(D):
+        coord = cc[d].view(-1, 1) * n + aa[d].view(1, -1)
+        idx += coord * stride
+        stride *= L
+    return idx
+
+
+def sample_cells(cfg):
+    N, D = cfg.N, cfg.dim
+    rng = np.random.default_rng(17)
+    pts = [[0] * D, [N // 2] * D, list(rng.integers(0, N, D))]
+    out = []
+    for p in pts:
+        c = 0
+        for d in reversed(range(D)):
+            c = c * N + int(p[d])
+        out.append(c)
+    return np.array(sorted(set(out)), dtype=np.int64)
+
+
+@pytest.mark.parametrize("key", [2, 3, 4, 5])
+def test_fullsize_one_step_sampled(key):
+    cfg = CONFIGS[key]
+    torch.cuda.empty_cache()
+    S = make_solver(cfg)
+    fill_w0(cfg, S.w)
+    S.set_equilibrium(S.w)
+    pb = O.Problem.from_config(cfg)
+    samples = sample_cells(cfg)
+    plan = O.m2_cone_plan(pb, samples)
+    # inputs of the oracle: the same seeded w0, gathered at the cells each pass needs
+    need = np.unique(np.concatenate(plan["first"]))
+    idx = cell_node_index(cfg, need).to(S.w.device)
+    w_need = S.w.view(cfg.m, -1)[:, idx.view(-1)].view(cfg.m, need.size, -1).cpu().numpy()
+    f_need = O.equilibrium_field(pb, np.ascontiguousarray(w_need))  # [nv, ncell_need, Nd]
+    def f0_of(i, cells):
+        return np.ascontiguousarray(f_need[i][np.searchsorted(need, cells)])
+
+    S.step(1)
+    sidx = cell_node_index(cfg, samples).to(S.f.device)
+    got = S.f.view(cfg.nv, -1)[:, sidx.view(-1)].view(cfg.nv, samples.size, -1).cpu().numpy()
+    ref = O.m2_cone_step(pb, plan, f0_of, f0_of)  # w_b = w0 (reading C12): f^b = f0 on the faces
+    assert rel_maxnorm(got, ref) < TOL
+    S.destroy()
+    del S
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("key", [3, 5])
+def test_fullsize_fused_passes_equal_separate_steps(key):
+    """step(3) (fused TT passes, NPASS=2 kernels) == 3 x step(1) (NPASS=1 kernels)."""
+    cfg = CONFIGS[key]
+    torch.cuda.empty_cache()
+    S = make_solver(cfg)
+    fill_w0(cfg, S.w)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    pick = torch.randint(0, S.sizes.f_elems, (1 << 20,), generator=g).to(S.f.device)
+    S.set_equilibrium(S.w)
+    S.step(3)
+    a = S.f[pick].cpu().numpy()
+    fill_w0(cfg, S.w)
+    S.set_equilibrium(S.w)
+    for _ in range(3):
+        S.step(1)
+    b = S.f[pick].cpu().numpy()
+    assert rel_maxnorm(a, b) < 1e-13
+    S.destroy()
+    del S
+    torch.cuda.empty_cache()
