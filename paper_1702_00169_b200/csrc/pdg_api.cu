@@ -170,6 +170,7 @@ struct pdg_ctx {
     pdg::NcclComm comm;
     int device = 0;
     Profiler prof;
+    int sms = 148;
 };
 
 namespace {
@@ -237,6 +238,23 @@ double sweep_bytes(const pdg_ctx *c, const pdg::SweepParams &sp)
 
 enum { SWEEP_ALL = 0, SWEEP_YZ = 1, SWEEP_X = 2 };
 
+// Segments per strided line: 1 when the lines alone fill the GPU several times over,
+// else enough segments (<= 32, >= 4 cells each) to reach ~2 waves of threads.
+int strided_segments(const pdg_ctx *c, const pdg::SweepParams &sp)
+{
+    int64_t lines = 0;
+    int ncells = 1 << 30;
+    for (int i = 0; i < sp.nvel; ++i) {
+        lines += sp.v[i].nlines;
+        ncells = std::min(ncells, sp.v[i].ncells);
+    }
+    const int64_t target = (int64_t)c->sms * 2048 * 2;
+    if (lines >= target / 2 || ncells < 8) return 1;
+    int nseg = (int)std::min<int64_t>(32, (target + lines - 1) / std::max<int64_t>(lines, 1));
+    nseg = std::min(nseg, ncells / 4);
+    return std::max(1, nseg);
+}
+
 template <int N, int NPASS>
 void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParams &yzp, int which)
 {
@@ -244,10 +262,16 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
         int64_t maxl = 0;
         for (int i = 0; i < yzp.nvel; ++i) maxl = std::max(maxl, yzp.v[i].nlines);
         const int e = prof_begin(c);
-        // prefetch depth tuned on B200 (tools/microbench_strided.cu): n=3 -> 2, n=4 -> 3 (one sweep) / 1 (two)
-        constexpr int PF = (N == 4) ? (NPASS == 1 ? 3 : 1) : 2;
-        dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
-        pdg::sweep_strided_kernel<N, NPASS, PF><<<grid, 256, 0, c->stream>>>(yzp);
+        const int nseg = strided_segments(c, yzp);
+        if (nseg > 1) {
+            dim3 grid((unsigned)((maxl + 31) / 32), (unsigned)yzp.nvel);
+            pdg::sweep_strided_seg_kernel<N, NPASS><<<grid, dim3(32, nseg), 0, c->stream>>>(yzp, nseg);
+        } else {
+            // prefetch depth tuned on B200 (tools/microbench_strided.cu): n=3 -> 2, n=4 -> 3 (one sweep) / 1 (two)
+            constexpr int PF = (N == 4) ? (NPASS == 1 ? 3 : 1) : 2;
+            dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)yzp.nvel);
+            pdg::sweep_strided_kernel<N, NPASS, PF><<<grid, 256, 0, c->stream>>>(yzp);
+        }
         prof_end(c, e, PDG_K_SWEEP_STRIDED, sweep_bytes(c, yzp));
     }
     if (xp.nvel > 0 && which != SWEEP_YZ) {
@@ -546,6 +570,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     c->counter = (unsigned long long *)work_dev;
     c->stream = (cudaStream_t)p->cuda_stream;
     cudaGetDevice(&c->device);
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
     std::memset(&c->mp, 0, sizeof(c->mp));
     if (p->flux == PDG_FLUX_LINEAR_ADVECTION)
         for (int d = 0; d < p->dim; ++d) c->mp.a[d] = p->flux_params[d];

@@ -200,6 +200,79 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
 }
 
 // ---------------------------------------------------------------------------
+// Segmented T2 sweep along a strided axis, for grids with too few lines to fill the GPU
+// (e.g. 2-D config 2: 6144 y-lines).  Block = 32 consecutive lines (lanes, coalesced)
+// x nseg segments (threadIdx.y).  Per pass: each thread walks its segment with zero
+// inflow to get s_out = A + B s_in (B = beta^cells), the true segment inflows follow by
+// composing the affine maps of the upstream segments (shared memory), then the segment
+// is walked again with the exact recurrence.  Re-reads the data (L2-resident sizes).
+// ---------------------------------------------------------------------------
+template <int N, int NPASS>
+__global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepParams P, int nseg)
+{
+    __shared__ double sA[32][33], sB[32][33];
+    const SweepVel V = P.v[blockIdx.y];
+    const int lane = threadIdx.x, sg = threadIdx.y;
+    const int64_t line = (int64_t)blockIdx.x * 32 + lane;
+    const bool active = line < V.nlines;
+    const int64_t Lk = (int64_t)V.ncells * N;
+    const int64_t ln = active ? line : 0;
+    const int64_t base = (ln / V.inner) * (V.inner * Lk) + (ln % V.inner);
+    const int64_t step = (V.sign > 0) ? V.inner : -V.inner;
+    double *p0 = P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    const int ks = (V.ncells + nseg - 1) / nseg;
+    const int c0 = min(V.ncells, sg * ks), c1 = min(V.ncells, c0 + ks);
+
+    double M[N * N], g[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
+    const double beta = g[N - 1];
+    const double s0 = active ? 2.0 * P.fb[V.fb_off + line] : 0.0;  // ghost: f^b old + new
+
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) {
+        double A = 0.0, B = 1.0;
+        if (active) {
+            for (int c = c0; c < c1; ++c) {
+                double fo[N];
+#pragma unroll
+                for (int a = 0; a < N; ++a) fo[a] = p0[((int64_t)c * N + a) * step];
+                double r = fo[N - 1];
+#pragma unroll
+                for (int b = 0; b < N; ++b) r = fma(M[(N - 1) * N + b], fo[b], r);
+                A = fma(beta, A, r);
+                B *= beta;
+            }
+        }
+        sA[sg][lane] = A;
+        sB[sg][lane] = B;
+        __syncthreads();
+        double s = s0;
+        for (int j = 0; j < sg; ++j) s = fma(sB[j][lane], s, sA[j][lane]);
+        if (active) {
+            for (int c = c0; c < c1; ++c) {
+                double fo[N], fn[N];
+#pragma unroll
+                for (int a = 0; a < N; ++a) fo[a] = p0[((int64_t)c * N + a) * step];
+#pragma unroll
+                for (int a = 0; a < N; ++a) {
+                    double acc = g[a] * s;
+#pragma unroll
+                    for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
+                    fn[a] = acc;
+                }
+                s = fo[N - 1] + fn[N - 1];
+#pragma unroll
+                for (int a = 0; a < N; ++a) p0[((int64_t)c * N + a) * step] = fn[a];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Warp sweep of one line held in shared memory: lane = segment of K consecutive cells
 // (flow order).  Per pass: zero-inflow carry of each segment (s_out = A + B s_in,
 // B = beta^cells), a 5-step warp-shuffle affine scan for the true segment inflows,
