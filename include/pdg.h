@@ -79,7 +79,10 @@ typedef enum {
 
 typedef enum {
     PDG_SCHEME_M2 = 0,    /* T2(dt/2) C2(dt) T2(dt/2), the hot path */
-    PDG_SCHEME_M2KIN = 1  /* T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) */
+    PDG_SCHEME_M2KIN = 1, /* T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) */
+    PDG_SCHEME_M4 = 2     /* M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1:
+                             palindromic composition raising the order to 4; needs
+                             2 tau + g2 dt/2 > 0 when tau > 0 */
 } pdg_scheme;
 
 /* pdg_problem.flags */
@@ -121,10 +124,12 @@ typedef struct {
     double dt;                   /* time step of one palindromic step (may be negative) */
     int32_t scheme;              /* pdg_scheme */
     int32_t rank, nranks;        /* velocity shard: contiguous block of nv/nranks velocity indices */
-    const void *nccl_id;         /* 128-byte ncclUniqueId (identical on all ranks).  NULL with nranks > 1
-                                    creates a communicator-less shard: pdg_collide/pdg_moments then return
-                                    PDG_E_NCCL and the caller reduces w_dev itself between
-                                    pdg_partial_moments and pdg_relax_from_w */
+    const void *nccl_id;         /* 128-byte ncclUniqueId (identical on all ranks).  Non-NULL: the context
+                                    owns an NCCL communicator and the collision takes the sharded path
+                                    (partial moments, NCCL sum, relax) -- also with nranks == 1.
+                                    NULL with nranks > 1 creates a communicator-less shard:
+                                    pdg_collide/pdg_moments then return PDG_E_NCCL and the caller reduces
+                                    w_dev itself between pdg_partial_moments and pdg_relax_from_w */
     void *cuda_stream;           /* cudaStream_t for every launch of this context */
     uint32_t flags;              /* PDG_CHECK_STATE | PDG_SYNC_ERRORS | PDG_NO_FUSION */
 } pdg_problem;

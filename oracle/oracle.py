@@ -323,6 +323,39 @@ def m2_run(pb: Problem, f_grid: np.ndarray, fb_grid: np.ndarray, nsteps: int, ca
     return pb.cells_to_grid(fc)
 
 
+def m2kin_substep(pb: Problem, fc, fbc, h: float):
+    """M2kin(h) = T2(h/4) C2(h/2) T2(h/2) C2(h/2) T2(h/4)  (P:500-505), in place, cell-blocked."""
+    t2_all(pb, h / 4, fc, fbc)
+    collide(pb, fc, h / 2)
+    t2_all(pb, h / 2, fc, fbc)
+    collide(pb, fc, h / 2)
+    t2_all(pb, h / 4, fc, fbc)
+
+
+def scheme_run(pb: Problem, f_grid: np.ndarray, fb_grid: np.ndarray, nsteps: int, scheme: str) -> np.ndarray:
+    """nsteps of 'm2', 'm2kin' or 'm4': the symmetric triple-jump
+    composition M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1
+    (palindromic composition to higher even order)."""
+    fc = pb.grid_to_cells(np.asarray(f_grid, dtype=np.float64))
+    fbc = pb.grid_to_cells(np.asarray(fb_grid, dtype=np.float64))
+    g1 = 1.0 / (2.0 - 2.0 ** (1.0 / 3.0))
+    g2 = 1.0 - 2.0 * g1
+    for _ in range(nsteps):
+        if scheme == "m2":
+            t2_all(pb, 0.5 * pb.dt, fc, fbc)
+            collide(pb, fc, pb.dt)
+            t2_all(pb, 0.5 * pb.dt, fc, fbc)
+        elif scheme == "m2kin":
+            m2kin_substep(pb, fc, fbc, pb.dt)
+        elif scheme == "m4":
+            m2kin_substep(pb, fc, fbc, g1 * pb.dt)
+            m2kin_substep(pb, fc, fbc, g2 * pb.dt)
+            m2kin_substep(pb, fc, fbc, g1 * pb.dt)
+        else:
+            raise ValueError(scheme)
+    return pb.cells_to_grid(fc)
+
+
 def initial_data(pb: Problem, w0_grid: np.ndarray, wb_grid: np.ndarray):
     """f0 = f^eq(w0) at every node, f^b = f^eq(w_b) (readings C12, C13)."""
     return equilibrium_field(pb, w0_grid), equilibrium_field(pb, wb_grid)

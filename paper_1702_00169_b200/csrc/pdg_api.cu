@@ -55,7 +55,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     if (!(p->lambda > 0.0) || !std::isfinite(p->lambda)) return fail(PDG_E_INVALID_ARGUMENT, "lambda must be > 0");
     if (!(p->dt != 0.0) || !std::isfinite(p->dt)) return fail(PDG_E_INVALID_ARGUMENT, "dt must be finite and != 0");
     if (!(p->tau >= 0.0) || !std::isfinite(p->tau)) return fail(PDG_E_INVALID_ARGUMENT, "tau must be >= 0");
-    if (p->scheme != PDG_SCHEME_M2 && p->scheme != PDG_SCHEME_M2KIN)
+    if (p->scheme != PDG_SCHEME_M2 && p->scheme != PDG_SCHEME_M2KIN && p->scheme != PDG_SCHEME_M4)
         return fail(PDG_E_INVALID_ARGUMENT, "unknown scheme");
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
     g->dim = p->dim;
@@ -424,12 +424,15 @@ void collision_coeffs(const pdg_ctx *c, double dt, double *ca, double *cb)
     }
 }
 
+// Sharded collision path: several ranks, or a communicator given explicitly (also with one rank).
+bool sharded(const pdg_ctx *c) { return c->prob.nranks > 1 || c->comm.comm != nullptr; }
+
 pdg_status partial_and_reduce(pdg_ctx *c)
 {
     PDG_DISPATCH(launch_partial_t, c);
     pdg_status s = post_launch(c, "partial_moments");
     if (s != PDG_OK) return s;
-    if (c->prob.nranks > 1) {
+    if (sharded(c)) {
         std::string err;
         if (!c->comm.comm) return fail(PDG_E_NCCL, "communicator-less shard context: reduce w_dev yourself "
                                                    "between pdg_partial_moments and pdg_relax_from_w");
@@ -445,7 +448,7 @@ pdg_status collide(pdg_ctx *c, double dt)
 {
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
-    if (c->prob.nranks == 1) {
+    if (!sharded(c)) {
         PDG_DISPATCH(launch_relax_t, c, ca, cb);
         return post_launch(c, "relax");
     }
@@ -483,8 +486,79 @@ pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
 
 bool use_relax_x(const pdg_ctx *c)
 {
-    return c->prob.nranks == 1 && !(c->prob.flags & PDG_NO_FUSION) && relax_x_smem(c) <= 110 * 1024 &&
+    return !sharded(c) && !(c->prob.flags & PDG_NO_FUSION) && relax_x_smem(c) <= 110 * 1024 &&
            c->g.nnodes / (c->g.ncell[0] * c->g.n) < (int64_t)1 << 31;
+}
+
+// ---- the palindromic step as a list of operators ------------------------------------------
+// T(h) = T2(h) on every velocity, C(h) = C2(h).  Execution fuses, without changing any
+// operator: two consecutive T(h) with the same h into one pass over f (two sweeps), and a
+// C followed by T's into the collision + x-sweep kernel plus one y/z sweep pass.
+struct Op {
+    int kind;  // 0: T, 1: C
+    double h;
+};
+
+void append_m2kin(std::vector<Op> &ops, double dt)
+{
+    // M2kin(dt) = T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4)
+    ops.push_back({0, 0.25 * dt});
+    ops.push_back({1, 0.5 * dt});
+    ops.push_back({0, 0.5 * dt});
+    ops.push_back({1, 0.5 * dt});
+    ops.push_back({0, 0.25 * dt});
+}
+
+void append_scheme(std::vector<Op> &ops, int scheme, double dt)
+{
+    if (scheme == PDG_SCHEME_M2) {
+        // M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
+        ops.push_back({0, 0.5 * dt});
+        ops.push_back({1, dt});
+        ops.push_back({0, 0.5 * dt});
+    } else if (scheme == PDG_SCHEME_M2KIN) {
+        append_m2kin(ops, dt);
+    } else {
+        // M4 = M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt): symmetric triple jump, a palindromic
+        // composition of M2kin raising the order to 4; g1 = 1/(2 - 2^{1/3}).
+        const long double cr = cbrtl(2.0L);
+        const double g1 = (double)(1.0L / (2.0L - cr));
+        const double g2 = (double)(-cr / (2.0L - cr));
+        append_m2kin(ops, g1 * dt);
+        append_m2kin(ops, g2 * dt);
+        append_m2kin(ops, g1 * dt);
+    }
+}
+
+pdg_status execute_ops(pdg_ctx *c, const std::vector<Op> &ops)
+{
+    const bool fuse = !(c->prob.flags & PDG_NO_FUSION);
+    const bool fx = use_relax_x(c);
+    const size_t n = ops.size();
+    size_t i = 0;
+    pdg_status s = PDG_OK;
+    while (i < n && s == PDG_OK) {
+        if (ops[i].kind == 1) {
+            int np = 0;
+            if (i + 1 < n && ops[i + 1].kind == 0) {
+                np = 1;
+                if (fuse && i + 2 < n && ops[i + 2].kind == 0 && ops[i + 2].h == ops[i + 1].h) np = 2;
+            }
+            if (fx && np > 0) {
+                s = collide_xsweep(c, ops[i].h, ops[i + 1].h, np);
+                if (s == PDG_OK) s = transport_pass(c, ops[i + 1].h, np, SWEEP_YZ);
+                i += 1 + np;
+            } else {
+                s = collide(c, ops[i].h);
+                i += 1;
+            }
+        } else {
+            const int np = (fuse && i + 1 < n && ops[i + 1].kind == 0 && ops[i + 1].h == ops[i].h) ? 2 : 1;
+            s = transport_pass(c, ops[i].h, np);
+            i += np;
+        }
+    }
+    return s;
 }
 
 void build_sweep_params(pdg_ctx *c)
@@ -595,7 +669,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
             return fail(PDG_E_CUDA, "cudaEventCreate failed");
         }
     }
-    if (p->nranks > 1 && p->nccl_id) {
+    if (p->nccl_id) {
         std::string err;
         if (!c->comm.init(p->nccl_id, p->nranks, p->rank, &err)) {
             delete c;
@@ -700,54 +774,9 @@ pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
     if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (nsteps == 0) return PDG_OK;
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
-    const double dt = c->prob.dt;
-    const bool fuse = !(c->prob.flags & PDG_NO_FUSION);
-    pdg_status s = PDG_OK;
-    const bool fx = use_relax_x(c);
-    if (c->prob.scheme == PDG_SCHEME_M2) {
-        // M2(dt) = T2(dt/2) C2(dt) T2(dt/2); the trailing T2(dt/2) of step k and the
-        // leading T2(dt/2) of step k+1 are swept in one pass (two sweeps, no collapse).
-        s = transport_pass(c, 0.5 * dt, 1);
-        for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
-            const bool last = (k + 1 == nsteps);
-            if (fx) {
-                const int np = last ? 1 : 2;
-                s = collide_xsweep(c, dt, 0.5 * dt, np);
-                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, np, SWEEP_YZ);
-            } else {
-                s = collide(c, dt);
-                if (s != PDG_OK) break;
-                if (!last && fuse) s = transport_pass(c, 0.5 * dt, 2);
-                else if (!last) {
-                    s = transport_pass(c, 0.5 * dt, 1);
-                    if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
-                } else s = transport_pass(c, 0.5 * dt, 1);
-            }
-        }
-    } else {
-        // M2kin(dt) = T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4)
-        s = transport_pass(c, 0.25 * dt, 1);
-        for (int64_t k = 0; k < nsteps && s == PDG_OK; ++k) {
-            const bool last = (k + 1 == nsteps);
-            if (fx) {
-                s = collide_xsweep(c, 0.5 * dt, 0.5 * dt, 1);
-                if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1, SWEEP_YZ);
-                const int np = last ? 1 : 2;
-                if (s == PDG_OK) s = collide_xsweep(c, 0.5 * dt, 0.25 * dt, np);
-                if (s == PDG_OK) s = transport_pass(c, 0.25 * dt, np, SWEEP_YZ);
-                continue;
-            }
-            s = collide(c, 0.5 * dt);
-            if (s == PDG_OK) s = transport_pass(c, 0.5 * dt, 1);
-            if (s == PDG_OK) s = collide(c, 0.5 * dt);
-            if (s != PDG_OK) break;
-            if (!last && fuse) s = transport_pass(c, 0.25 * dt, 2);
-            else if (!last) {
-                s = transport_pass(c, 0.25 * dt, 1);
-                if (s == PDG_OK) s = transport_pass(c, 0.25 * dt, 1);
-            } else s = transport_pass(c, 0.25 * dt, 1);
-        }
-    }
+    std::vector<Op> ops;
+    for (int64_t k = 0; k < nsteps; ++k) append_scheme(ops, c->prob.scheme, c->prob.dt);
+    pdg_status s = execute_ops(c, ops);
     if (s != PDG_OK) return s;
     if (c->prob.flags & PDG_CHECK_STATE) {
         int64_t bad = 0;
@@ -776,7 +805,7 @@ pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad)
     if (!c || !n_bad) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     PDG_CUDA_TRY(cudaMemsetAsync(c->counter, 0, sizeof(unsigned long long), c->stream));
     const int grid = grid_for(c->g.nnodes, 256);
-    const int check_rho = (c->prob.flux != PDG_FLUX_LINEAR_ADVECTION && c->prob.nranks == 1) ? 1 : 0;
+    const int check_rho = (c->prob.flux != PDG_FLUX_LINEAR_ADVECTION && !sharded(c)) ? 1 : 0;
     if (c->g.dim == 2)
         pdg::check_state_kernel<2><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, check_rho,
                                                                 c->counter);

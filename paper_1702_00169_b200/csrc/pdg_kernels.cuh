@@ -619,18 +619,17 @@ __global__ void __launch_bounds__(256) relax_from_w_kernel(double *__restrict__ 
     constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
-        double wl[M];
+        double fl[NV], wl[M];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fl[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
 #pragma unroll
         for (int c = 0; c < M; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
         double q[DIM][M];
         Md::flux(wl, q, P);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            if (i >= v0 && i < v0 + nvl) {
-                double *fi = f + (int64_t)(i - v0) * nnodes + x;
-                __stcs(fi, fma(cb, feq_of<DIM, M>(i, wl, q, P), ca * __ldcs(fi)));
-            }
-        }
+        for (int i = 0; i < NV; ++i)
+            if (i >= v0 && i < v0 + nvl)
+                __stcs(f + (int64_t)(i - v0) * nnodes + x, fma(cb, feq_of<DIM, M>(i, wl, q, P), ca * fl[i]));
     }
 }
 

@@ -32,6 +32,7 @@ PDG_FLUX_EULER = 1
 PDG_FLUX_ISOTHERMAL = 2
 PDG_SCHEME_M2 = 0
 PDG_SCHEME_M2KIN = 1
+PDG_SCHEME_M4 = 2
 PDG_CHECK_STATE = 0x1
 PDG_SYNC_ERRORS = 0x2
 PDG_NO_FUSION = 0x4

@@ -339,3 +339,35 @@ def test_odd_line_count():
     S = gpu_with_state(cfg, f0, fbg)
     S.step(3)
     assert rel_maxnorm(to_np(S.get_state(), f0.shape), O.m2_run(pb, f0, fbg, 3)) < TOL_STEP
+
+
+def test_nccl_communicator_path_single_rank():
+    """The sharded collision through libpdg's own NCCL communicator (1 rank): dlopen of
+    libnccl, ncclCommInitRank, partial moments, ncclAllReduce, relax_from_w."""
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(6).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg, nccl_id=pdg.nccl_unique_id(), flags=pdg.PDG_PROFILE)
+    S.step(3)
+    got = to_np(S.get_state(), f0.shape)
+    prof = S.profile_read()
+    assert prof["allreduce"][1] == 3 and prof["relax_from_w"][1] == 3 and prof["relax_xsweep"][1] == 0
+    assert rel_maxnorm(got, O.m2_run(pb, f0, fbg, 3)) < TOL_STEP
+    w = to_np(S.moments(), (cfg.m,) + cfg.grid_shape)
+    assert rel_maxnorm(w, O.moments(pb, O.m2_run(pb, f0, fbg, 3))) < TOL_STEP
+
+
+@pytest.mark.parametrize("scheme_name,tau", [("m2kin", 0.0), ("m4", 0.05), ("m4", 0.0)])
+def test_composed_schemes(scheme_name, tau):
+    """M2kin (NEXT-1) and the fourth-order composition M4 (NEXT-4) vs the oracle."""
+    from paper_1702_00169_b200 import pdg
+    code = {"m2kin": pdg.PDG_SCHEME_M2KIN, "m4": pdg.PDG_SCHEME_M4}[scheme_name]
+    # the negative substep of M4 sweeps with kappa < 0, where the carry factor |beta| grows
+    # quickly: only small CFL numbers are stable (config-1 model, nu = 0.5)
+    cfg = CONFIGS[1].resized(16) if scheme_name == "m4" else CONFIGS[3].resized(5).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    pb.tau = tau
+    S = gpu_with_state(cfg, f0, fbg, scheme=code, tau=tau)
+    S.step(3)
+    ref = O.scheme_run(pb, f0, fbg, 3, scheme_name)
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP

@@ -492,3 +492,23 @@ def test_layout_roundtrip():
     cell = 1 + 3 * (0 + 3 * 2)
     loc = 3 + 4 * (1 + 4 * 0)
     assert c[cell, loc] == g[8, 1, 7]
+
+
+@pytest.mark.parametrize("scheme,tau,order", [("m2kin", 0.05, 2.0), ("m2kin", 0.0, 2.0), ("m4", 0.05, 4.0)])
+def test_palindromic_composition_orders(scheme, tau, order):
+    """M2kin is second order also at tau = 0; its symmetric triple-jump
+    composition is fourth order.  Config-1 model, N = 8, T = 0.25."""
+    base = CONFIGS[1].resized(8)
+    from pdg_inputs import w0_grid, wb_grid
+    w0 = w0_grid(base).numpy()
+    wb = wb_grid(base, w0_grid(base)).numpy()
+
+    def run(nsteps):
+        pb = O.Problem.from_config(base, tau=tau)
+        pb.dt = 0.25 / nsteps
+        f0, fb = O.initial_data(pb, w0, wb)
+        return O.scheme_run(pb, f0, fb, nsteps, scheme)
+    ref = run(512)
+    errs = [np.max(np.abs(run(s) - ref)) for s in (16, 32, 64)]
+    slopes = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
+    assert all(abs(s - order) < 0.15 for s in slopes), (errs, slopes)
