@@ -32,11 +32,12 @@
  *  - node grid: for an N_0 x N_1 (x N_2) cell box of degree p, n = p+1 nodes per
  *    cell and axis; node index (Z, Y, X) with X = c_x*n + a_x (a_x = local GL
  *    node along x), same for Y, Z.  nnodes = prod_d (N_d * n).
- *  - f:  [nv_local][Z][Y][X]   (local velocities of this rank, see pdg_sizes)
+ *  - f:  [nv_local][Z][Y][X]   (local velocities of this rank, see pdg_sizes; with PDG_DECOMP_ZSLAB
+ *        all velocities and only the rank's planes cell_begin..cell_begin+cell_count-1 of the slowest axis)
  *  - fb: [nv_local][plane_stride]; velocity i (axis k_i) stores its inflow
  *        plane = the node grid with axis k_i removed, in the same order
  *        (e.g. axis y in 3-D: [Z][X]); plane_stride = max over axes.
- *  - w:  [m][Z][Y][X]
+ *  - w:  [m][Z][Y][X]   (the rank's planes with PDG_DECOMP_ZSLAB)
  *
  * Velocity set: the vectorial D2Q4 / D3Q6-per-component set (reading C6):
  *   velocity i = c*2D + 2k + s has v_i = (s ? -lambda : +lambda) e_k and
@@ -85,6 +86,16 @@ typedef enum {
                              2 tau + g2 dt/2 > 0 when tau > 0 */
 } pdg_scheme;
 
+typedef enum {
+    PDG_DECOMP_VELOCITY = 0, /* rank r owns velocities [r nv/G, (r+1) nv/G) on the whole grid; one NCCL
+                                sum of the m moment fields per collision (north star) */
+    PDG_DECOMP_ZSLAB = 1     /* rank r owns the cell planes [r N/G, (r+1) N/G) of the slowest axis (z in 3-D,
+                                y in 2-D) with every velocity; sweeps along that axis run per slab with zero
+                                inflow, the exact inflows follow from an affine scan of the slabs' outgoing
+                                carries (linear superposition of the carry recurrence; NCCL all-gather of
+                                carry planes) and a correction of the first cells of each slab */
+} pdg_decomposition;
+
 /* pdg_problem.flags */
 #define PDG_CHECK_STATE 0x1u  /* after each pdg_step, count nodes with rho <= 0 or non-finite f (one extra pass) */
 #define PDG_SYNC_ERRORS 0x2u  /* synchronise the stream after every call and report asynchronous faults there */
@@ -104,7 +115,8 @@ typedef enum {
     PDG_K_ALLREDUCE = 5,     /* NCCL sum of w */
     PDG_K_OTHER = 6,         /* initialisation / checks */
     PDG_K_RELAX_X = 7,       /* collision fused with moments and the following x-velocity sweep(s) */
-    PDG_NUM_KERNEL_KINDS = 8
+    PDG_K_ZSLAB = 8,         /* z-slab carry scan + correction (and the carry all-gather) */
+    PDG_NUM_KERNEL_KINDS = 9
 } pdg_kernel_kind;
 
 typedef struct {
@@ -131,18 +143,24 @@ typedef struct {
                                     pdg_collide/pdg_moments then return PDG_E_NCCL and the caller reduces
                                     w_dev itself between pdg_partial_moments and pdg_relax_from_w */
     void *cuda_stream;           /* cudaStream_t for every launch of this context */
-    uint32_t flags;              /* PDG_CHECK_STATE | PDG_SYNC_ERRORS | PDG_NO_FUSION */
+    uint32_t flags;              /* PDG_CHECK_STATE | PDG_SYNC_ERRORS | PDG_NO_FUSION | PDG_PROFILE */
+    int32_t decomposition;       /* pdg_decomposition: how nranks > 1 split the work */
+    int32_t slabs_per_rank;      /* PDG_DECOMP_ZSLAB: sub-slabs per rank (>= 1; > 1 emulates more ranks
+                                    on one GPU with the same arithmetic) */
 } pdg_problem;
 
 typedef struct {
-    size_t f_elems;        /* doubles in f_dev  = nv_local * nnodes */
+    size_t f_elems;        /* doubles in f_dev  = nv_local * nnodes_local */
     size_t fb_elems;       /* doubles in fb_dev = nv_local * plane_stride */
-    size_t w_elems;        /* doubles in w_dev  = m * nnodes (moments / sharded exchange / equilibrium init) */
-    size_t work_bytes;     /* bytes of work_dev (device scratch: counters) */
+    size_t w_elems;        /* doubles in w_dev  = m * nnodes_local (moments / exchange / equilibrium init) */
+    size_t work_bytes;     /* bytes of work_dev (device scratch: counters, slab carry planes and tables) */
     int64_t nnodes;        /* nodes of the full grid */
     int64_t plane_stride;  /* doubles per velocity in fb */
     int32_t nv_local;      /* velocities owned by this rank */
     int32_t v_begin;       /* first owned velocity index */
+    int64_t nnodes_local;  /* nodes owned by this rank (== nnodes unless PDG_DECOMP_ZSLAB) */
+    int64_t cell_begin;    /* PDG_DECOMP_ZSLAB: first owned cell plane of the slowest axis (else 0) */
+    int64_t cell_count;    /* PDG_DECOMP_ZSLAB: owned cell planes (else ncell of that axis) */
 } pdg_sizes;
 
 /* Validate *p and return the buffer sizes of this rank.  Host-only: needs no GPU.

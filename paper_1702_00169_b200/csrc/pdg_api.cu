@@ -38,14 +38,29 @@ pdg_status fail(pdg_status s, const std::string &msg)
             return fail(PDG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));               \
     } while (0)
 
+constexpr int kMaxSlabs = 64;
+
 struct Geometry {
     int dim = 0, p = 0, n = 0, m = 0, nv = 0, nvl = 0, v0 = 0;
-    int64_t ncell[3] = {1, 1, 1};
-    int64_t L[3] = {1, 1, 1};      // nodes per axis
-    int64_t stride[3] = {1, 1, 1}; // element stride of each axis in the node grid
-    int64_t nnodes = 0, plane_stride = 0;
+    int64_t ncell[3] = {1, 1, 1};  // LOCAL cells per axis (the rank's slab along the outer axis)
+    int64_t L[3] = {1, 1, 1};      // local nodes per axis
+    int64_t stride[3] = {1, 1, 1}; // element stride of each axis in the local node grid
+    int64_t nnodes = 0, plane_stride = 0;  // local
+    int64_t gnnodes = 0;                   // global
     double h[3] = {1, 1, 1};
+    // PDG_DECOMP_ZSLAB
+    int zslab = 0;          // 1 if the z-slab decomposition is active
+    int outer = 0;          // slowest axis (dim - 1)
+    int nslab = 1;          // global number of slabs
+    int slab0 = 0;          // first global slab of this rank
+    int nslab_local = 1;    // slabs of this rank
+    int64_t gncell_outer = 0, cell_begin = 0;
+    int64_t slab_begin[kMaxSlabs + 1] = {0};  // global cell plane where slab s starts
+    size_t carry_doubles = 0;                 // one carry/inflow buffer (doubles)
+    size_t table_doubles = 0;                 // one correction table (doubles)
 };
+
+constexpr int kMaxTables = 16;
 
 pdg_status validate(const pdg_problem *p, Geometry *g)
 {
@@ -120,10 +135,55 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
         }
     }
     g->nv = p->nv;
-    if (p->nv % p->nranks != 0) return fail(PDG_E_INVALID_ARGUMENT, "nv must be divisible by nranks");
-    g->nvl = p->nv / p->nranks;
-    g->v0 = p->rank * g->nvl;
+    g->gnnodes = g->nnodes;
+    if (p->decomposition == PDG_DECOMP_VELOCITY) {
+        if (p->nv % p->nranks != 0) return fail(PDG_E_INVALID_ARGUMENT, "nv must be divisible by nranks");
+        g->nvl = p->nv / p->nranks;
+        g->v0 = p->rank * g->nvl;
+        g->gncell_outer = g->ncell[p->dim - 1];
+        return PDG_OK;
+    }
+    if (p->decomposition != PDG_DECOMP_ZSLAB) return fail(PDG_E_INVALID_ARGUMENT, "unknown decomposition");
+    // z-slab decomposition: all velocities local, the rank owns a range of cell planes of the outer axis
+    const int outer = p->dim - 1;
+    const int spr = p->slabs_per_rank < 1 ? 1 : p->slabs_per_rank;
+    const int64_t S = (int64_t)p->nranks * spr;
+    const int64_t Nout = g->ncell[outer];
+    if (S > kMaxSlabs) return fail(PDG_E_INVALID_ARGUMENT, "at most 64 slabs");
+    if (S > Nout) return fail(PDG_E_INVALID_ARGUMENT, "more slabs than cell planes");
+    g->zslab = (S > 1) ? 1 : 0;
+    g->outer = outer;
+    g->nslab = (int)S;
+    g->slab0 = p->rank * spr;
+    g->nslab_local = spr;
+    g->gncell_outer = Nout;
+    for (int64_t sl = 0; sl <= S; ++sl) g->slab_begin[sl] = (sl * Nout) / S;
+    g->cell_begin = g->slab_begin[g->slab0];
+    const int64_t cnt = g->slab_begin[g->slab0 + spr] - g->cell_begin;
+    g->nvl = p->nv;
+    g->v0 = 0;
+    g->ncell[outer] = cnt;
+    g->L[outer] = cnt * g->n;
+    g->stride[0] = 1;
+    g->stride[1] = g->L[0];
+    g->stride[2] = g->L[0] * g->L[1];
+    g->nnodes = g->L[0] * g->L[1] * g->L[2];
+    int64_t ps2 = 0;
+    for (int d = 0; d < p->dim; ++d) ps2 = std::max(ps2, g->nnodes / g->L[d]);
+    g->plane_stride = ps2;
+    const int64_t plane = g->nnodes / g->L[outer];  // lines along the outer axis
+    const int nvo = 2 * p->m;                         // velocities along the outer axis
+    g->carry_doubles = (size_t)S * nvo * 2 * (size_t)plane;
+    const int64_t lmax = (Nout + S - 1) / S + 1;
+    g->table_doubles = (size_t)(2 * lmax * g->n + 2 * (lmax + 1));
     return PDG_OK;
+}
+
+size_t work_bytes_of(const Geometry &g)
+{
+    size_t b = 256;
+    if (g.zslab) b += sizeof(double) * (2 * g.carry_doubles + kMaxTables * g.table_doubles);
+    return b;
 }
 
 void fill_sizes(const Geometry &g, pdg_sizes *out)
@@ -131,11 +191,14 @@ void fill_sizes(const Geometry &g, pdg_sizes *out)
     out->f_elems = (size_t)g.nvl * (size_t)g.nnodes;
     out->fb_elems = (size_t)g.nvl * (size_t)g.plane_stride;
     out->w_elems = (size_t)g.m * (size_t)g.nnodes;
-    out->work_bytes = 256;
-    out->nnodes = g.nnodes;
+    out->work_bytes = work_bytes_of(g);
+    out->nnodes = g.gnnodes;
     out->plane_stride = g.plane_stride;
     out->nv_local = g.nvl;
     out->v_begin = g.v0;
+    out->nnodes_local = g.nnodes;
+    out->cell_begin = g.cell_begin;
+    out->cell_count = g.ncell[g.dim - 1];
 }
 
 struct ProfRec {
@@ -171,9 +234,20 @@ struct pdg_ctx {
     int device = 0;
     Profiler prof;
     int sms = 148;
+    // z-slab decomposition
+    std::vector<pdg::SweepVel> outer_entries;  // per (outer velocity, local slab)
+    double *zcarry = nullptr, *zinflow = nullptr, *ztables = nullptr;
+    struct ZTable {
+        double dtp;
+        int npass, slot, leff;
+        std::vector<double> B, C;  // by slab length
+    };
+    std::vector<ZTable> ztables_host;
 };
 
 namespace {
+
+pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass);
 
 pdg_status post_launch(pdg_ctx *c, const char *what)
 {
@@ -293,16 +367,35 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_A
     std::memcpy(xp.blk, blk, sizeof(blk));
     std::memcpy(yzp.blk, blk, sizeof(blk));
     const int n = c->g.n;
-    if (npass == 1) {
-        if (n == 2) launch_sweeps<2, 1>(c, xp, yzp, which);
-        else if (n == 3) launch_sweeps<3, 1>(c, xp, yzp, which);
-        else launch_sweeps<4, 1>(c, xp, yzp, which);
-    } else {
-        if (n == 2) launch_sweeps<2, 2>(c, xp, yzp, which);
-        else if (n == 3) launch_sweeps<3, 2>(c, xp, yzp, which);
-        else launch_sweeps<4, 2>(c, xp, yzp, which);
+    auto launch = [&](const pdg::SweepParams &a, const pdg::SweepParams &b, int wh) {
+        if (npass == 1) {
+            if (n == 2) launch_sweeps<2, 1>(c, a, b, wh);
+            else if (n == 3) launch_sweeps<3, 1>(c, a, b, wh);
+            else launch_sweeps<4, 1>(c, a, b, wh);
+        } else {
+            if (n == 2) launch_sweeps<2, 2>(c, a, b, wh);
+            else if (n == 3) launch_sweeps<3, 2>(c, a, b, wh);
+            else launch_sweeps<4, 2>(c, a, b, wh);
+        }
+    };
+    launch(xp, yzp, which);
+    const bool outer = c->g.zslab && which != SWEEP_X && !c->outer_entries.empty();
+    if (outer) {
+        // slab sweeps of the outer-axis velocities, in launches of at most kMaxVel entries
+        pdg::SweepParams op = yzp;
+        pdg::SweepParams none = xp;
+        none.nvel = 0;
+        op.cout = c->zcarry;
+        const size_t ne = c->outer_entries.size();
+        for (size_t b0 = 0; b0 < ne; b0 += pdg::kMaxVel) {
+            op.nvel = (int32_t)std::min<size_t>(pdg::kMaxVel, ne - b0);
+            for (int i = 0; i < op.nvel; ++i) op.v[i] = c->outer_entries[b0 + i];
+            launch(none, op, SWEEP_YZ);
+        }
     }
-    return post_launch(c, "sweep");
+    pdg_status s = post_launch(c, "sweep");
+    if (s == PDG_OK && outer) s = zslab_resolve(c, dtp, npass);
+    return s;
 }
 
 // ---- collision fused with the x-velocity sweeps (nranks == 1) ----------------------------
@@ -425,7 +518,10 @@ void collision_coeffs(const pdg_ctx *c, double dt, double *ca, double *cb)
 }
 
 // Sharded collision path: several ranks, or a communicator given explicitly (also with one rank).
-bool sharded(const pdg_ctx *c) { return c->prob.nranks > 1 || c->comm.comm != nullptr; }
+bool sharded(const pdg_ctx *c)
+{
+    return c->prob.decomposition == PDG_DECOMP_VELOCITY && (c->prob.nranks > 1 || c->comm.comm != nullptr);
+}
 
 pdg_status partial_and_reduce(pdg_ctx *c)
 {
@@ -584,10 +680,165 @@ void build_sweep_params(pdg_ctx *c)
         V.sign = s ? -1 : 1;
         V.axis = k;
         V.vel = i;
+        V.cout_off = -1;
+        V.zero_inflow = 0;
         c->all_params.v[c->all_params.nvel++] = V;
         if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
-        else c->yz_params.v[c->yz_params.nvel++] = V;
+        else if (g.zslab && k == g.outer) {
+            // one entry per local slab: zero inflow unless the velocity enters the domain there
+            const int jo = 2 * (i / (2 * g.dim)) + s;  // index among the outer-axis velocities
+            for (int t = 0; t < g.nslab_local; ++t) {
+                const int sl = g.slab0 + t;
+                const int64_t lb = g.slab_begin[sl] - g.cell_begin;
+                pdg::SweepVel E = V;
+                E.f_off = (int64_t)j * g.nnodes + lb * g.n * g.stride[k];
+                E.ncells = (int32_t)(g.slab_begin[sl + 1] - g.slab_begin[sl]);
+                E.zero_inflow = (sl == (s ? g.nslab - 1 : 0)) ? 0 : 1;
+                E.cout_off = ((int64_t)sl * (2 * g.m) + jo) * 2 * V.nlines;
+                c->outer_entries.push_back(E);
+            }
+        } else
+            c->yz_params.v[c->yz_params.nvel++] = V;
     }
+}
+
+// ---- z-slab carry tables ------------------------------------------------------------------
+// For one sweep pass structure (T2(dtp) applied npass times): Q_l = g beta^l (response of cell l
+// to a unit inflow), P_l (pass-2 response to a unit pass-1 inflow), B_len = beta^len and C_len
+// (pass-2 outgoing carry response), computed in long double by running the recurrence on unit
+// inputs.  Truncated at leff where |P_l|, |Q_l| < 2^-64 for every later l.
+pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out)
+{
+    for (const auto &t : c->ztables_host)
+        if (t.dtp == dtp && t.npass == npass) {
+            *out = &t;
+            return PDG_OK;
+        }
+    if ((int)c->ztables_host.size() >= kMaxTables) return fail(PDG_E_UNSUPPORTED, "too many distinct z-slab steps");
+    const Geometry &g = c->g;
+    const int n = g.n;
+    int64_t lmax = 0;
+    for (int sl = 0; sl < g.nslab; ++sl) lmax = std::max(lmax, g.slab_begin[sl + 1] - g.slab_begin[sl]);
+    lmax += 1;
+    pdg::CellBlock cb;
+    const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)g.h[g.outer];
+    if (!pdg::cell_block(g.p, kappa, &cb)) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block");
+    // long-double copies of the block
+    long double M[16], gv[4];
+    {
+        // recompute in long double for the tables (the kernel block is its double rounding)
+        long double x[4], w[4], D[16], G[16], A[16], Ai[16];
+        pdg::gl_nodes(g.p, x, w);
+        pdg::lagrange_derivative(n, x, D);
+        for (int i = 0; i < n; ++i)
+            for (int jj = 0; jj < n; ++jj) {
+                long double v = D[jj * n + i] * w[jj];
+                if (i == n - 1 && jj == n - 1) v -= 1.0L;
+                G[i * n + jj] = v / w[i];
+                A[i * n + jj] = ((i == jj) ? 1.0L : 0.0L) - kappa * G[i * n + jj];
+            }
+        pdg::invert(n, A, Ai);
+        for (int i = 0; i < n; ++i) {
+            for (int jj = 0; jj < n; ++jj) {
+                long double acc = 0.0L;
+                for (int k = 0; k < n; ++k) acc += Ai[i * n + k] * (((k == jj) ? 1.0L : 0.0L) + kappa * G[k * n + jj]);
+                M[i * n + jj] = acc;
+            }
+            gv[i] = Ai[i * n + 0] * kappa / w[0];
+        }
+    }
+    std::vector<double> table((size_t)2 * lmax * n, 0.0);
+    pdg_ctx::ZTable zt;
+    zt.dtp = dtp;
+    zt.npass = npass;
+    zt.B.assign(lmax + 1, 0.0);
+    zt.C.assign(lmax + 1, 0.0);
+    long double c1 = 1.0L, c2 = 0.0L;  // carries of pass 1 (unit inflow) and pass 2 (zero inflow)
+    int leff = 0;
+    zt.B[0] = 1.0;
+    zt.C[0] = 0.0;
+    for (int64_t l = 0; l < lmax; ++l) {
+        long double d1[4], d2[4];
+        for (int a = 0; a < n; ++a) d1[a] = gv[a] * c1;  // pass-1 response (old data 0)
+        c1 = d1[n - 1];
+        for (int a = 0; a < n; ++a) {
+            long double acc = gv[a] * c2;
+            for (int b = 0; b < n; ++b) acc += M[a * n + b] * d1[b];
+            d2[a] = acc;
+        }
+        c2 = d1[n - 1] + d2[n - 1];
+        bool big = false;
+        for (int a = 0; a < n; ++a) {
+            table[(size_t)l * n + a] = (double)d2[a];               // P_l
+            table[(size_t)lmax * n + l * n + a] = (double)d1[a];   // Q_l
+            if (fabsl(d1[a]) >= 0x1p-64L || (npass > 1 && fabsl(d2[a]) >= 0x1p-64L)) big = true;
+        }
+        if (big) leff = (int)l + 1;
+        zt.B[l + 1] = (double)c1;
+        zt.C[l + 1] = (double)c2;
+    }
+    zt.leff = leff;
+    zt.slot = (int)c->ztables_host.size();
+    cudaError_t e = cudaMemcpy(c->ztables + (size_t)zt.slot * g.table_doubles, table.data(),
+                               sizeof(double) * table.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(PDG_E_CUDA, std::string("z-slab table upload: ") + cudaGetErrorString(e));
+    c->ztables_host.push_back(zt);
+    *out = &c->ztables_host.back();
+    return PDG_OK;
+}
+
+// Exact inflows of every slab from the outgoing carries, then the correction of the local slabs.
+pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
+{
+    const Geometry &g = c->g;
+    const pdg_ctx::ZTable *zt = nullptr;
+    pdg_status st = ztable(c, dtp, npass, &zt);
+    if (st != PDG_OK) return st;
+    const int e = prof_begin(c);
+    if (c->prob.nranks > 1) {
+        std::string err;
+        if (!c->comm.comm) return fail(PDG_E_NCCL, "z-slab decomposition over ranks needs nccl_id");
+        const size_t per_rank = g.carry_doubles / (size_t)c->prob.nranks;
+        if (!c->comm.allgather(c->zcarry, per_rank, c->prob.rank, c->stream, &err)) return fail(PDG_E_NCCL, err);
+    }
+    pdg::ZSlabParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.carry = c->zcarry;
+    P.inflow = c->zinflow;
+    P.f = c->f;
+    P.table = c->ztables + (size_t)zt->slot * g.table_doubles;
+    P.plane = g.nnodes / g.L[g.outer];
+    P.nnodes = g.nnodes;
+    P.inner = g.stride[g.outer];
+    P.nslab = g.nslab;
+    P.slab0 = g.slab0;
+    P.nslab_local = g.nslab_local;
+    P.nvo = 2 * g.m;
+    P.npass = npass;
+    P.leff = zt->leff;
+    P.lmax = (int)(zt->B.size() - 1);
+    for (int jo = 0; jo < P.nvo; ++jo) {
+        const int comp = jo / 2, sgn = jo % 2;
+        P.vel[jo] = comp * 2 * g.dim + 2 * g.outer + sgn;
+        P.sign[jo] = sgn ? -1 : 1;
+    }
+    for (int sl = 0; sl < g.nslab; ++sl) {
+        const int len = (int)(g.slab_begin[sl + 1] - g.slab_begin[sl]);
+        P.cells[sl] = len;
+        P.local_begin[sl] = (int)(g.slab_begin[sl] - g.cell_begin);
+        P.B[sl] = zt->B[len];
+        P.C[sl] = zt->C[len];
+    }
+    dim3 g1((unsigned)((P.plane + 255) / 256), (unsigned)P.nvo);
+    pdg::zslab_scan_kernel<<<g1, 256, 0, c->stream>>>(P);
+    dim3 g2((unsigned)((P.plane + 255) / 256), (unsigned)(P.nvo * g.nslab_local));
+    if (g.n == 2) pdg::zslab_correct_kernel<2><<<g2, 256, 0, c->stream>>>(P);
+    else if (g.n == 3) pdg::zslab_correct_kernel<3><<<g2, 256, 0, c->stream>>>(P);
+    else pdg::zslab_correct_kernel<4><<<g2, 256, 0, c->stream>>>(P);
+    const double corr_bytes = 16.0 * (double)P.nvo * (double)(g.nslab_local) * (double)P.plane *
+                              (double)std::min<int64_t>(zt->leff, P.lmax) * g.n;
+    prof_end(c, e, PDG_K_ZSLAB, corr_bytes + 16.0 * (double)g.carry_doubles);
+    return post_launch(c, "zslab_resolve");
 }
 
 bool is_device_pointer(const void *p)
@@ -652,7 +903,26 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     if (p->flux == PDG_FLUX_ISOTHERMAL) c->mp.c2 = p->flux_params[0] * p->flux_params[0];
     c->mp.inv2D = 1.0 / (2.0 * p->dim);
     c->mp.inv2lam = 1.0 / (2.0 * p->lambda);
+    if (c->g.zslab) {
+        c->zcarry = reinterpret_cast<double *>(static_cast<char *>(work_dev) + 256);
+        c->zinflow = c->zcarry + c->g.carry_doubles;
+        c->ztables = c->zinflow + c->g.carry_doubles;
+    }
     build_sweep_params(c);
+    if (c->g.zslab) {  // tables of the scheme's sweeps (single and fused double passes)
+        std::vector<Op> ops;
+        append_scheme(ops, p->scheme, p->dt);
+        for (const Op &o : ops)
+            if (o.kind == 0)
+                for (int np = 1; np <= 2; ++np) {
+                    const pdg_ctx::ZTable *zt = nullptr;
+                    pdg_status zs = ztable(c, o.h, np, &zt);
+                    if (zs != PDG_OK) {
+                        delete c;
+                        return zs;
+                    }
+                }
+    }
     if (p->flags & PDG_PROFILE) {
         c->prof.on = true;
         c->prof.ev.resize(2 * 4096);

@@ -19,12 +19,14 @@ struct NcclApi {
     typedef int (*GetUniqueId_t)(void *);
     typedef int (*CommInitRank_t)(void **, int, const void *, int);  // (comm*, nranks, id (by value: 128 B), rank)
     typedef int (*AllReduce_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+    typedef int (*AllGather_t)(const void *, void *, size_t, int, void *, cudaStream_t);
     typedef int (*CommDestroy_t)(void *);
     typedef const char *(*GetErrorString_t)(int);
     void *handle = nullptr;
     GetUniqueId_t getUniqueId = nullptr;
     void *commInitRank = nullptr;
     AllReduce_t allReduce = nullptr;
+    AllGather_t allGather = nullptr;
     CommDestroy_t commDestroy = nullptr;
     GetErrorString_t getErrorString = nullptr;
 
@@ -40,9 +42,10 @@ struct NcclApi {
         getUniqueId = (GetUniqueId_t)dlsym(handle, "ncclGetUniqueId");
         commInitRank = dlsym(handle, "ncclCommInitRank");
         allReduce = (AllReduce_t)dlsym(handle, "ncclAllReduce");
+        allGather = (AllGather_t)dlsym(handle, "ncclAllGather");
         commDestroy = (CommDestroy_t)dlsym(handle, "ncclCommDestroy");
         getErrorString = (GetErrorString_t)dlsym(handle, "ncclGetErrorString");
-        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy) {
+        if (!getUniqueId || !commInitRank || !allReduce || !allGather || !commDestroy) {
             *err = "libnccl.so.2 lacks a required symbol";
             return false;
         }
@@ -102,6 +105,18 @@ struct NcclComm {
         int r = a.allReduce(buf, buf, count, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm, stream);
         if (r != 0) {
             *err = "ncclAllReduce: " + a.message(r);
+            return false;
+        }
+        return true;
+    }
+
+    // in-place fp64 all-gather: rank r's block of `count` doubles sits at buf + r * count
+    bool allgather(double *buf, size_t count, int rank, cudaStream_t stream, std::string *err)
+    {
+        NcclApi &a = nccl_api();
+        int r = a.allGather(buf + (size_t)rank * count, buf, count, /*ncclFloat64*/ 8, comm, stream);
+        if (r != 0) {
+            *err = "ncclAllGather: " + a.message(r);
             return false;
         }
         return true;

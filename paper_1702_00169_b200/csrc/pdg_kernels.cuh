@@ -38,12 +38,16 @@ struct SweepVel {
     int32_t ncells;   // cells along the axis
     int32_t sign;     // +1: walk upward, -1: walk downward
     int32_t axis;
-    int32_t vel;      // global velocity index
+    int32_t vel;        // global velocity index
+    int64_t cout_off;   // >= 0: write the outgoing carry of pass q at cout[cout_off + q*nlines + line]
+    int32_t zero_inflow;  // 1: the line starts inside the domain (z-slab): inflow carry 0, corrected later
+    int32_t pad;
 };
 
 struct SweepParams {
     double *f;
     const double *fb;
+    double *cout;     // outgoing carries of slab sweeps (z-slab decomposition)
     DevBlock blk[3];  // per axis (kappa_k = lambda dt' / h_k)
     int32_t nvel;
     SweepVel v[kMaxVel];
@@ -152,7 +156,8 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
     for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
 
     double carry[NPASS];
-    const double s0 = 2.0 * P.fb[V.fb_off + line];  // ghost cell: f^b old + f^b new (reading C5)
+    // ghost cell: f^b old + f^b new (reading C5); a slab interior start has zero inflow
+    const double s0 = V.zero_inflow ? 0.0 : 2.0 * P.fb[V.fb_off + line];
 #pragma unroll
     for (int q = 0; q < NPASS; ++q) carry[q] = s0;
 
@@ -197,6 +202,10 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
             }
         }
     }
+    if (V.cout_off >= 0) {
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) P.cout[V.cout_off + q * V.nlines + line] = carry[q];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
 #pragma unroll
     for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
     const double beta = g[N - 1];
-    const double s0 = active ? 2.0 * P.fb[V.fb_off + line] : 0.0;  // ghost: f^b old + new
+    const double s0 = (active && !V.zero_inflow) ? 2.0 * P.fb[V.fb_off + line] : 0.0;  // ghost: f^b old + new
 
 #pragma unroll
     for (int q = 0; q < NPASS; ++q) {
@@ -267,6 +276,7 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
 #pragma unroll
                 for (int a = 0; a < N; ++a) p0[((int64_t)c * N + a) * step] = fn[a];
             }
+            if (V.cout_off >= 0 && c1 == V.ncells && c0 < c1) P.cout[V.cout_off + q * V.nlines + line] = s;
         }
         __syncthreads();
     }
@@ -697,6 +707,88 @@ __global__ void __launch_bounds__(256) check_state_kernel(const double *__restri
     }
     for (int off = 16; off > 0; off >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, off);
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Z-slab decomposition: along the outer axis every slab is swept with zero
+// inflow (except the slab where the velocity enters the domain) and writes its outgoing
+// carries A_q (pass q).  The carry recurrence is affine, so the exact inflows follow from
+// the slabs upstream: with B = beta^len and C = the pass-2 carry response to a unit
+// pass-1 inflow (host tables),
+//   S1(next) = A1 + B S1,   S2(next) = A2 + C S1 + B S2.
+// The slab's values are then corrected cell by cell: f_l += P_l S1 + Q_l S2 (two passes) or
+// f_l += Q_l S1 (one pass), Q_l = g beta^l, P_l = pass-2 response (host tables, truncated
+// where |P_l|, |Q_l| < 2^-64).
+// ---------------------------------------------------------------------------
+struct ZSlabParams {
+    const double *carry;   // [slab][vel][2][plane] outgoing carries of the slab sweeps
+    double *inflow;        // [slab][vel][2][plane] exact inflows (output of the scan)
+    double *f;
+    const double *table;   // P[lmax][n], Q[lmax][n]
+    double B[64], C[64];   // per global slab: beta^len, pass-2 carry response
+    int64_t plane;         // lines per slab
+    int64_t nnodes;        // local nodes per velocity
+    int64_t inner;         // stride of the outer axis
+    int32_t nslab, slab0, nslab_local, nvo, npass, leff, lmax;
+    int32_t vel[16];       // global velocity index of outer velocity j
+    int32_t sign[16];
+    int32_t cells[64];     // cells of global slab s
+    int32_t local_begin[64];  // first local cell plane of global slab s (valid for local slabs)
+};
+
+__global__ void __launch_bounds__(256) zslab_scan_kernel(const ZSlabParams P)
+{
+    const int j = blockIdx.y;
+    const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= P.plane) return;
+    const bool up = P.sign[j] > 0;
+    const int first = up ? 0 : P.nslab - 1;
+    const int64_t vstride = 2 * P.plane;
+    const int64_t sstride = (int64_t)P.nvo * vstride;
+    double c1 = P.carry[first * sstride + j * vstride + line];
+    double c2 = (P.npass > 1) ? P.carry[first * sstride + j * vstride + P.plane + line] : 0.0;
+    for (int k = 1; k < P.nslab; ++k) {
+        const int s = up ? k : P.nslab - 1 - k;
+        const int64_t o = s * sstride + j * vstride + line;
+        P.inflow[o] = c1;
+        if (P.npass > 1) P.inflow[o + P.plane] = c2;
+        const double a1 = P.carry[o];
+        const double n1 = fma(P.B[s], c1, a1);
+        if (P.npass > 1) c2 = fma(P.B[s], c2, fma(P.C[s], c1, P.carry[o + P.plane]));
+        c1 = n1;
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) zslab_correct_kernel(const ZSlabParams P)
+{
+    const int j = blockIdx.y % P.nvo;
+    const int t = blockIdx.y / P.nvo;  // local slab
+    const int s = P.slab0 + t;
+    const bool up = P.sign[j] > 0;
+    if (s == (up ? 0 : P.nslab - 1)) return;  // the entry slab saw the true inflow
+    const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= P.plane) return;
+    const int64_t vstride = 2 * P.plane;
+    const int64_t o = s * (int64_t)P.nvo * vstride + j * vstride + line;
+    const double S1 = P.inflow[o];
+    const double S2 = (P.npass > 1) ? P.inflow[o + P.plane] : 0.0;
+    const int ncell = P.cells[s];
+    const int lend = min(ncell, P.leff);
+    double *col = P.f + (int64_t)P.vel[j] * P.nnodes + line;  // the outer axis is the slowest: base = line
+    const double *Pt = P.table;
+    const double *Qt = P.table + (int64_t)P.lmax * N;
+    for (int l = 0; l < lend; ++l) {
+        const int cell = P.local_begin[s] + (up ? l : ncell - 1 - l);
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            const int am = up ? a : N - 1 - a;
+            double *ptr = col + ((int64_t)cell * N + am) * P.inner;
+            double corr = Qt[l * N + a] * ((P.npass > 1) ? S2 : S1);
+            if (P.npass > 1) corr = fma(Pt[l * N + a], S1, corr);
+            *ptr += corr;
+        }
+    }
 }
 
 }  // namespace pdg

@@ -38,7 +38,9 @@ PDG_SYNC_ERRORS = 0x2
 PDG_NO_FUSION = 0x4
 PDG_PROFILE = 0x8
 KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other",
-                "relax_xsweep"]
+                "relax_xsweep", "zslab"]
+PDG_DECOMP_VELOCITY = 0
+PDG_DECOMP_ZSLAB = 1
 
 EXPORTED = [
     "pdg_query_sizes", "pdg_create", "pdg_set_state", "pdg_set_equilibrium", "pdg_get_state", "pdg_step",
@@ -57,13 +59,15 @@ class pdg_problem(ctypes.Structure):
         ("n_flux_params", ctypes.c_int32), ("tau", ctypes.c_double), ("dt", ctypes.c_double),
         ("scheme", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint32),
+        ("decomposition", ctypes.c_int32), ("slabs_per_rank", ctypes.c_int32),
     ]
 
 
 class pdg_sizes(ctypes.Structure):
     _fields_ = [("f_elems", ctypes.c_size_t), ("fb_elems", ctypes.c_size_t), ("w_elems", ctypes.c_size_t),
                 ("work_bytes", ctypes.c_size_t), ("nnodes", ctypes.c_int64), ("plane_stride", ctypes.c_int64),
-                ("nv_local", ctypes.c_int32), ("v_begin", ctypes.c_int32)]
+                ("nv_local", ctypes.c_int32), ("v_begin", ctypes.c_int32), ("nnodes_local", ctypes.c_int64),
+                ("cell_begin", ctypes.c_int64), ("cell_count", ctypes.c_int64)]
 
 
 class PdgError(RuntimeError):
@@ -135,7 +139,8 @@ def version() -> str:
 
 
 def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, tau=0.0, scheme=PDG_SCHEME_M2,
-                 rank=0, nranks=1, nccl_id=None, stream=None, flags=0, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0)):
+                 rank=0, nranks=1, nccl_id=None, stream=None, flags=0, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
+                 decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1):
     """Build a pdg_problem; the returned object keeps its host arrays alive."""
     pb = pdg_problem()
     pb.dim = dim
@@ -162,6 +167,8 @@ def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, t
         pb.nccl_id = ctypes.cast(pb._id, ctypes.c_void_p)
     pb.cuda_stream = stream
     pb.flags = flags
+    pb.decomposition = decomposition
+    pb.slabs_per_rank = slabs_per_rank
     return pb
 
 
@@ -296,9 +303,11 @@ class Solver:
             pass
 
 
-def problem_from_config(cfg, tau=0.0, scheme=PDG_SCHEME_M2, rank=0, nranks=1, nccl_id=None, flags=0, stream=None):
+def problem_from_config(cfg, tau=0.0, scheme=PDG_SCHEME_M2, rank=0, nranks=1, nccl_id=None, flags=0, stream=None,
+                        decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1):
     """pdg_problem for a pdg_inputs.Config (the seeded workload descriptions)."""
     vel, comp = cfg.velocities()
     return make_problem(cfg.dim, cfg.N, cfg.p, cfg.m, vel, comp, cfg.lam, cfg.flux, list(cfg.fparams), cfg.dt,
                         tau=tau, scheme=scheme, rank=rank, nranks=nranks, nccl_id=nccl_id, flags=flags,
-                        stream=stream, lo=cfg.lo, hi=cfg.hi)
+                        stream=stream, lo=cfg.lo, hi=cfg.hi, decomposition=decomposition,
+                        slabs_per_rank=slabs_per_rank)

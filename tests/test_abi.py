@@ -86,3 +86,25 @@ def test_solver_refuses_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         pdg.Solver(pdg.problem_from_config(CONFIGS[1]))
+
+
+def test_query_sizes_zslab():
+    cfg = CONFIGS[5]
+    G = 8
+    begins = []
+    for r in range(G):
+        s = pdg.query_sizes(pdg.problem_from_config(cfg, rank=r, nranks=G, decomposition=pdg.PDG_DECOMP_ZSLAB))
+        assert s.nv_local == cfg.nv and s.v_begin == 0
+        assert s.cell_count == cfg.N // G and s.cell_begin == r * (cfg.N // G)
+        assert s.nnodes_local == cfg.nnodes // G and s.nnodes == cfg.nnodes
+        assert s.f_elems == cfg.nv * cfg.nnodes // G
+        begins.append(s.cell_begin)
+        # carry planes: 8 slabs x 8 z-velocities x 2 passes x 768^2 doubles
+        assert s.work_bytes >= 8 * (2 * 8 * 8 * 2 * 768 * 768)
+    assert begins == sorted(begins)
+    s = pdg.query_sizes(pdg.problem_from_config(CONFIGS[3].resized(10), decomposition=pdg.PDG_DECOMP_ZSLAB,
+                                                slabs_per_rank=4))
+    assert s.cell_count == 10 and s.nnodes_local == s.nnodes
+    with pytest.raises(pdg.PdgError):
+        pdg.query_sizes(pdg.problem_from_config(CONFIGS[3].resized(4), decomposition=pdg.PDG_DECOMP_ZSLAB,
+                                                slabs_per_rank=8))

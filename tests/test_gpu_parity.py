@@ -371,3 +371,47 @@ def test_composed_schemes(scheme_name, tau):
     S.step(3)
     ref = O.scheme_run(pb, f0, fbg, 3, scheme_name)
     assert rel_maxnorm(to_np(S.get_state(), f0.shape), ref) < TOL_STEP
+
+
+# --------------------------------------------------------------------------
+# Row e: z-slab decomposition, emulated on one GPU with sub-slabs (same arithmetic as
+# one slab per rank: zero-inflow slab sweeps, affine carry scan, correction)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("key,N,S,steps", [(3, 8, 2, 3), (3, 8, 4, 3), (3, 10, 4, 2), (4, 6, 3, 2),
+                                           (5, 16, 8, 2), (2, 24, 5, 3), (1, 37, 6, 3)])
+def test_zslab_emulated_parity(key, N, S, steps):
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[key].resized(N)
+    if key != 1:
+        cfg = cfg.stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    Z = gpu_with_state(cfg, f0, fbg, decomposition=pdg.PDG_DECOMP_ZSLAB, slabs_per_rank=S, flags=pdg.PDG_PROFILE)
+    Z.step(steps)
+    assert Z.profile_read()["zslab"][1] > 0
+    got = to_np(Z.get_state(), f0.shape)
+    assert rel_maxnorm(got, O.m2_run(pb, f0, fbg, steps)) < TOL_STEP
+
+
+@pytest.mark.parametrize("dtp_frac", [0.5, 1.7, -0.05])
+def test_zslab_single_transport(dtp_frac):
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[4].resized(6)
+    f, fb_full = random_inputs(cfg, 21)
+    Z = gpu_with_state(cfg, f, fb_full, decomposition=pdg.PDG_DECOMP_ZSLAB, slabs_per_rank=3)
+    dtp = dtp_frac * cfg.dt
+    Z.transport(dtp)
+    pb = oracle_problem(cfg)
+    fc = pb.grid_to_cells(f)
+    O.t2_all(pb, dtp, fc, pb.grid_to_cells(fb_full))
+    assert rel_maxnorm(to_np(Z.get_state(), f.shape), pb.cells_to_grid(fc)) < TOL_OP
+
+
+def test_zslab_m2kin_and_unfused():
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(8).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    for kw in (dict(scheme=pdg.PDG_SCHEME_M2KIN), dict(flags=pdg.PDG_NO_FUSION)):
+        Z = gpu_with_state(cfg, f0, fbg, decomposition=pdg.PDG_DECOMP_ZSLAB, slabs_per_rank=4, **kw)
+        Z.step(2)
+        ref = O.scheme_run(pb, f0, fbg, 2, "m2kin" if "scheme" in kw else "m2")
+        assert rel_maxnorm(to_np(Z.get_state(), f0.shape), ref) < TOL_STEP
