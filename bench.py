@@ -190,32 +190,37 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def config_block(cfg, G):
+def config_block(cfg, G, decomp="velocity", spr=1):
     return {"workload": cfg.name, "dim": cfg.dim, "cells_per_axis": cfg.N, "degree": cfg.p, "m": cfg.m,
             "nv": cfg.nv, "lambda": cfg.lam, "dt": cfg.dt, "nodes": cfg.nnodes,
             "updates_per_step": cfg.updates_per_step, "f_bytes": 8 * cfg.nv * cfg.nnodes,
             "l2": "inputs larger than L2 (f = %.1f GB >> 126 MB); no flush" % (8e-9 * cfg.nv * cfg.nnodes)
             if 8 * cfg.nv * cfg.nnodes > 4 * 126e6 else "f fits in L2: HBM fraction not meaningful",
-            "parallelism": f"velocity-sharded x{G}" + (" + NCCL allreduce of w" if G > 1 else ""),
+            "parallelism": (f"velocity-sharded x{G}" + (" + NCCL allreduce of w" if G > 1 else "")) if decomp == "velocity"
+            else f"z-slab x{G} ({spr} slab(s)/rank) + NCCL all-gather of carry planes",
             "scheme": "M2 = T2(dt/2) C2(dt) T2(dt/2), consecutive half-steps swept in one pass"}
 
 
 # ----------------------------------------------------------------------------
 # product arm
 # ----------------------------------------------------------------------------
-def fill_w0(cfg, w_flat, device):
-    """Seeded w0 on the device, generated in z-slabs straight into w_flat ([m][nodes])."""
+def fill_w0(cfg, w_flat, device, sizes=None):
+    """Seeded w0 of this rank's node planes (all of them unless z-slab decomposed), generated
+    in slabs straight into w_flat ([m][local nodes])."""
     import torch
     from pdg_inputs import w0_grid
-    w = w_flat.view((cfg.m,) + cfg.grid_shape)
-    if cfg.dim == 2:
-        w.copy_(w0_grid(cfg, device=device))
-        return
     L = cfg.N * cfg.n
+    p0 = 0 if sizes is None else int(sizes.cell_begin) * cfg.n
+    p1 = L if sizes is None else (int(sizes.cell_begin) + int(sizes.cell_count)) * cfg.n
+    shape = (cfg.m, p1 - p0) + cfg.grid_shape[1:]
+    w = w_flat.view(shape)
+    if cfg.dim == 2:
+        w.copy_(w0_grid(cfg, device=device)[:, p0:p1])
+        return
     slab = max(1, min(L, (1 << 25) // (L * L)))
-    for z0 in range(0, L, slab):
-        z1 = min(L, z0 + slab)
-        w[:, z0:z1].copy_(w0_grid(cfg, device=device, zslab=(z0, z1)))
+    for z0 in range(p0, p1, slab):
+        z1 = min(p1, z0 + slab)
+        w[:, z0 - p0:z1 - p0].copy_(w0_grid(cfg, device=device, zslab=(z0, z1)))
     torch.cuda.synchronize(device)
 
 
@@ -236,8 +241,10 @@ def run_product(args, cfg):
         dist.init_process_group("nccl", device_id=device)
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
-        S = pdist.sharded_solver(cfg, device, flags=pdg.PDG_PROFILE, stream=stream.cuda_stream)
-        fill_w0(cfg, S.w, device)
+        decomp = {"velocity": pdg.PDG_DECOMP_VELOCITY, "zslab": pdg.PDG_DECOMP_ZSLAB}[args.decomp]
+        S = pdist.sharded_solver(cfg, device, flags=pdg.PDG_PROFILE, stream=stream.cuda_stream,
+                                 decomposition=decomp, slabs_per_rank=args.slabs_per_rank)
+        fill_w0(cfg, S.w, device, S.sizes)
         S.set_equilibrium(S.w)
         S.step(args.warmup)
         S.profile_read()  # discard warm-up launches
@@ -282,7 +289,7 @@ def run_product(args, cfg):
             n_e2e = max(1, min(args.steps, args.e2e_steps))
             w_host = torch.empty(S.sizes.w_elems, dtype=torch.float64, pin_memory=True)
             w_out = torch.empty(S.sizes.w_elems, dtype=torch.float64, pin_memory=True)
-            fill_w0(cfg, S.w, device)
+            fill_w0(cfg, S.w, device, S.sizes)
             w_host.copy_(S.w)
             torch.cuda.synchronize(device)
             if launched:
@@ -316,7 +323,7 @@ def run_product(args, cfg):
                     "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                     "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                     "data": "synthetic (seeded pdg_inputs recipe of the config)",
-                    "config": config_block(cfg, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                    "config": config_block(cfg, world, args.decomp, args.slabs_per_rank), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                     "gpu_launches": launches, "clocks": clk, "kernels": kernels,
                     "hbm_roofline_frac_48B": value * 48.0 / (peak * 1e9 * world)}
             print(json.dumps(line), flush=True)
@@ -337,11 +344,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=64)
     ap.add_argument("--ref-cells", type=int, default=32)
+    ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
+                    help="multi-GPU decomposition (default: zslab when launched on several ranks)")
+    ap.add_argument("--slabs-per-rank", type=int, default=1)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "product":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     from pdg_inputs import CONFIGS
     cfg = CONFIGS[args.config]
+    if args.decomp is None:
+        args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "velocity"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -306,7 +306,8 @@ bool fill_blocks(pdg_ctx *c, double dtp, pdg::DevBlock blk[3])
 double sweep_bytes(const pdg_ctx *c, const pdg::SweepParams &sp)
 {
     double b = 0.0;
-    for (int i = 0; i < sp.nvel; ++i) b += 16.0 * (double)c->g.nnodes + 8.0 * (double)sp.v[i].nlines;
+    for (int i = 0; i < sp.nvel; ++i)
+        b += 16.0 * (double)sp.v[i].ncells * c->g.n * (double)sp.v[i].nlines + 8.0 * (double)sp.v[i].nlines;
     return b;
 }
 
