@@ -21,6 +21,8 @@ import subprocess
 
 import numpy as np
 
+FLUX_LBM = 3  # lattice-Boltzmann isothermal model
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pdg_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
@@ -63,6 +65,7 @@ def lib():
             "or_flux": [ctypes.c_int, ctypes.c_int, pd, pd, pd],
             "or_equilibrium": [ctypes.c_int, ctypes.c_int, pd, pi32, ctypes.c_int, d, ctypes.c_int, pd, pd, pd],
             "or_moments": [ctypes.c_int, pi32, ctypes.c_int, i64, pd, pd],
+            "or_moments_lbm": [ctypes.c_int, ctypes.c_int, pd, i64, pd, pd],
             "or_collide": [ctypes.c_int, ctypes.c_int, pd, pi32, ctypes.c_int, d, ctypes.c_int, pd, d, d, i64, pd],
             "or_equilibrium_field": [ctypes.c_int, ctypes.c_int, pd, pi32, ctypes.c_int, d, ctypes.c_int, pd,
                                      i64, pd, pd],
@@ -122,7 +125,7 @@ class Problem:
     @classmethod
     def from_config(cls, cfg, tau=0.0):
         vel, comp = cfg.velocities()
-        return cls(cfg.dim, cfg.N, cfg.p, vel, comp, cfg.m, cfg.lam, cfg.flux, cfg.fparams, cfg.dt, tau,
+        return cls(cfg.dim, cfg.N, cfg.p, vel, comp, cfg.m, cfg.lam, cfg.flux, cfg.flux_params(), cfg.dt, tau,
                    lo=cfg.lo, hi=cfg.hi)
 
     def mesh(self) -> Mesh:
@@ -289,10 +292,14 @@ def equilibrium_field(pb: Problem, w_nodes: np.ndarray) -> np.ndarray:
 
 
 def moments(pb: Problem, f_nodes: np.ndarray) -> np.ndarray:
+    """w = P f: block sums for the vectorial models, P = [1; v^T] for LBM."""
     f = np.ascontiguousarray(f_nodes, dtype=np.float64)
     nn = f[0].size
     w = np.zeros((pb.m,) + f.shape[1:])
-    _check(lib().or_moments(pb.nv, _pi32(pb.comp), pb.m, nn, _pd(f), _pd(w)), "moments")
+    if pb.flux == FLUX_LBM:
+        _check(lib().or_moments_lbm(pb.dim, pb.nv, _pd(pb.vel), nn, _pd(f), _pd(w)), "moments")
+    else:
+        _check(lib().or_moments(pb.nv, _pi32(pb.comp), pb.m, nn, _pd(f), _pd(w)), "moments")
     return w
 
 

@@ -534,7 +534,39 @@ int or_apply_L(const or_mesh *m, const double *v, const double *f, const double 
 /* ------------------------------------------------------------------------- */
 /* Kinetic model: moments, flux, equilibrium, collision.                      */
 /* ------------------------------------------------------------------------- */
-enum { OR_FLUX_ADVECTION = 0, OR_FLUX_EULER = 1, OR_FLUX_ISOTHERMAL = 2 };
+enum { OR_FLUX_ADVECTION = 0, OR_FLUX_EULER = 1, OR_FLUX_ISOTHERMAL = 2, OR_FLUX_LBM = 3 };
+
+/*
+ * Lattice-Boltzmann isothermal model (the paper's D2Q9; the same formula
+ * for the D3Q15/19/27 lattices of P:856-858): w = P f with P = [1; v^T] (rho = sum f_i,
+ * rho u = sum f_i v_i), and
+ *   f^eq_i = w_i rho (1 + (u.v_i)/c^2 + (u.v_i)^2/(2 c^4) - (u.u)/(2 c^2))
+ * with fp = {c, w_0, ..., w_{nv-1}} (the lattice weights).
+ */
+static void lbm_moments(int dim, int nv, const double *vel, const double *fnode, double *w)
+{
+    for (int c = 0; c <= dim; c++) w[c] = 0.0;
+    for (int i = 0; i < nv; i++) {
+        w[0] += fnode[i];
+        for (int d = 0; d < dim; d++) w[1 + d] += fnode[i] * vel[3 * i + d];
+    }
+}
+
+static void lbm_equilibrium(int dim, int nv, const double *vel, const double *fp, const double *w, double *feq)
+{
+    const double c = fp[0], c2 = c * c;
+    const double rho = w[0];
+    double u[3] = { 0, 0, 0 }, uu = 0.0;
+    for (int d = 0; d < dim; d++) {
+        u[d] = w[1 + d] / rho;
+        uu += u[d] * u[d];
+    }
+    for (int i = 0; i < nv; i++) {
+        double uv = 0.0;
+        for (int d = 0; d < dim; d++) uv += u[d] * vel[3 * i + d];
+        feq[i] = fp[1 + i] * rho * (1.0 + uv / c2 + (uv * uv) / (2.0 * c2 * c2) - uu / (2.0 * c2));
+    }
+}
 
 /*
  * Physical flux q^k(w), k = 0..dim-1, written to q[k*mm + c] (P:161-172 eq
@@ -590,6 +622,10 @@ int or_equilibrium(int dim, int nv, const double *vel, const int32_t *comp, int 
                    int flux, const double *fp, const double *w, double *feq)
 {
     double q[3 * 8];
+    if (flux == OR_FLUX_LBM) {
+        lbm_equilibrium(dim, nv, vel, fp, w, feq);
+        return 0;
+    }
     if (mm > 8) return -1;
     if (or_flux(dim, flux, fp, w, q)) return -1;
     for (int i = 0; i < nv; i++) {
@@ -597,6 +633,19 @@ int or_equilibrium(int dim, int nv, const double *vel, const int32_t *comp, int 
         double vq = 0.0;
         for (int k = 0; k < dim; k++) vq += vel[3 * i + k] * q[k * mm + c];
         feq[i] = w[c] / (2.0 * dim) + vq / (2.0 * lambda * lambda);
+    }
+    return 0;
+}
+
+/* w = P f for the LBM model (P = [1; v^T]), summed in index order. */
+int or_moments_lbm(int dim, int nv, const double *vel, int64_t nnodes, const double *f, double *w)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < nnodes; x++) {
+        double fl[64], wl[4];
+        for (int i = 0; i < nv; i++) fl[i] = f[(int64_t)i * nnodes + x];
+        lbm_moments(dim, nv, vel, fl, wl);
+        for (int c = 0; c <= dim; c++) w[(int64_t)c * nnodes + x] = wl[c];
     }
     return 0;
 }
@@ -627,7 +676,13 @@ int or_collide(int dim, int nv, const double *vel, const int32_t *comp, int mm, 
 #pragma omp parallel for schedule(static) reduction(min : rc)
     for (int64_t x = 0; x < nnodes; x++) {
         double w[8] = { 0, 0, 0, 0, 0, 0, 0, 0 }, feq[64];
-        for (int i = 0; i < nv; i++) w[comp[i]] += f[(int64_t)i * nnodes + x];
+        if (flux == OR_FLUX_LBM) {
+            double fl[64];
+            for (int i = 0; i < nv; i++) fl[i] = f[(int64_t)i * nnodes + x];
+            lbm_moments(dim, nv, vel, fl, w);
+        } else {
+            for (int i = 0; i < nv; i++) w[comp[i]] += f[(int64_t)i * nnodes + x];
+        }
         if (or_equilibrium(dim, nv, vel, comp, mm, lambda, flux, fp, w, feq)) { rc = -1; continue; }
         for (int i = 0; i < nv; i++) {
             double *fi = f + (int64_t)i * nnodes + x;

@@ -25,6 +25,34 @@ import torch
 FLUX_ADVECTION = 0
 FLUX_EULER = 1
 FLUX_ISOTHERMAL = 2
+FLUX_LBM = 3
+
+# Lattice-Boltzmann velocity sets (unit vectors; scaled by lambda) and weights.
+# D2Q9 in the paper's order and with its weights; the 3-D lattices are the
+# standard D3Q15/D3Q19/D3Q27 sets the paper benchmarks.
+def _lattice(name):
+    axis2 = [(1, 0), (0, 1), (-1, 0), (0, -1)]
+    if name == "D2Q9":
+        v = [(0, 0)] + axis2 + [(1, 1), (-1, 1), (-1, -1), (1, -1)]
+        w = [4 / 9] + [1 / 9] * 4 + [1 / 36] * 4
+        return [list(x) + [0] for x in v], w
+    axis3 = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+    edges = [(a, b, 0) for a in (1, -1) for b in (1, -1)] + [(a, 0, b) for a in (1, -1) for b in (1, -1)] + \
+            [(0, a, b) for a in (1, -1) for b in (1, -1)]
+    corners = [(a, b, c) for a in (1, -1) for b in (1, -1) for c in (1, -1)]
+    if name == "D3Q15":
+        return [(0, 0, 0)] + axis3 + corners, [2 / 9] + [1 / 9] * 6 + [1 / 72] * 8
+    if name == "D3Q19":
+        return [(0, 0, 0)] + axis3 + edges, [1 / 3] + [1 / 18] * 6 + [1 / 36] * 12
+    if name == "D3Q27":
+        return [(0, 0, 0)] + axis3 + edges + corners, [8 / 27] + [2 / 27] * 6 + [1 / 54] * 12 + [1 / 216] * 8
+    raise ValueError(name)
+
+
+def lattice(name: str, lam: float):
+    """(velocities [nv][3], weights [nv]) of a lattice scaled by lambda."""
+    v, w = _lattice(name)
+    return [[lam * float(c) for c in x] for x in v], [float(x) for x in w]
 
 MASK64 = (1 << 64) - 1
 
@@ -88,6 +116,7 @@ class Config:
     wb_zero: bool = False   # config 1: inflow f^b = f^eq(0) = 0
     lo: tuple = (0.0, 0.0, 0.0)
     hi: tuple = (1.0, 1.0, 1.0)
+    lattice: str = ""       # LBM lattice name (flux == FLUX_LBM); fparams = (c,) then
 
     @property
     def n(self) -> int:
@@ -95,6 +124,8 @@ class Config:
 
     @property
     def nv(self) -> int:
+        if self.lattice:
+            return len(_lattice(self.lattice)[1])
         return self.m * 2 * self.dim
 
     @property
@@ -115,7 +146,16 @@ class Config:
         return self.nnodes * self.nv
 
     def velocities(self):
+        if self.lattice:
+            v, _ = lattice(self.lattice, self.lam)
+            return v, [0] * len(v)
         return velocity_set(self.dim, self.m, self.lam)
+
+    def flux_params(self):
+        """Model parameters as both sides take them: LBM -> (c, w_0..w_{nv-1})."""
+        if self.lattice:
+            return tuple(self.fparams) + tuple(lattice(self.lattice, self.lam)[1])
+        return tuple(self.fparams)
 
     def resized(self, N: int, steps: int | None = None, name: str | None = None) -> "Config":
         """Same recipe and CFL number nu = lambda dt / h on an N-cell grid."""
@@ -142,6 +182,16 @@ CONFIGS = {
     5: Config("cfg5_iso3d_scale", 3, 256, 2, 4, 2.0, FLUX_ISOTHERMAL, (1.0,), 1.0 / 256.0, 10,
               0x5EED0005, "iso3d_multimode"),
 }
+
+
+def lbm_config(lattice_name: str, N: int, p: int = 2, lam: float = 1.0, nu: float = 0.5, steps: int = 4,
+               seed: int = 0x5EED0009) -> Config:
+    """An isothermal LBM workload (NEXT-2): c = lambda/sqrt(3), density pulse plus a
+    small seeded vortical velocity; inflow data f^eq(w0(x_b))."""
+    dim = 2 if lattice_name.startswith("D2") else 3
+    h = 1.0 / N
+    return Config(f"lbm_{lattice_name}_N{N}", dim, N, p, dim + 1, lam, FLUX_LBM, (lam / math.sqrt(3.0),),
+                  nu * h / lam, steps, seed, "lbm_pulse", lattice=lattice_name)
 
 
 def node_axis(cfg: Config, axis: int, dtype=torch.float64, device="cpu") -> torch.Tensor:
@@ -191,6 +241,16 @@ def _fields(cfg: Config, X, Y, Z):
                 ud = ud + 0.02 * torch.sin(two_pi * (k + 1) * coords[(d + 1) % 3] + psi[k][d])
             vel.append(ud)
         return [rho, rho * vel[0], rho * vel[1], rho * vel[2]]
+    if cfg.recipe == "lbm_pulse":
+        ph = phases(cfg.seed, 3)
+        r2 = (X - 0.5) ** 2 + (Y - 0.5) ** 2 + ((Z - 0.5) ** 2 if cfg.dim == 3 else 0.0)
+        rho = 1.0 + 0.05 * torch.exp(-50.0 * r2)
+        u = 0.02 * cfg.lam * torch.sin(two_pi * Y + ph[0])
+        v = 0.02 * cfg.lam * torch.sin(two_pi * X + ph[1])
+        out = [rho, rho * u, rho * v]
+        if cfg.dim == 3:
+            out.append(rho * 0.02 * cfg.lam * torch.sin(two_pi * X + ph[2]) * torch.cos(two_pi * Y))
+        return out
     raise ValueError(cfg.recipe)
 
 

@@ -512,3 +512,65 @@ def test_palindromic_composition_orders(scheme, tau, order):
     errs = [np.max(np.abs(run(s) - ref)) for s in (16, 32, 64)]
     slopes = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
     assert all(abs(s - order) < 0.15 for s in slopes), (errs, slopes)
+
+
+# --------------------------------------------------------------------------
+# Lattice-Boltzmann models (NEXT-2)
+# --------------------------------------------------------------------------
+def test_d2q9_matches_paper(golden):
+    from pdg_inputs import lattice
+    g = golden("d2q9.json")
+    lam = 1.7
+    v, w = lattice("D2Q9", lam)
+    assert [[x / lam for x in vi[:2]] for vi in v] == g["velocities_unit"]
+    np.testing.assert_allclose(w, [_val(x) for x in g["weights"]], atol=1e-16)
+    P = np.vstack([np.ones(9), np.array(v)[:, :2].T])
+    np.testing.assert_allclose(P, np.array(g["P_rows_unit"]) * np.array([[1.0], [lam], [lam]]), atol=0)
+
+
+@pytest.mark.parametrize("lat", ["D2Q9", "D3Q15", "D3Q19", "D3Q27"])
+def test_lbm_equilibrium_moments(lat):
+    """P f^eq = w (rho, rho u conserved) and the second moment is the isothermal
+    Euler flux Pi = rho c^2 I + rho u u; at rest f^eq_i = w_i rho."""
+    from pdg_inputs import lbm_config
+    cfg = lbm_config(lat, 2, lam=1.3)
+    pb = O.Problem.from_config(cfg)
+    D = cfg.dim
+    rng = np.random.default_rng(8)
+    c2 = (cfg.lam / math.sqrt(3.0)) ** 2
+    P = np.vstack([np.ones(pb.nv), pb.vel[:, :D].T])
+    for _ in range(5):
+        rho = 0.5 + rng.random()
+        u = 0.1 * (rng.random(D) - 0.5)
+        w = np.concatenate([[rho], rho * u])
+        feq = O.equilibrium(pb, w)
+        np.testing.assert_allclose(P @ feq, w, atol=1e-15)
+        Pi = np.einsum("i,ia,ib->ab", feq, pb.vel[:, :D], pb.vel[:, :D])
+        np.testing.assert_allclose(Pi, rho * c2 * np.eye(D) + rho * np.outer(u, u), atol=2e-15)
+    feq = O.equilibrium(pb, np.concatenate([[1.3], np.zeros(D)]))
+    np.testing.assert_allclose(feq, 1.3 * np.array(cfg.flux_params()[1:]), atol=1e-15)
+
+
+def test_lbm_collision_conserves_and_m2_order():
+    from pdg_inputs import lbm_config, w0_grid, wb_grid
+    cfg = lbm_config("D2Q9", 6)
+    pb = O.Problem.from_config(cfg)
+    rng = np.random.default_rng(3)
+    f = O.equilibrium_field(pb, w0_grid(cfg).numpy()) * (1 + 0.01 * rng.standard_normal((9,) + cfg.grid_shape))
+    f = np.ascontiguousarray(f)
+    w0 = O.moments(pb, f)
+    O.collide(pb, f, cfg.dt)
+    assert np.max(np.abs(O.moments(pb, f) - w0)) < 1e-14
+    # second order in time of M2 on the D2Q9 model (diagonal transports included)
+    base = lbm_config("D2Q9", 8)
+    w0 = w0_grid(base).numpy()
+
+    def run(nsteps):
+        p2 = O.Problem.from_config(base)
+        p2.dt = 0.1 / nsteps
+        f0, fb = O.initial_data(p2, w0, wb_grid(base, w0_grid(base)).numpy())
+        return O.moments(p2, O.m2_run(p2, f0, fb, nsteps))
+    ref = run(256)
+    errs = [np.max(np.abs(run(s) - ref)) for s in (8, 16, 32)]
+    slopes = [math.log2(errs[k] / errs[k + 1]) for k in range(2)]
+    assert all(1.85 <= s <= 2.15 for s in slopes), (errs, slopes)
