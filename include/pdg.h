@@ -37,12 +37,18 @@
  *  - fb: [nv_local][plane_stride]; velocity i (axis k_i) stores its inflow
  *        plane = the node grid with axis k_i removed, in the same order
  *        (e.g. axis y in 3-D: [Z][X]); plane_stride = max over axes.
+ *        PDG_FLUX_LBM (lattice sets): [nv_local][dim][plane_stride]: plane k of velocity i is
+ *        its inflow face across axis k (lo face if v_i^k > 0, hi face if v_i^k < 0), same
+ *        order as above; planes of axes with v_i^k = 0 are unused.
  *  - w:  [m][Z][Y][X]   (the rank's planes with PDG_DECOMP_ZSLAB)
  *
  * Velocity set: the vectorial D2Q4 / D3Q6-per-component set (reading C6):
  *   velocity i = c*2D + 2k + s has v_i = (s ? -lambda : +lambda) e_k and
  *   belongs to component c (P = block sums).  Any other set is rejected with
- *   PDG_E_VELOCITY_SET.
+ *   PDG_E_VELOCITY_SET -- except with PDG_FLUX_LBM, which takes a lattice set
+ *   (components in {0, +-lambda}, e.g. the paper's D2Q9): velocities with
+ *   several non-zero components are swept along genuinely diagonal wavefronts with the
+ *   dense (p+1)^d local block (NEXT-2).
  */
 #ifndef PDG_H
 #define PDG_H
@@ -75,7 +81,14 @@ typedef enum {
 typedef enum {
     PDG_FLUX_LINEAR_ADVECTION = 0, /* m = 1:      q^k = a_k w;                      flux_params = a[dim] */
     PDG_FLUX_EULER = 1,            /* m = dim+2:  compressible Euler, w = (rho, rho u, E); flux_params = {gamma} */
-    PDG_FLUX_ISOTHERMAL = 2        /* m = dim+1:  w = (rho, rho u), p = c^2 rho;    flux_params = {c} */
+    PDG_FLUX_ISOTHERMAL = 2,       /* m = dim+1:  w = (rho, rho u), p = c^2 rho;    flux_params = {c} */
+    PDG_FLUX_LBM = 3               /* m = dim+1:  lattice-Boltzmann isothermal model (NEXT-2):
+                                      w = P f with P = [1; v^T] (rho = sum f_i, rho u = sum f_i v_i),
+                                      f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2));
+                                      flux_params = {c, w_0, ..., w_{nv-1}} (n_flux_params = 1 + nv);
+                                      the velocity set is any lattice with components in {0, +-lambda}:
+                                      D2Q9 (nv = 9), D3Q15/D3Q19/D3Q27 (nv = 15/19/27) are compiled;
+                                      comp[] is ignored (may be NULL) */
 } pdg_flux;
 
 typedef enum {
@@ -116,7 +129,8 @@ typedef enum {
     PDG_K_OTHER = 6,         /* initialisation / checks */
     PDG_K_RELAX_X = 7,       /* collision fused with moments and the following x-velocity sweep(s) */
     PDG_K_ZSLAB = 8,         /* z-slab carry scan + correction (and the carry all-gather) */
-    PDG_NUM_KERNEL_KINDS = 9
+    PDG_K_LATTICE = 9,       /* T2 sweeps of lattice velocities with >= 2 non-zero components (NEXT-2) */
+    PDG_NUM_KERNEL_KINDS = 10
 } pdg_kernel_kind;
 
 typedef struct {

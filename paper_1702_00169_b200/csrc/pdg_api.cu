@@ -15,7 +15,12 @@
 #include "../../include/pdg.h"
 #include "pdg_comm.hpp"
 #include "pdg_kernels.cuh"
+#include "pdg_lattice.cuh"
 #include "pdg_tables.hpp"
+
+#include <cstdlib>
+#include <map>
+#include <utility>
 
 #ifndef PDG_VERSION
 #define PDG_VERSION "0.1.0"
@@ -58,7 +63,80 @@ struct Geometry {
     int64_t slab_begin[kMaxSlabs + 1] = {0};  // global cell plane where slab s starts
     size_t carry_doubles = 0;                 // one carry/inflow buffer (doubles)
     size_t table_doubles = 0;                 // one correction table (doubles)
+    // lattice velocity sets (PDG_FLUX_LBM, NEXT-2)
+    int lattice = 0;                          // 1: general velocities, fb = [nvl][dim][plane_stride]
+    int nplanes = 1;                          // inflow planes per velocity in fb
+    size_t lat_ints = 0;                      // ticket + progress counters (max over classes)
+    size_t lat_xbuf = 0, lat_ybuf = 0;        // boundary trace buffers (doubles, max over classes)
 };
+
+// Work decomposition of one active-axis class of lattice velocities (pdg_lattice.cuh).
+struct LatPlan {
+    int act = 0, d = 0, nvel = 0;
+    int vel[pdg::kLatMaxVel] = {0};  // local velocity indices
+    int Wx = 1, Wy = 1, ngx = 1, ngy = 1, nlane = 1, nw = 1, nc = 1, ntasks = 0;
+    size_t xbuf = 0, ybuf = 0;       // doubles
+};
+
+int popcount3(int a) { return (a & 1) + ((a >> 1) & 1) + ((a >> 2) & 1); }
+
+void plan_lattice(const Geometry &g, LatPlan &P)
+{
+    const int D = g.dim, act = P.act;
+    const int XA = act & 1, YA = (act >> 1) & 1, ZA = (D == 3) ? ((act >> 2) & 1) : 0;
+    const int CA = ZA ? 2 : 1;
+    const int PIPE = (D == 3 && ZA && YA) ? 1 : 0;
+    const int BA = (D == 3 && !ZA) ? 2 : ((D == 3 && !YA) ? 1 : -1);
+    P.d = XA + YA + ZA;
+    P.nlane = (int)(XA ? g.ncell[0] : g.L[0]);
+    P.nw = (int)(PIPE ? g.ncell[1] : (BA >= 0 ? g.L[BA] : 1));
+    P.nc = (int)g.ncell[CA];
+    P.Wx = std::min(8, (P.nlane + 31) / 32);
+    P.Wy = std::max(1, std::min(8 / P.Wx, P.nw));
+    // test knob: force small CTAs so that the cross-CTA hand-over paths run on small grids
+    if (const char *e = std::getenv("PDG_LATTICE_WARPS")) {
+        int wx = 0, wy = 0;
+        if (std::sscanf(e, "%d,%d", &wx, &wy) == 2 && wx >= 1 && wy >= 1 && wx * wy <= 8) {
+            P.Wx = std::min(wx, std::max(1, (P.nlane + 31) / 32));
+            P.Wy = std::min(wy, P.nw);
+        }
+    }
+    P.ngx = (P.nlane + 32 * P.Wx - 1) / (32 * P.Wx);
+    P.ngy = (P.nw + P.Wy - 1) / P.Wy;
+    P.ntasks = P.nvel * P.ngx * P.ngy;
+    int mf = 1;
+    for (int t = 1; t < P.d; ++t) mf *= g.n;
+    P.xbuf = (XA && P.ngx > 1) ? (size_t)P.ntasks * P.nc * P.Wy * mf : 0;
+    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)P.ntasks * P.nc * P.Wx * 32 * mf : 0;
+}
+
+// Active-axis mask of a lattice velocity (bit k set if v_k != 0).
+int act_mask(const double *v, int dim)
+{
+    int a = 0;
+    for (int k = 0; k < dim; ++k)
+        if (v[k] != 0.0) a |= 1 << k;
+    return a;
+}
+
+void lattice_classes(const Geometry &g, const double *vel, std::vector<LatPlan> &out)
+{
+    out.clear();
+    for (int j = 0; j < g.nvl; ++j) {
+        const int act = act_mask(vel + 3 * (g.v0 + j), g.dim);
+        if (popcount3(act) < 2) continue;
+        LatPlan *pl = nullptr;
+        for (auto &q : out)
+            if (q.act == act && q.nvel < pdg::kLatMaxVel) pl = &q;
+        if (!pl) {
+            out.emplace_back();
+            pl = &out.back();
+            pl->act = act;
+        }
+        pl->vel[pl->nvel++] = j;
+    }
+    for (auto &q : out) plan_lattice(g, q);
+}
 
 constexpr int kMaxTables = 16;
 
@@ -114,16 +192,39 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
         m_expect = p->dim + 1;
         if (!p->flux_params || p->n_flux_params < 1 || !(p->flux_params[0] > 0.0))
             return fail(PDG_E_FLUX_MODEL, "isothermal needs flux_params = {c > 0}");
+    } else if (p->flux == PDG_FLUX_LBM) {
+        m_expect = p->dim + 1;
+        if (!p->flux_params || p->n_flux_params < 1 + p->nv || !(p->flux_params[0] > 0.0))
+            return fail(PDG_E_FLUX_MODEL, "LBM needs flux_params = {c > 0, w_0 .. w_{nv-1}}");
     } else {
         return fail(PDG_E_FLUX_MODEL, "unknown flux model");
     }
     if (p->m != m_expect) return fail(PDG_E_FLUX_MODEL, "m does not match the flux model");
     g->m = p->m;
 
+    if (p->flux == PDG_FLUX_LBM) {
+        // lattice velocity set (NEXT-2): components in {0, +-lambda}
+        g->lattice = 1;
+        g->nplanes = p->dim;
+        if (!p->vel) return fail(PDG_E_INVALID_ARGUMENT, "vel is NULL");
+        const bool nv_ok = (p->dim == 2) ? (p->nv == 9) : (p->nv == 15 || p->nv == 19 || p->nv == 27);
+        if (!nv_ok) return fail(PDG_E_UNSUPPORTED, "LBM lattices compiled: D2Q9, D3Q15, D3Q19, D3Q27");
+        for (int i = 0; i < p->nv; ++i) {
+            for (int d = 0; d < 3; ++d) {
+                const double v = p->vel[3 * i + d];
+                const bool ok = (d < p->dim) ? (v == 0.0 || v == p->lambda || v == -p->lambda) : (v == 0.0);
+                if (!ok) return fail(PDG_E_VELOCITY_SET, "lattice velocity components must be 0 or +-lambda");
+            }
+            if (popcount3(act_mask(p->vel + 3 * i, p->dim)) == 3 && p->degree == 3)
+                return fail(PDG_E_UNSUPPORTED, "p = 3 with body-diagonal velocities (64x64 block) is not compiled");
+        }
+        if (p->decomposition == PDG_DECOMP_ZSLAB && p->nranks * std::max(1, p->slabs_per_rank) > 1)
+            return fail(PDG_E_UNSUPPORTED, "the z-slab decomposition is implemented for axis-aligned sets only");
+    } else {
     // velocity set: canonical vectorial D2Q4 / D3Q6 per component (reading C6)
     if (p->nv != p->m * 2 * p->dim) return fail(PDG_E_VELOCITY_SET, "nv must be m * 2 * dim");
     if (p->nv > pdg::kMaxVel) return fail(PDG_E_VELOCITY_SET, "too many velocities");
-    if (!p->vel || !p->comp) return fail(PDG_E_INVALID_ARGUMENT, "vel/comp are NULL");
+    if (!p->vel || !p->comp) return fail(PDG_E_INVALID_ARGUMENT, "vel/comp are NULL");  // comp optional for LBM
     for (int i = 0; i < p->nv; ++i) {
         const int c = i / (2 * p->dim), k = (i % (2 * p->dim)) / 2, s = i % 2;
         if (p->comp[i] != c) return fail(PDG_E_VELOCITY_SET, "comp[i] must be i / (2 dim)");
@@ -134,6 +235,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
                                                     " must be (s ? -lambda : lambda) e_k, i = c*2D + 2k + s");
         }
     }
+    }
     g->nv = p->nv;
     g->gnnodes = g->nnodes;
     if (p->decomposition == PDG_DECOMP_VELOCITY) {
@@ -141,6 +243,15 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
         g->nvl = p->nv / p->nranks;
         g->v0 = p->rank * g->nvl;
         g->gncell_outer = g->ncell[p->dim - 1];
+        if (g->lattice) {
+            std::vector<LatPlan> cls;
+            lattice_classes(*g, p->vel, cls);
+            for (const auto &q : cls) {
+                g->lat_ints = std::max(g->lat_ints, (size_t)q.ntasks + 1);
+                g->lat_xbuf = std::max(g->lat_xbuf, q.xbuf);
+                g->lat_ybuf = std::max(g->lat_ybuf, q.ybuf);
+            }
+        }
         return PDG_OK;
     }
     if (p->decomposition != PDG_DECOMP_ZSLAB) return fail(PDG_E_INVALID_ARGUMENT, "unknown decomposition");
@@ -179,17 +290,20 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     return PDG_OK;
 }
 
+size_t lat_ints_bytes(const Geometry &g) { return ((g.lat_ints * sizeof(int) + 255) / 256) * 256; }
+
 size_t work_bytes_of(const Geometry &g)
 {
     size_t b = 256;
     if (g.zslab) b += sizeof(double) * (2 * g.carry_doubles + kMaxTables * g.table_doubles);
+    if (g.lattice) b += lat_ints_bytes(g) + sizeof(double) * (g.lat_xbuf + g.lat_ybuf);
     return b;
 }
 
 void fill_sizes(const Geometry &g, pdg_sizes *out)
 {
     out->f_elems = (size_t)g.nvl * (size_t)g.nnodes;
-    out->fb_elems = (size_t)g.nvl * (size_t)g.plane_stride;
+    out->fb_elems = (size_t)g.nvl * (size_t)g.nplanes * (size_t)g.plane_stride;
     out->w_elems = (size_t)g.m * (size_t)g.nnodes;
     out->work_bytes = work_bytes_of(g);
     out->nnodes = g.gnnodes;
@@ -243,6 +357,12 @@ struct pdg_ctx {
         std::vector<double> B, C;  // by slab length
     };
     std::vector<ZTable> ztables_host;
+    // lattice velocity sets (NEXT-2)
+    std::vector<LatPlan> lat_plans;            // one per active-axis class with >= 2 active axes
+    pdg::LbmParams lbm{};
+    int *lat_ints = nullptr;                   // ticket + progress counters
+    double *lat_xbuf = nullptr, *lat_ybuf = nullptr;
+    std::map<std::pair<int, double>, pdg::LatticeBlockLD> lat_blocks;  // (act, dt') -> block
 };
 
 namespace {
@@ -359,6 +479,106 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
     }
 }
 
+// ---- lattice sweeps (NEXT-2) ------------------------------------------------------------
+const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
+{
+    const auto key = std::make_pair(act, dtp);
+    auto it = c->lat_blocks.find(key);
+    if (it != c->lat_blocks.end()) return &it->second;
+    long double kap[3] = {0, 0, 0};
+    int d = 0;
+    for (int k = 0; k < c->g.dim; ++k)
+        if (act & (1 << k)) kap[d++] = (long double)c->prob.lambda * (long double)dtp / (long double)c->g.h[k];
+    pdg::LatticeBlockLD B;
+    if (!pdg::lattice_block(c->g.p, d, kap, &B)) return nullptr;
+    return &(c->lat_blocks[key] = std::move(B));
+}
+
+template <int D, int N, int ACT>
+pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B)
+{
+    using PP = pdg::LatParams<D, N, ACT>;
+    using TB = pdg::LatTab<N, pdg::LatShape<D, ACT>::DA>;
+    constexpr int DA = pdg::LatShape<D, ACT>::DA;
+    std::vector<char> mem(sizeof(PP), 0);
+    PP &P = *reinterpret_cast<PP *>(mem.data());
+    const Geometry &g = c->g;
+    P.f = c->f;
+    P.fb = c->fb;
+    P.ticket = c->lat_ints;
+    P.progress = c->lat_ints + 1;
+    P.xbuf = c->lat_xbuf;
+    P.ybuf = c->lat_ybuf;
+    for (int k = 0; k < 3; ++k) {
+        P.g.L[k] = g.L[k];
+        P.g.stride[k] = g.stride[k];
+        P.g.ncell[k] = (int32_t)g.ncell[k];
+    }
+    P.g.plane_stride = g.plane_stride;
+    P.g.Wx = pl.Wx;
+    P.g.Wy = pl.Wy;
+    P.g.ngx = pl.ngx;
+    P.g.ngy = pl.ngy;
+    P.g.nlane = pl.nlane;
+    P.g.nw = pl.nw;
+    P.g.nc = pl.nc;
+    P.g.ntasks = pl.ntasks;
+    P.g.nvel = pl.nvel;
+    for (int q = 0; q < pl.nvel; ++q) {
+        const int j = pl.vel[q];
+        const double *v = c->vel.data() + 3 * (g.v0 + j);
+        P.v[q].f_off = (int64_t)j * g.nnodes;
+        P.v[q].fb_off = (int64_t)j * g.dim * g.plane_stride;
+        for (int k = 0; k < 3; ++k) P.v[q].sign[k] = (v[k] < 0.0) ? -1 : 1;
+    }
+    for (int t = 0; t < DA; ++t) {
+        for (int i = 0; i < N * N; ++i) P.tab.KG[t][i] = (double)(B.kappa[t] * B.G[i]);
+        P.tab.cin[t] = (double)(B.kappa[t] / B.w0);
+    }
+    for (int i = 0; i < TB::NB * TB::NB; ++i) P.tab.Ainv[i] = (double)B.Ainv[i];
+    for (int i = 0; i < TB::NB * TB::MF; ++i) P.tab.Qx[i] = (double)B.Qx[i];
+    for (int s = 0; s < 5; ++s)
+        for (int i = 0; i < TB::MF * TB::MF; ++i) P.tab.Bp[s][i] = (double)B.Bpow[(size_t)s * TB::MF * TB::MF + i];
+    const int threads = 32 * pl.Wx * pl.Wy;
+    static std::map<int, int> occ_cache;
+    int occ = 0;
+    auto oc = occ_cache.find(threads);
+    if (oc != occ_cache.end()) occ = oc->second;
+    else {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT>, threads, 0) !=
+            cudaSuccess)
+            occ = 1;
+        occ = std::max(1, occ);
+        occ_cache[threads] = occ;
+    }
+    const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
+    PDG_CUDA_TRY(cudaMemsetAsync(c->lat_ints, 0, sizeof(int) * ((size_t)pl.ntasks + 1), c->stream));
+    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, 0, c->stream>>>(P);
+    return PDG_OK;
+}
+
+pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp)
+{
+    const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, dtp);
+    if (!B) return fail(PDG_E_INVALID_ARGUMENT, "singular lattice block for this dt");
+    const int D = c->g.dim, n = c->g.n, a = pl.act;
+    const int e = prof_begin(c);
+    pdg_status s = PDG_E_UNSUPPORTED;
+#define PDG_LAT(DD, NN, AA) \
+    else if (D == DD && n == NN && a == AA) s = launch_lattice_t<DD, NN, AA>(c, pl, *B)
+    if (false) {}
+    PDG_LAT(2, 2, 3); PDG_LAT(2, 3, 3); PDG_LAT(2, 4, 3);
+    PDG_LAT(3, 2, 3); PDG_LAT(3, 3, 3); PDG_LAT(3, 4, 3);
+    PDG_LAT(3, 2, 5); PDG_LAT(3, 3, 5); PDG_LAT(3, 4, 5);
+    PDG_LAT(3, 2, 6); PDG_LAT(3, 3, 6); PDG_LAT(3, 4, 6);
+    PDG_LAT(3, 2, 7); PDG_LAT(3, 3, 7);
+#undef PDG_LAT
+    if (s == PDG_E_UNSUPPORTED) return fail(s, "lattice sweep not compiled for this (dim, degree, axes)");
+    if (s != PDG_OK) return s;
+    prof_end(c, e, PDG_K_LATTICE, 16.0 * (double)pl.nvel * (double)c->g.nnodes);
+    return post_launch(c, "lattice_sweep");
+}
+
 // One pass over f applying T2(dtp) npass times (npass in {1, 2}) to the selected velocities.
 pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_ALL)
 {
@@ -396,6 +616,12 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_A
     }
     pdg_status s = post_launch(c, "sweep");
     if (s == PDG_OK && outer) s = zslab_resolve(c, dtp, npass);
+    if (which != SWEEP_X)
+        for (int q = 0; q < npass && s == PDG_OK; ++q)
+            for (const LatPlan &pl : c->lat_plans) {
+                s = launch_lattice(c, pl, dtp);
+                if (s != PDG_OK) break;
+            }
     return s;
 }
 
@@ -506,6 +732,70 @@ void launch_equilibrium_t(pdg_ctx *c, const double *w, const double *wb)
         else FN<3, pdg::MODEL_ISO>(__VA_ARGS__);                                                    \
     } while (0)
 
+// ---- LBM model kernels (lattice sets, NEXT-2) ------------------------------------------
+template <int D, int NV>
+void launch_relax_lbm_t(pdg_ctx *c, double ca, double cb)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, ca, cb);
+    prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
+}
+
+template <int D, int NV>
+void launch_partial_lbm_t(pdg_ctx *c)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::partial_moments_lbm_kernel<D, NV>
+        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm);
+    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)c->g.nnodes);
+}
+
+template <int D, int NV>
+void launch_relax_from_w_lbm_t(pdg_ctx *c, double ca, double cb)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    const int e = prof_begin(c);
+    pdg::relax_from_w_lbm_kernel<D, NV>
+        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm, ca, cb);
+    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)c->g.nnodes);
+}
+
+// f = f^eq(w) (f_only) or, additionally, the inflow planes fb from f^eq(wb)
+template <int D, int NV>
+void launch_equilibrium_lbm_t(pdg_ctx *c, const double *w, const double *wb, bool f_only)
+{
+    const int grid = grid_for(c->g.nnodes, 256);
+    if (w) pdg::equilibrium_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm);
+    if (f_only) return;
+    pdg::LatInflowParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.fb = c->fb;
+    P.wb = wb;
+    P.nnodes = c->g.nnodes;
+    P.plane_stride = c->g.plane_stride;
+    for (int k = 0; k < 3; ++k) {
+        P.L[k] = c->g.L[k];
+        P.stride[k] = c->g.stride[k];
+    }
+    P.v0 = c->g.v0;
+    P.nvl = c->g.nvl;
+    P.dim = D;
+    P.lbm = c->lbm;
+    dim3 g2((unsigned)((c->g.plane_stride + 255) / 256), (unsigned)c->g.nvl, (unsigned)D);
+    pdg::lattice_inflow_kernel<D, NV><<<g2, 256, 0, c->stream>>>(P);
+}
+
+#define PDG_LBM_DISPATCH(FN, ...)                                                                   \
+    do {                                                                                            \
+        const int d_ = c->g.dim, nv_ = c->g.nv;                                                     \
+        if (d_ == 2) FN<2, 9>(__VA_ARGS__);                                                         \
+        else if (nv_ == 15) FN<3, 15>(__VA_ARGS__);                                                 \
+        else if (nv_ == 19) FN<3, 19>(__VA_ARGS__);                                                 \
+        else FN<3, 27>(__VA_ARGS__);                                                                \
+    } while (0)
+
 void collision_coeffs(const pdg_ctx *c, double dt, double *ca, double *cb)
 {
     const double tau = c->prob.tau;
@@ -526,7 +816,8 @@ bool sharded(const pdg_ctx *c)
 
 pdg_status partial_and_reduce(pdg_ctx *c)
 {
-    PDG_DISPATCH(launch_partial_t, c);
+    if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
+    else PDG_DISPATCH(launch_partial_t, c);
     pdg_status s = post_launch(c, "partial_moments");
     if (s != PDG_OK) return s;
     if (sharded(c)) {
@@ -546,12 +837,14 @@ pdg_status collide(pdg_ctx *c, double dt)
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
     if (!sharded(c)) {
-        PDG_DISPATCH(launch_relax_t, c, ca, cb);
+        if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_lbm_t, c, ca, cb);
+        else PDG_DISPATCH(launch_relax_t, c, ca, cb);
         return post_launch(c, "relax");
     }
     pdg_status s = partial_and_reduce(c);
     if (s != PDG_OK) return s;
-    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, ca, cb);
+    else PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
     return post_launch(c, "relax_from_w");
 }
 
@@ -583,7 +876,7 @@ pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
 
 bool use_relax_x(const pdg_ctx *c)
 {
-    return !sharded(c) && !(c->prob.flags & PDG_NO_FUSION) && relax_x_smem(c) <= 110 * 1024 &&
+    return !c->g.lattice && !sharded(c) && !(c->prob.flags & PDG_NO_FUSION) && relax_x_smem(c) <= 110 * 1024 &&
            c->g.nnodes / (c->g.ncell[0] * c->g.n) < (int64_t)1 << 31;
 }
 
@@ -667,6 +960,32 @@ void build_sweep_params(pdg_ctx *c)
     for (auto *sp : {&c->x_params, &c->yz_params, &c->all_params}) {
         sp->f = c->f;
         sp->fb = c->fb;
+    }
+    if (g.lattice) {
+        // lattice set: single-axis velocities take the line sweeps, diagonal ones the
+        // lattice kernel (lattice_classes), the rest velocity v = 0 is transported by the identity
+        for (int j = 0; j < g.nvl; ++j) {
+            const int i = g.v0 + j;
+            const double *v = c->vel.data() + 3 * i;
+            const int act = act_mask(v, g.dim);
+            if (popcount3(act) != 1) continue;
+            const int k = (act == 1) ? 0 : (act == 2 ? 1 : 2);
+            pdg::SweepVel V{};
+            V.f_off = (int64_t)j * g.nnodes;
+            V.fb_off = ((int64_t)j * g.dim + k) * g.plane_stride;
+            V.inner = g.stride[k];
+            V.nlines = g.nnodes / g.L[k];
+            V.ncells = (int32_t)g.ncell[k];
+            V.sign = v[k] > 0.0 ? 1 : -1;
+            V.axis = k;
+            V.vel = i;
+            V.cout_off = -1;
+            V.zero_inflow = 0;
+            if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
+            else c->yz_params.v[c->yz_params.nvel++] = V;
+        }
+        lattice_classes(g, c->vel.data(), c->lat_plans);
+        return;
     }
     for (int j = 0; j < g.nvl; ++j) {
         const int i = g.v0 + j;
@@ -884,7 +1203,8 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     c->g = g;
     c->prob = *p;
     c->vel.assign(p->vel, p->vel + 3 * p->nv);
-    c->comp.assign(p->comp, p->comp + p->nv);
+    if (p->comp) c->comp.assign(p->comp, p->comp + p->nv);
+    else c->comp.assign(p->nv, 0);
     for (int i = 0; i < p->n_flux_params && i < 3; ++i) c->fparams[i] = p->flux_params[i];
     c->prob.vel = c->vel.data();
     c->prob.comp = c->comp.data();
@@ -904,6 +1224,20 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     if (p->flux == PDG_FLUX_ISOTHERMAL) c->mp.c2 = p->flux_params[0] * p->flux_params[0];
     c->mp.inv2D = 1.0 / (2.0 * p->dim);
     c->mp.inv2lam = 1.0 / (2.0 * p->lambda);
+    if (c->g.lattice) {
+        const double cc = p->flux_params[0];
+        for (int i = 0; i < p->nv; ++i) {
+            for (int d = 0; d < 3; ++d) c->lbm.v[i][d] = p->vel[3 * i + d];
+            c->lbm.wgt[i] = p->flux_params[1 + i];
+        }
+        c->lbm.inv_c2 = 1.0 / (cc * cc);
+        c->lbm.inv_2c4 = 1.0 / (2.0 * cc * cc * cc * cc);
+        c->lbm.inv_2c2 = 1.0 / (2.0 * cc * cc);
+        char *base = static_cast<char *>(work_dev) + 256;
+        c->lat_ints = reinterpret_cast<int *>(base);
+        c->lat_xbuf = reinterpret_cast<double *>(base + lat_ints_bytes(c->g));
+        c->lat_ybuf = c->lat_xbuf + c->g.lat_xbuf;
+    }
     if (c->g.zslab) {
         c->zcarry = reinterpret_cast<double *>(static_cast<char *>(work_dev) + 256);
         c->zinflow = c->zcarry + c->g.carry_doubles;
@@ -957,7 +1291,8 @@ pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_d
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (f) PDG_CUDA_TRY(cudaMemcpyAsync(c->f, f, sizeof(double) * c->g.nvl * c->g.nnodes, kind, c->stream));
     if (fb)
-        PDG_CUDA_TRY(cudaMemcpyAsync(c->fb, fb, sizeof(double) * c->g.nvl * c->g.plane_stride, kind, c->stream));
+        PDG_CUDA_TRY(cudaMemcpyAsync(c->fb, fb, sizeof(double) * c->g.nvl * c->g.nplanes * c->g.plane_stride, kind,
+                                     c->stream));
     if (!on_device || (c->prob.flags & PDG_SYNC_ERRORS)) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->state_set = true;
     return PDG_OK;
@@ -968,6 +1303,25 @@ pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, in
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!w) return fail(PDG_E_INVALID_ARGUMENT, "w is NULL");
     const size_t wbytes = sizeof(double) * c->g.m * c->g.nnodes;
+    if (c->g.lattice) {
+        if (!on_device) {
+            PDG_CUDA_TRY(cudaMemcpyAsync(c->w, wb ? wb : w, wbytes, cudaMemcpyHostToDevice, c->stream));
+            PDG_LBM_DISPATCH(launch_equilibrium_lbm_t, c, wb ? nullptr : c->w, c->w, false);
+            if (wb) {
+                PDG_CUDA_TRY(cudaMemcpyAsync(c->w, w, wbytes, cudaMemcpyHostToDevice, c->stream));
+                PDG_LBM_DISPATCH(launch_equilibrium_lbm_t, c, c->w, nullptr, true);
+            }
+            pdg_status s = post_launch(c, "equilibrium");
+            if (s != PDG_OK) return s;
+            PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        } else {
+            PDG_LBM_DISPATCH(launch_equilibrium_lbm_t, c, w, wb ? wb : w, false);
+            pdg_status s = post_launch(c, "equilibrium");
+            if (s != PDG_OK) return s;
+        }
+        c->state_set = true;
+        return PDG_OK;
+    }
     if (!on_device) {
         // stage through w_dev: inflow data first (from wb), then the interior (from w)
         PDG_CUDA_TRY(cudaMemcpyAsync(c->w, wb ? wb : w, wbytes, cudaMemcpyHostToDevice, c->stream));
@@ -1026,7 +1380,8 @@ pdg_status pdg_collide(pdg_ctx *c, double dt)
 pdg_status pdg_partial_moments(pdg_ctx *c)
 {
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
-    PDG_DISPATCH(launch_partial_t, c);
+    if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
+    else PDG_DISPATCH(launch_partial_t, c);
     return post_launch(c, "partial_moments");
 }
 
@@ -1035,7 +1390,8 @@ pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
-    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, ca, cb);
+    else PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
     return post_launch(c, "relax_from_w");
 }
 
@@ -1077,12 +1433,9 @@ pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad)
     PDG_CUDA_TRY(cudaMemsetAsync(c->counter, 0, sizeof(unsigned long long), c->stream));
     const int grid = grid_for(c->g.nnodes, 256);
     const int check_rho = (c->prob.flux != PDG_FLUX_LINEAR_ADVECTION && !sharded(c)) ? 1 : 0;
-    if (c->g.dim == 2)
-        pdg::check_state_kernel<2><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, check_rho,
-                                                                c->counter);
-    else
-        pdg::check_state_kernel<3><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, check_rho,
-                                                                c->counter);
+    const int nrho = c->g.lattice ? c->g.nv : 2 * c->g.dim;  // velocities whose sum is rho
+    pdg::check_state_kernel<<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, nrho, check_rho,
+                                                         c->counter);
     pdg_status s = post_launch(c, "check_state");
     if (s != PDG_OK) return s;
     unsigned long long h = 0;

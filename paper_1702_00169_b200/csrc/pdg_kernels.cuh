@@ -688,9 +688,8 @@ __global__ void __launch_bounds__(256) inflow_equilibrium_kernel(double *__restr
 }
 
 // Count nodes with rho <= 0 (component-0 block sum) or a non-finite local f.
-template <int DIM>
 __global__ void __launch_bounds__(256) check_state_kernel(const double *__restrict__ f, int64_t nnodes, int v0,
-                                                          int nvl, int check_rho, unsigned long long *count)
+                                                          int nvl, int nrho, int check_rho, unsigned long long *count)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long bad = 0;
@@ -700,7 +699,7 @@ __global__ void __launch_bounds__(256) check_state_kernel(const double *__restri
         for (int j = 0; j < nvl; ++j) {
             const double v = f[(int64_t)j * nnodes + x];
             ok = ok && isfinite(v);
-            if (v0 + j < 2 * DIM) rho += v;
+            if (v0 + j < nrho) rho += v;
         }
         if (check_rho && !(rho > 0.0)) ok = false;
         bad += ok ? 0 : 1;

@@ -1,0 +1,570 @@
+// sm_100a kernels for lattice velocity sets: D2Q9 (the paper's
+// Euler-with-gravity model) and the D3Q15/19/27 sets of its scaling tests
+// (P:856-858).  Velocities have components in {0, +-lambda}; a velocity with
+// d >= 2 non-zero components couples the d active axes of a cell through a dense
+// n^d x n^d local block (pdg_tables.hpp lattice_block) and its dependency graph has
+// genuinely diagonal wavefronts (Fig. dependency_graph).
+//
+//  lattice_sweep_kernel<D, N, ACT>: T2(dt') (solved downwind P:622-637) for the
+//  velocities whose active-axis mask is ACT (binary x=1, y=2, z=4; d >= 2).
+//   * "unit" = the active-axis nodes of one cell (inactive axes decouple: each inactive
+//     node index is an independent problem).  One lane owns one unit per row.
+//   * lanes run along x: 32 consecutive x-cells (x active) or x-nodes (x inactive), so
+//     every load/store of a warp is a contiguous run (coalesced).
+//   * the CHAIN axis (z if active, else y) is walked serially; the chain in-trace stays in
+//     registers (the lane owns the same x position in every row).
+//   * the x dependency inside a row is an affine recurrence of n^{d-1}-vectors
+//     s_out = a + Bx s_in (Bx uniform): a 5-step warp-shuffle Kogge-Stone scan with the
+//     precomputed powers Bx^(2^j); warps along x and along the PIPE axis (y, when y and z
+//     are both active) are skewed by one row per warp inside the CTA and hand traces over
+//     through shared memory (one __syncthreads per row).
+//   * across CTAs the same hand-over goes through global memory with per-task row
+//     progress counters (release/acquire); tasks are claimed in dependency order with an
+//     atomic ticket, so every wait targets a task already owned by a running CTA.
+//   * dense block constants live in the kernel parameter space (constant bank): every
+//     DFMA of the n^d x n^d mat-vec takes its coefficient as a c[0x0][...] operand.
+//
+//  relax_lbm_kernel<D, NV>: collision fused with the moments w = (rho, rho u) = P f,
+//  P = [1; v^T], f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2))
+//  (P:1138-1145), f <- ca f + cb f^eq (eq collision_cn).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pdg {
+
+constexpr int kLatMaxVel = 12;   // velocities of one active-axis class (D3Q27: 12 face diagonals)
+constexpr int kLbmMaxVel = 27;
+
+__host__ __device__ constexpr int ipow(int b, int e)
+{
+    int r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+template <int D, int ACT>
+struct LatShape {
+    static constexpr int XA = ACT & 1;
+    static constexpr int YA = (ACT >> 1) & 1;
+    static constexpr int ZA = (D == 3) ? ((ACT >> 2) & 1) : 0;
+    static constexpr int DA = XA + YA + ZA;                 // active axes
+    static constexpr int CA = ZA ? 2 : 1;                   // chain axis (walked serially)
+    static constexpr int PIPE = (D == 3 && ZA && YA) ? 1 : 0;  // y handed over warp to warp
+    static constexpr int BA = (D == 3 && !ZA) ? 2 : ((D == 3 && !YA) ? 1 : -1);  // batch axis (inactive)
+    // index t of each physical axis among the active ones (-1: inactive)
+    static constexpr int T0 = XA ? 0 : -1;
+    static constexpr int T1 = YA ? XA : -1;
+    static constexpr int T2 = ZA ? XA + YA : -1;
+    __host__ __device__ static constexpr int t_of(int k) { return k == 0 ? T0 : (k == 1 ? T1 : T2); }
+    static constexpr int TC = (CA == 2) ? T2 : T1;
+};
+
+template <int N, int DA>
+struct LatTab {
+    static constexpr int NB = ipow(N, DA);
+    static constexpr int MF = NB / N;
+    double KG[DA][N * N];   // kappa_t G (flow order)
+    double cin[DA];         // kappa_t / omega_0
+    double Ainv[NB * NB];
+    double Qx[NB * MF];
+    double Bp[5][MF * MF];  // Bx^(2^j)
+};
+
+struct LatVel {
+    int64_t f_off;   // element offset of the velocity's node grid in f
+    int64_t fb_off;  // element offset of its D inflow planes in fb
+    int32_t sign[3]; // flow direction per axis (+1 / -1; inactive axes +1)
+    int32_t pad;
+};
+
+struct LatGeom {
+    int64_t L[3];        // nodes per axis
+    int64_t stride[3];   // element stride per axis
+    int64_t plane_stride;
+    int32_t ncell[3];
+    int32_t Wx, Wy;      // warps per CTA along x / along the pipe (or batch) dimension
+    int32_t ngx, ngy;    // CTA groups along x / pipe-or-batch
+    int32_t nlane;       // x cells (x active) or x nodes
+    int32_t nw;          // pipe cells, batch nodes or 1
+    int32_t nc;          // chain cells
+    int32_t ntasks;
+    int32_t nvel;
+    int32_t pad;
+};
+
+template <int D, int N, int ACT>
+struct LatParams {
+    using S = LatShape<D, ACT>;
+    double *f;
+    const double *fb;
+    int *ticket;     // [0]; progress counters follow: progress[task] = rows published
+    int *progress;
+    double *xbuf;    // [task][row][Wy][MF]       x out-traces at CTA boundaries
+    double *ybuf;    // [task][row][Wx][32][MF]   y out-traces at CTA boundaries
+    LatGeom g;
+    LatVel v[kLatMaxVel];
+    LatTab<N, S::DA> tab;
+};
+
+__device__ __forceinline__ int ld_acquire(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_progress(const int *p, int need)
+{
+    if (ld_acquire(p) >= need) return;
+    while (ld_acquire(p) < need) __nanosleep(64);
+}
+
+// Index of a node (given by its flow coordinates u[] on every axis) in the inflow plane of
+// axis k: the node grid with axis k removed, same order (include/pdg.h).
+template <int D>
+__device__ __forceinline__ int64_t plane_index(const LatGeom &g, int k, const int64_t (&ph)[3])
+{
+    if (D == 2) return k == 0 ? ph[1] : ph[0];
+    if (k == 0) return ph[2] * g.L[1] + ph[1];
+    if (k == 1) return ph[2] * g.L[0] + ph[0];
+    return ph[1] * g.L[0] + ph[0];
+}
+
+// 2 f^b at the in-face nodes (face axis k, active index t) of the unit with cell/coord ucell[].
+template <int D, int N, int ACT, int K>
+__device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const LatVel &V, const int (&ucell)[3],
+                                           double (&s)[LatTab<N, LatShape<D, ACT>::DA>::MF])
+{
+    using S = LatShape<D, ACT>;
+    constexpr int MF = LatTab<N, S::DA>::MF;
+    constexpr int T = S::t_of(K);
+    const double *pl = P.fb + V.fb_off + (int64_t)K * P.g.plane_stride;
+#pragma unroll
+    for (int j = 0; j < MF; ++j) {
+        const int r = (j % ipow(N, T)) + (j / ipow(N, T)) * ipow(N, T + 1);  // digit T = 0
+        int64_t ph[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            if (a == K) continue;
+            const int ta = S::t_of(a);
+            int64_t u = (ta >= 0) ? (int64_t)ucell[a] * N + (r / ipow(N, ta)) % N : (int64_t)ucell[a];
+            if (ta >= 0 && V.sign[a] < 0) u = P.g.L[a] - 1 - u;
+            ph[a] = u;
+        }
+        s[j] = 2.0 * pl[plane_index<D>(P.g, K, ph)];
+    }
+}
+
+template <int D, int N, int ACT>
+__global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
+{
+    using S = LatShape<D, ACT>;
+    using TB = LatTab<N, S::DA>;
+    constexpr int DA = S::DA, NB = TB::NB, MF = TB::MF;
+    constexpr int XA = S::XA, PIPE = S::PIPE, CA = S::CA, TC = S::TC;
+    constexpr int TY = S::T1;
+    const unsigned FULL = 0xffffffffu;
+
+    __shared__ double xs[2][8][XA ? MF : 1];
+    __shared__ double ys[2][8][PIPE ? 32 : 1][PIPE ? MF : 1];
+    __shared__ int s_task;
+
+    const LatGeom &g = P.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qx = warp % g.Wx, wy = warp / g.Wx;
+    const int skew = (XA ? qx : 0) + (PIPE ? wy : 0);
+    const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? g.Wy - 1 : 0);
+
+    for (;;) {
+        if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
+        __syncthreads();
+        const int task = s_task;
+        __syncthreads();
+        if (task >= g.ntasks) return;
+        const int per_v = g.ngx * g.ngy;
+        const int vi = task / per_v, rem = task - vi * per_v;
+        const int gy = rem / g.ngx, gx = rem - gy * g.ngx;
+        const LatVel &V = P.v[vi];
+        const int ux = (gx * g.Wx + qx) * 32 + lane;  // x cell (XA) or x node
+        const int uw = gy * g.Wy + wy;                // pipe cell, batch node or 0
+        const bool wvalid = uw < g.nw && (gx * g.Wx + qx) * 32 < g.nlane;  // warp has work
+        const bool valid = wvalid && ux < g.nlane;
+
+        // unit coordinates: flow cell index on active axes, node index on inactive ones
+        int ucell[3] = {0, 0, 0};
+        ucell[0] = ux;
+        if (PIPE) ucell[1] = uw;
+        if (S::BA >= 0) ucell[S::BA] = uw;
+        // address: base of the unit's first node + sum_t digit_t * dstep_t
+        int64_t dstep[3] = {0, 0, 0};
+        int64_t ibase = V.f_off;  // contribution of the non-chain coordinates
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int ta = S::t_of(a);
+            if (ta >= 0) {
+                dstep[ta] = (int64_t)V.sign[a] * g.stride[a];
+                if (a != CA) {
+                    const int64_t u0 = (int64_t)ucell[a] * N;
+                    ibase += ((V.sign[a] > 0) ? u0 : g.L[a] - 1 - u0) * g.stride[a];
+                }
+            } else {
+                ibase += (int64_t)ucell[a] * g.stride[a];
+            }
+        }
+        const int64_t cstep = (int64_t)V.sign[CA] * g.stride[CA] * N;                        // one chain cell
+        const int64_t cbase = (V.sign[CA] > 0) ? 0 : (g.L[CA] - 1) * g.stride[CA];          // chain cell 0
+
+        double sc[MF];
+#pragma unroll
+        for (int j = 0; j < MF; ++j) sc[j] = 0.0;
+        if (valid) ghost_face<D, N, ACT, CA>(P, V, ucell, sc);
+
+        for (int t = 0; t < g.nc + maxskew; ++t) {
+            const int r = t - skew;
+            if (r >= 0 && r < g.nc && wvalid) {
+                ucell[CA] = r;
+                const int64_t ub = ibase + cbase + (int64_t)r * cstep;
+                double fo[NB];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    int64_t off = 0;
+#pragma unroll
+                    for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
+                    fo[q] = valid ? __ldcs(P.f + ub + off) : 0.0;
+                }
+                // pipe (y) in-trace
+                double sy[PIPE ? MF : 1];
+                if constexpr (PIPE) {
+                    if (wy > 0) {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) sy[j] = ys[(t - 1) & 1][warp - g.Wx][lane][j];
+                    } else if (gy > 0) {
+                        wait_progress(P.progress + task - g.ngx, r + 1);
+                        const double *src = P.ybuf + ((((int64_t)(task - g.ngx) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) sy[j] = __ldcg(src + j);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) sy[j] = 0.0;
+                        if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
+                    }
+                }
+                // rhs = (I + sum_t kappa_t G^(t)) f_old + inflows of the chain and pipe axes
+                double rhs[NB];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    double acc = fo[q];
+#pragma unroll
+                    for (int tt = 0; tt < DA; ++tt) {
+                        const int a = (q / ipow(N, tt)) % N;
+#pragma unroll
+                        for (int b = 0; b < N; ++b) acc = fma(P.tab.KG[tt][a * N + b], fo[q + (b - a) * ipow(N, tt)], acc);
+                    }
+                    rhs[q] = acc;
+                }
+#pragma unroll
+                for (int j = 0; j < MF; ++j) {
+                    const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1);
+                    rhs[q] = fma(P.tab.cin[TC], sc[j], rhs[q]);
+                }
+                if constexpr (PIPE) {
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) {
+                        const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1);
+                        rhs[q] = fma(P.tab.cin[TY], sy[j], rhs[q]);
+                    }
+                }
+                double fn[NB];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int c = 0; c < NB; ++c) acc = fma(P.tab.Ainv[q * NB + c], rhs[c], acc);
+                    fn[q] = acc;
+                }
+                if constexpr (XA) {
+                    // x in-trace of the warp (lane 0's cell)
+                    double s0[MF];
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) s0[j] = 0.0;
+                    if (qx > 0) {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) s0[j] = xs[(t - 1) & 1][warp - 1][j];
+                    } else if (gx > 0) {
+                        wait_progress(P.progress + task - 1, r + 1);
+                        const double *src = P.xbuf + (((int64_t)(task - 1) * g.nc + r) * g.Wy + wy) * MF;
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) s0[j] = __ldcg(src + j);
+                    } else if (lane == 0 && valid) {
+                        ghost_face<D, N, ACT, 0>(P, V, ucell, s0);
+                    }
+                    // zero-inflow x out-trace of every cell; lane 0 adds Bx s0
+                    double a[MF];
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) a[j] = valid ? fo[j * N + N - 1] + fn[j * N + N - 1] : 0.0;
+                    if (lane == 0) {
+#pragma unroll
+                        for (int i = 0; i < MF; ++i) {
+                            double acc = a[i];
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) acc = fma(P.tab.Bp[0][i * MF + j], s0[j], acc);
+                            a[i] = acc;
+                        }
+                    }
+                    // inclusive scan y_l = a_l + Bx y_{l-1}
+#pragma unroll
+                    for (int sidx = 0; sidx < 5; ++sidx) {
+                        const int o = 1 << sidx;
+                        double pv[MF];
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) pv[j] = __shfl_up_sync(FULL, a[j], o);
+                        if (lane >= o) {
+#pragma unroll
+                            for (int i = 0; i < MF; ++i) {
+                                double acc = a[i];
+#pragma unroll
+                                for (int j = 0; j < MF; ++j) acc = fma(P.tab.Bp[sidx][i * MF + j], pv[j], acc);
+                                a[i] = acc;
+                            }
+                        }
+                    }
+                    double sin_[MF];
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) {
+                        const double up = __shfl_up_sync(FULL, a[j], 1);
+                        sin_[j] = (lane == 0) ? s0[j] : up;
+                    }
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) {
+                        double acc = fn[q];
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) acc = fma(P.tab.Qx[q * MF + j], sin_[j], acc);
+                        fn[q] = acc;
+                    }
+                    // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
+                    if (lane == 31) {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) xs[t & 1][warp][j] = a[j];
+                        if (qx == g.Wx - 1 && gx < g.ngx - 1) {
+                            double *dst = P.xbuf + (((int64_t)task * g.nc + r) * g.Wy + wy) * MF;
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
+                            __threadfence();
+                        }
+                    }
+                }
+                if (valid) {
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) {
+                        int64_t off = 0;
+#pragma unroll
+                        for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
+                        __stcs(P.f + ub + off, fn[q]);
+                    }
+                }
+                // chain out-trace -> next row (registers)
+#pragma unroll
+                for (int j = 0; j < MF; ++j) {
+                    const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1) + (N - 1) * ipow(N, TC);
+                    sc[j] = fo[q] + fn[q];
+                }
+                if constexpr (PIPE) {
+                    double ty[MF];
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) {
+                        const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1) + (N - 1) * ipow(N, TY);
+                        ty[j] = fo[q] + fn[q];
+                    }
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) ys[t & 1][warp][lane][j] = ty[j];
+                    if (wy == g.Wy - 1 && gy < g.ngy - 1) {
+                        double *dst = P.ybuf + ((((int64_t)task * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
+                        __threadfence();
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LBM collision fused with the moments (nranks == 1).
+// ---------------------------------------------------------------------------
+struct LbmParams {
+    double v[kLbmMaxVel][3];
+    double wgt[kLbmMaxVel];
+    double inv_c2, inv_2c4, inv_2c2;
+};
+
+template <int D, int NV>
+__device__ __forceinline__ void lbm_feq(const double (&w)[D + 1], const LbmParams &L, double (&feq)[NV])
+{
+    const double rho = w[0];
+    const double inv = 1.0 / rho;
+    double u[D];
+    double uu = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        u[d] = w[1 + d] * inv;
+        uu = fma(u[d], u[d], uu);
+    }
+    const double base = 1.0 - uu * L.inv_2c2;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double uv = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) uv = fma(u[d], L.v[i][d], uv);
+        const double poly = fma(uv, fma(uv, L.inv_2c4, L.inv_c2), base);
+        feq[i] = L.wgt[i] * rho * poly;
+    }
+}
+
+template <int D, int NV>
+__device__ __forceinline__ void lbm_moments(const double (&fv)[NV], const LbmParams &L, double (&w)[D + 1])
+{
+#pragma unroll
+    for (int c = 0; c <= D; ++c) w[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        w[0] += fv[i];
+#pragma unroll
+        for (int d = 0; d < D; ++d) w[1 + d] = fma(fv[i], L.v[i][d], w[1 + d]);
+    }
+}
+
+template <int D, int NV>
+__global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
+                                                        const __grid_constant__ LbmParams L, double ca, double cb)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
+        double w[D + 1];
+        lbm_moments<D, NV>(fv, L, w);
+        double feq[NV];
+        lbm_feq<D, NV>(w, L, feq);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fma(cb, feq[i], ca * fv[i]));
+    }
+}
+
+// Partial moments of the local velocities [v0, v0 + nvl) (sharded path, pdg_moments).
+template <int D, int NV>
+__global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *__restrict__ f, double *__restrict__ w,
+                                                                  int64_t nnodes, int v0, int nvl,
+                                                                  const __grid_constant__ LbmParams L)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
+        double wl[D + 1];
+        lbm_moments<D, NV>(fv, L, wl);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) __stcs(w + (int64_t)c * nnodes + x, wl[c]);
+    }
+}
+
+// Collision of the local velocities from reduced moments w (sharded path).
+template <int D, int NV>
+__global__ void __launch_bounds__(256) relax_from_w_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
+                                                               int64_t nnodes, int v0, int nvl,
+                                                               const __grid_constant__ LbmParams L, double ca,
+                                                               double cb)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double wl[D + 1];
+#pragma unroll
+        for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
+        double feq[NV];
+        lbm_feq<D, NV>(wl, L, feq);
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (i >= v0 && i < v0 + nvl) {
+                double *p = f + (int64_t)(i - v0) * nnodes + x;
+                *p = fma(cb, feq[i], ca * __ldcs(p));
+            }
+    }
+}
+
+// f_i = f^eq_i(w) for the local velocities.
+template <int D, int NV>
+__global__ void __launch_bounds__(256) equilibrium_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
+                                                              int64_t nnodes, int v0, int nvl,
+                                                              const __grid_constant__ LbmParams L)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+        double wl[D + 1];
+#pragma unroll
+        for (int c = 0; c <= D; ++c) wl[c] = w[(int64_t)c * nnodes + x];
+        double feq[NV];
+        lbm_feq<D, NV>(wl, L, feq);
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+            if (i >= v0 && i < v0 + nvl) __stcs(f + (int64_t)(i - v0) * nnodes + x, feq[i]);
+    }
+}
+
+// Inflow planes of the local velocities: plane k of velocity i (v_i^k != 0) holds f^eq_i(wb)
+// at the nodes of its inflow face (lo face for v^k > 0, hi face for v^k < 0).
+struct LatInflowParams {
+    double *fb;
+    const double *wb;
+    int64_t nnodes, plane_stride;
+    int64_t L[3], stride[3];
+    int32_t v0, nvl, dim;
+    LbmParams lbm;
+};
+
+template <int D, int NV>
+__global__ void __launch_bounds__(256) lattice_inflow_kernel(const __grid_constant__ LatInflowParams P)
+{
+    const int j = blockIdx.y;         // local velocity
+    const int k = blockIdx.z;         // plane axis
+    const int i = P.v0 + j;
+    const double vk = P.lbm.v[i][k];
+    if (vk == 0.0) return;
+    const int64_t np = P.nnodes / P.L[k];
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= np) return;
+    // plane index -> node coordinates (axis k removed, remaining axes in x, y, z order)
+    int64_t c[3] = {0, 0, 0};
+    int64_t rest = idx;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if (a == k) continue;
+        c[a] = rest % P.L[a];
+        rest /= P.L[a];
+    }
+    c[k] = (vk > 0.0) ? 0 : P.L[k] - 1;
+    int64_t node = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) node += c[a] * P.stride[a];
+    double wl[D + 1];
+#pragma unroll
+    for (int cc = 0; cc <= D; ++cc) wl[cc] = P.wb[(int64_t)cc * P.nnodes + node];
+    double feq[NV];
+    lbm_feq<D, NV>(wl, P.lbm, feq);
+    double val = 0.0;
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+        if (q == i) val = feq[q];
+    P.fb[(int64_t)j * D * P.plane_stride + (int64_t)k * P.plane_stride + idx] = val;
+}
+
+}  // namespace pdg

@@ -19,6 +19,8 @@
 #pragma once
 #include <cmath>
 #include <cstring>
+#include <utility>
+#include <vector>
 
 namespace pdg {
 
@@ -126,6 +128,120 @@ inline bool cell_block(int p, long double kappa, CellBlock *out)
         out->g[i] = (double)(Ai[i * n + 0] * kappa / w[0]);
     }
     out->beta = out->g[n - 1];
+    return true;
+}
+
+
+// ---------------------------------------------------------------------------
+// Dense local block of a lattice velocity (NEXT-2: non-axis-aligned sets such as
+// D2Q9, D3Q15/19/27).  For v with components in {0, +-lambda}
+// on an axis-aligned Cartesian cell the DG_reduit block is the Kronecker
+// SUM over the active axes t (v_t != 0) of kappa_t G (nodes in flow order along every
+// active axis; inactive axes decouple: I on their nodes), with kappa_t = |v_t| dt'/h_t:
+//
+//   A = I - sum_t kappa_t G^(t),   rhs = (I + sum_t kappa_t G^(t)) f_old + sum_t (kappa_t/omega_0) E_in^(t) s_t
+//   f_new = A^{-1} rhs,            s_t^out = f_old[out face t] + f_new[out face t]
+//
+// A^{-1} is dense (n^d x n^d, d = number of active axes): the "pre-inverted local block"
+// of the north star.  Reduced node r = sum_t a_t n^t (t = 0 the lowest active axis).
+// For the x-scan (axis t = 0 active): Qx = A^{-1} E_in^(0) kappa_0/omega_0 (n^d x n^{d-1}),
+// Bx = rows of Qx on the x-out face (n^{d-1} square) and its powers Bx^(2^j).
+// ---------------------------------------------------------------------------
+struct LatticeBlockLD {
+    int n = 0, d = 0, nb = 0, mf = 0;
+    long double G[kMaxN * kMaxN];            // 1-D G in flow order (positive velocity)
+    long double kappa[3];                    // per active axis
+    long double w0;                          // omega_0
+    std::vector<long double> Ainv;           // nb x nb
+    std::vector<long double> Qx;             // nb x mf
+    std::vector<long double> Bpow;           // 5 x mf x mf
+};
+
+inline bool invert_dense(int n, std::vector<long double> A, std::vector<long double> &Ainv)
+{
+    Ainv.assign((size_t)n * n, 0.0L);
+    for (int i = 0; i < n; ++i) Ainv[(size_t)i * n + i] = 1.0L;
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r)
+            if (fabsl(A[(size_t)r * n + c]) > fabsl(A[(size_t)piv * n + c])) piv = r;
+        if (A[(size_t)piv * n + c] == 0.0L) return false;
+        if (piv != c)
+            for (int j = 0; j < n; ++j) {
+                std::swap(A[(size_t)c * n + j], A[(size_t)piv * n + j]);
+                std::swap(Ainv[(size_t)c * n + j], Ainv[(size_t)piv * n + j]);
+            }
+        const long double dd = A[(size_t)c * n + c];
+        for (int j = 0; j < n; ++j) {
+            A[(size_t)c * n + j] /= dd;
+            Ainv[(size_t)c * n + j] /= dd;
+        }
+        for (int r = 0; r < n; ++r) {
+            if (r == c || A[(size_t)r * n + c] == 0.0L) continue;
+            const long double fac = A[(size_t)r * n + c];
+            for (int j = 0; j < n; ++j) {
+                A[(size_t)r * n + j] -= fac * A[(size_t)c * n + j];
+                Ainv[(size_t)r * n + j] -= fac * Ainv[(size_t)c * n + j];
+            }
+        }
+    }
+    return true;
+}
+
+// d active axes with CN parameters kappa[0..d-1] (lowest axis first).
+inline bool lattice_block(int p, int d, const long double *kappa, LatticeBlockLD *out)
+{
+    long double x[kMaxN], w[kMaxN], D[kMaxN * kMaxN];
+    if (!gl_nodes(p, x, w) || d < 1 || d > 3) return false;
+    const int n = p + 1;
+    lagrange_derivative(n, x, D);
+    LatticeBlockLD &B = *out;
+    B.n = n;
+    B.d = d;
+    B.nb = 1;
+    for (int t = 0; t < d; ++t) B.nb *= n;
+    B.mf = B.nb / n;
+    B.w0 = w[0];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            long double v = D[j * n + i] * w[j];
+            if (i == n - 1 && j == n - 1) v -= 1.0L;
+            B.G[i * n + j] = v / w[i];
+        }
+    for (int t = 0; t < 3; ++t) B.kappa[t] = (t < d) ? kappa[t] : 0.0L;
+    const int nb = B.nb;
+    std::vector<long double> A((size_t)nb * nb, 0.0L);
+    int pw[4] = {1, n, n * n, n * n * n};
+    for (int r = 0; r < nb; ++r) {
+        A[(size_t)r * nb + r] += 1.0L;
+        for (int t = 0; t < d; ++t) {
+            const int at = (r / pw[t]) % n;
+            for (int b = 0; b < n; ++b) {
+                const int c = r + (b - at) * pw[t];
+                A[(size_t)r * nb + c] -= B.kappa[t] * B.G[at * n + b];
+            }
+        }
+    }
+    if (!invert_dense(nb, A, B.Ainv)) return false;
+    const int mf = B.mf;
+    B.Qx.assign((size_t)nb * mf, 0.0L);
+    // x-in face node j (digits of the other active axes) = reduced node j * n (a_0 = 0)
+    for (int r = 0; r < nb; ++r)
+        for (int j = 0; j < mf; ++j) B.Qx[(size_t)r * mf + j] = B.Ainv[(size_t)r * nb + j * n] * B.kappa[0] / B.w0;
+    std::vector<long double> Bx((size_t)mf * mf), T((size_t)mf * mf);
+    for (int i = 0; i < mf; ++i)
+        for (int j = 0; j < mf; ++j) Bx[(size_t)i * mf + j] = B.Qx[(size_t)(i * n + n - 1) * mf + j];
+    B.Bpow.assign((size_t)5 * mf * mf, 0.0L);
+    for (int s = 0; s < 5; ++s) {
+        for (size_t q = 0; q < Bx.size(); ++q) B.Bpow[(size_t)s * mf * mf + q] = Bx[q];
+        for (int i = 0; i < mf; ++i)
+            for (int j = 0; j < mf; ++j) {
+                long double acc = 0.0L;
+                for (int k = 0; k < mf; ++k) acc += Bx[(size_t)i * mf + k] * Bx[(size_t)k * mf + j];
+                T[(size_t)i * mf + j] = acc;
+            }
+        Bx = T;
+    }
     return true;
 }
 

@@ -30,6 +30,7 @@ PDG_E_UNSUPPORTED = 11
 PDG_FLUX_LINEAR_ADVECTION = 0
 PDG_FLUX_EULER = 1
 PDG_FLUX_ISOTHERMAL = 2
+PDG_FLUX_LBM = 3
 PDG_SCHEME_M2 = 0
 PDG_SCHEME_M2KIN = 1
 PDG_SCHEME_M4 = 2
@@ -38,7 +39,7 @@ PDG_SYNC_ERRORS = 0x2
 PDG_NO_FUSION = 0x4
 PDG_PROFILE = 0x8
 KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other",
-                "relax_xsweep", "zslab"]
+                "relax_xsweep", "zslab", "lattice"]
 PDG_DECOMP_VELOCITY = 0
 PDG_DECOMP_ZSLAB = 1
 
@@ -307,7 +308,7 @@ def problem_from_config(cfg, tau=0.0, scheme=PDG_SCHEME_M2, rank=0, nranks=1, nc
                         decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1):
     """pdg_problem for a pdg_inputs.Config (the seeded workload descriptions)."""
     vel, comp = cfg.velocities()
-    return make_problem(cfg.dim, cfg.N, cfg.p, cfg.m, vel, comp, cfg.lam, cfg.flux, list(cfg.fparams), cfg.dt,
+    return make_problem(cfg.dim, cfg.N, cfg.p, cfg.m, vel, comp, cfg.lam, cfg.flux, list(cfg.flux_params()), cfg.dt,
                         tau=tau, scheme=scheme, rank=rank, nranks=nranks, nccl_id=nccl_id, flags=flags,
                         stream=stream, lo=cfg.lo, hi=cfg.hi, decomposition=decomposition,
                         slabs_per_rank=slabs_per_rank)

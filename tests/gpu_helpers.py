@@ -75,3 +75,23 @@ def to_np(t: torch.Tensor, shape) -> np.ndarray:
 
 def oracle_problem(cfg, tau=0.0):
     return O.Problem.from_config(cfg, tau=tau)
+
+
+def lattice_planes(cfg, full: np.ndarray, plane_stride: int, v_begin: int = 0) -> np.ndarray:
+    """Lattice sets (PDG_FLUX_LBM): [nvl, grid...] -> [nvl, dim, plane_stride]; plane k of velocity i
+    is the face slice of its inflow face across axis k (include/pdg.h), unused when v_i^k = 0."""
+    vel, _ = cfg.velocities()
+    dim, shape = cfg.dim, cfg.grid_shape
+    nvl = full.shape[0]
+    out = np.zeros((nvl, dim, plane_stride))
+    for j in range(nvl):
+        for k in range(dim):
+            vk = vel[v_begin + j][k]
+            if vk == 0:
+                continue
+            ax = dim - 1 - k
+            idx = [slice(None)] * dim
+            idx[ax] = 0 if vk > 0 else shape[ax] - 1
+            pl = full[j][tuple(idx)].reshape(-1)
+            out[j, k, :pl.size] = pl
+    return out
