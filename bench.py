@@ -129,7 +129,7 @@ def oracle_prepare(cfg, N_sub):
     import numpy as np
     from oracle import oracle as O
     from pdg_inputs import w0_grid, wb_grid
-    sub = oracle_sample_cfg(cfg, N_sub)
+    sub = oracle_sample_cfg(cfg, min(N_sub, cfg.N))
     pb = O.Problem.from_config(sub)
     w0 = w0_grid(sub)
     f0, fb = O.initial_data(pb, w0.numpy(), wb_grid(sub, w0).numpy())
@@ -154,6 +154,7 @@ def omp_threads():
 
 def cpu_baseline(cfg, N_sub=64):
     sub, pb, fc, fbc, _ = oracle_prepare(cfg, N_sub)
+    N_sub = sub.N
     t0 = time.perf_counter()
     oracle_step(pb, fc, fbc)
     dt = time.perf_counter() - t0
@@ -347,11 +348,18 @@ def main():
     ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
                     help="multi-GPU decomposition (default: zslab when launched on several ranks)")
     ap.add_argument("--slabs-per-rank", type=int, default=1)
+    ap.add_argument("--lattice", default=None, choices=["D2Q9", "D3Q15", "D3Q19", "D3Q27"],
+                    help="NEXT-2 workload: isothermal LBM on this lattice (replaces --config)")
+    ap.add_argument("--cells", type=int, default=128, help="cells per axis of the --lattice workload")
+    ap.add_argument("--degree", type=int, default=2, help="degree p of the --lattice workload")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "product":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    from pdg_inputs import CONFIGS
-    cfg = CONFIGS[args.config]
+    from pdg_inputs import CONFIGS, lbm_config
+    cfg = lbm_config(args.lattice, args.cells, p=args.degree, nu=2.0) if args.lattice else CONFIGS[args.config]
+    if args.lattice:
+        args.cpu_cells = min(args.cpu_cells, 24 if cfg.dim == 3 else 256)
+        args.ref_cells = min(args.ref_cells, 16 if cfg.dim == 3 else 128)
     if args.decomp is None:
         args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "velocity"
     if args.impl == "reference":

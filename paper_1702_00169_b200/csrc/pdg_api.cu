@@ -91,8 +91,16 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     P.nlane = (int)(XA ? g.ncell[0] : g.L[0]);
     P.nw = (int)(PIPE ? g.ncell[1] : (BA >= 0 ? g.L[BA] : 1));
     P.nc = (int)g.ncell[CA];
-    P.Wx = std::min(8, (P.nlane + 31) / 32);
-    P.Wy = std::max(1, std::min(8 / P.Wx, P.nw));
+    if (XA) {
+        // x carries a dependency: the CTA's x-warps are skewed, keep them few enough that the
+        // grid still has tasks for every SM (2-D grids: one warp per CTA along x)
+        P.Wx = std::min(8, (P.nlane + 31) / 32);
+        P.Wy = std::max(1, std::min(8 / P.Wx, P.nw));
+    } else {
+        // lanes over independent x nodes: spend the warps on the pipe axis (y hand-over in smem)
+        P.Wy = std::max(1, std::min(8, P.nw));
+        P.Wx = std::max(1, std::min(8 / P.Wy, (P.nlane + 31) / 32));
+    }
     // test knob: force small CTAs so that the cross-CTA hand-over paths run on small grids
     if (const char *e = std::getenv("PDG_LATTICE_WARPS")) {
         int wx = 0, wy = 0;
@@ -540,12 +548,19 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     for (int s = 0; s < 5; ++s)
         for (int i = 0; i < TB::MF * TB::MF; ++i) P.tab.Bp[s][i] = (double)B.Bpow[(size_t)s * TB::MF * TB::MF + i];
     const int threads = 32 * pl.Wx * pl.Wy;
+    const size_t smem = sizeof(double) * (size_t)(threads / 32) * 2 * TB::NB * 32;  // cp.async row buffers
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024);
+        attr_set = true;
+    }
     static std::map<int, int> occ_cache;
     int occ = 0;
     auto oc = occ_cache.find(threads);
     if (oc != occ_cache.end()) occ = oc->second;
     else {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT>, threads, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT>, threads, smem) !=
             cudaSuccess)
             occ = 1;
         occ = std::max(1, occ);
@@ -553,7 +568,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     }
     const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
     PDG_CUDA_TRY(cudaMemsetAsync(c->lat_ints, 0, sizeof(int) * ((size_t)pl.ntasks + 1), c->stream));
-    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, 0, c->stream>>>(P);
+    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, smem, c->stream>>>(P);
     return PDG_OK;
 }
 
@@ -733,10 +748,13 @@ void launch_equilibrium_t(pdg_ctx *c, const double *w, const double *wb)
     } while (0)
 
 // ---- LBM model kernels (lattice sets, NEXT-2) ------------------------------------------
+// one node per thread for the LBM kernels (pdg_lattice.cuh)
+unsigned grid_all(int64_t work, int threads) { return (unsigned)std::max<int64_t>(1, (work + threads - 1) / threads); }
+
 template <int D, int NV>
 void launch_relax_lbm_t(pdg_ctx *c, double ca, double cb)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
     pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, ca, cb);
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
@@ -745,7 +763,7 @@ void launch_relax_lbm_t(pdg_ctx *c, double ca, double cb)
 template <int D, int NV>
 void launch_partial_lbm_t(pdg_ctx *c)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
     pdg::partial_moments_lbm_kernel<D, NV>
         <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm);
@@ -755,7 +773,7 @@ void launch_partial_lbm_t(pdg_ctx *c)
 template <int D, int NV>
 void launch_relax_from_w_lbm_t(pdg_ctx *c, double ca, double cb)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
     pdg::relax_from_w_lbm_kernel<D, NV>
         <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm, ca, cb);
@@ -766,7 +784,7 @@ void launch_relax_from_w_lbm_t(pdg_ctx *c, double ca, double cb)
 template <int D, int NV>
 void launch_equilibrium_lbm_t(pdg_ctx *c, const double *w, const double *wb, bool f_only)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const unsigned grid = grid_all(c->g.nnodes, 256);
     if (w) pdg::equilibrium_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm);
     if (f_only) return;
     pdg::LatInflowParams P;

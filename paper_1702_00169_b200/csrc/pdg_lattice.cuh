@@ -119,6 +119,15 @@ __device__ __forceinline__ void st_release(int *p, int v)
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
 __device__ __forceinline__ void wait_progress(const int *p, int need)
 {
     if (ld_acquire(p) >= need) return;
@@ -174,6 +183,9 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
     __shared__ double xs[2][8][XA ? MF : 1];
     __shared__ double ys[2][8][PIPE ? 32 : 1][PIPE ? MF : 1];
     __shared__ int s_task;
+    // per-warp double buffer of the unit values of the current and the next row (cp.async
+    // prefetch: the loads of row r+1 do not depend on the carries and overlap row r's math)
+    extern __shared__ double sfo[];  // [warp][2][NB][32]
 
     const LatGeom &g = P.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -187,9 +199,11 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
         const int task = s_task;
         __syncthreads();
         if (task >= g.ntasks) return;
-        const int per_v = g.ngx * g.ngy;
-        const int vi = task / per_v, rem = task - vi * per_v;
-        const int gy = rem / g.ngx, gx = rem - gy * g.ngx;
+        // ticket order (gy, velocity, gx): every velocity's pipeline advances together, and the
+        // tasks a task waits on (gx - 1: ticket - 1; gy - 1: ticket - nvel ngx) come earlier
+        const int per_gy = g.nvel * g.ngx;
+        const int gy = task / per_gy, rem = task - gy * per_gy;
+        const int vi = rem / g.ngx, gx = rem - vi * g.ngx;
         const LatVel &V = P.v[vi];
         const int ux = (gx * g.Wx + qx) * 32 + lane;  // x cell (XA) or x node
         const int uw = gy * g.Wy + wy;                // pipe cell, batch node or 0
@@ -225,19 +239,35 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
         for (int j = 0; j < MF; ++j) sc[j] = 0.0;
         if (valid) ghost_face<D, N, ACT, CA>(P, V, ucell, sc);
 
-        for (int t = 0; t < g.nc + maxskew; ++t) {
-            const int r = t - skew;
-            if (r >= 0 && r < g.nc && wvalid) {
-                ucell[CA] = r;
-                const int64_t ub = ibase + cbase + (int64_t)r * cstep;
-                double fo[NB];
+        double *wbuf = sfo + (size_t)warp * 2 * NB * 32;
+        // issue the copies of row rr into buffer rr & 1 (one commit group per row)
+        auto prefetch = [&](int rr) {
+            if (valid && rr < g.nc) {
+                const int64_t ubr = ibase + cbase + (int64_t)rr * cstep;
+                double *dst = wbuf + (rr & 1) * NB * 32 + lane;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) {
                     int64_t off = 0;
 #pragma unroll
                     for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
-                    fo[q] = valid ? __ldcs(P.f + ub + off) : 0.0;
+                    cp_async8(dst + q * 32, P.f + ubr + off);
                 }
+            }
+            cp_async_commit();
+        };
+
+        for (int t = 0; t < g.nc + maxskew; ++t) {
+            const int r = t - skew;
+            if (r >= 0 && r < g.nc && wvalid) {
+                ucell[CA] = r;
+                const int64_t ub = ibase + cbase + (int64_t)r * cstep;
+                if (r == 0) prefetch(0);
+                prefetch(r + 1);
+                cp_async_wait<1>();  // row r has landed (row r+1 may still be in flight)
+                double fo[NB];
+                const double *src = wbuf + (r & 1) * NB * 32 + lane;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) fo[q] = valid ? src[q * 32] : 0.0;
                 // pipe (y) in-trace
                 double sy[PIPE ? MF : 1];
                 if constexpr (PIPE) {
@@ -245,8 +275,8 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
 #pragma unroll
                         for (int j = 0; j < MF; ++j) sy[j] = ys[(t - 1) & 1][warp - g.Wx][lane][j];
                     } else if (gy > 0) {
-                        wait_progress(P.progress + task - g.ngx, r + 1);
-                        const double *src = P.ybuf + ((((int64_t)(task - g.ngx) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
+                        wait_progress(P.progress + task - per_gy, r + 1);
+                        const double *src = P.ybuf + ((((int64_t)(task - per_gy) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
 #pragma unroll
                         for (int j = 0; j < MF; ++j) sy[j] = __ldcg(src + j);
                     } else {
@@ -256,18 +286,19 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                     }
                 }
                 // rhs = (I + sum_t kappa_t G^(t)) f_old + inflows of the chain and pipe axes
+                // (loops ordered so that the NB accumulators are independent chains: ILP for the DFMA pipe)
                 double rhs[NB];
 #pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    double acc = fo[q];
+                for (int q = 0; q < NB; ++q) rhs[q] = fo[q];
 #pragma unroll
-                    for (int tt = 0; tt < DA; ++tt) {
-                        const int a = (q / ipow(N, tt)) % N;
+                for (int tt = 0; tt < DA; ++tt)
 #pragma unroll
-                        for (int b = 0; b < N; ++b) acc = fma(P.tab.KG[tt][a * N + b], fo[q + (b - a) * ipow(N, tt)], acc);
-                    }
-                    rhs[q] = acc;
-                }
+                    for (int b = 0; b < N; ++b)
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) {
+                            const int a = (q / ipow(N, tt)) % N;
+                            rhs[q] = fma(P.tab.KG[tt][a * N + b], fo[q + (b - a) * ipow(N, tt)], rhs[q]);
+                        }
 #pragma unroll
                 for (int j = 0; j < MF; ++j) {
                     const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1);
@@ -282,12 +313,11 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                 }
                 double fn[NB];
 #pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    double acc = 0.0;
+                for (int q = 0; q < NB; ++q) fn[q] = P.tab.Ainv[q * NB] * rhs[0];
 #pragma unroll
-                    for (int c = 0; c < NB; ++c) acc = fma(P.tab.Ainv[q * NB + c], rhs[c], acc);
-                    fn[q] = acc;
-                }
+                for (int c = 1; c < NB; ++c)
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Ainv[q * NB + c], rhs[c], fn[q]);
                 if constexpr (XA) {
                     // x in-trace of the warp (lane 0's cell)
                     double s0[MF];
@@ -326,12 +356,9 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                         for (int j = 0; j < MF; ++j) pv[j] = __shfl_up_sync(FULL, a[j], o);
                         if (lane >= o) {
 #pragma unroll
-                            for (int i = 0; i < MF; ++i) {
-                                double acc = a[i];
+                            for (int j = 0; j < MF; ++j)
 #pragma unroll
-                                for (int j = 0; j < MF; ++j) acc = fma(P.tab.Bp[sidx][i * MF + j], pv[j], acc);
-                                a[i] = acc;
-                            }
+                                for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[sidx][i * MF + j], pv[j], a[i]);
                         }
                     }
                     double sin_[MF];
@@ -341,12 +368,9 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                         sin_[j] = (lane == 0) ? s0[j] : up;
                     }
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) {
-                        double acc = fn[q];
+                    for (int j = 0; j < MF; ++j)
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) acc = fma(P.tab.Qx[q * MF + j], sin_[j], acc);
-                        fn[q] = acc;
-                    }
+                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Qx[q * MF + j], sin_[j], fn[q]);
                     // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
                     if (lane == 31) {
 #pragma unroll
@@ -394,6 +418,7 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
             __syncthreads();
             if (threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
         }
+        cp_async_wait<0>();
     }
 }
 
@@ -406,27 +431,38 @@ struct LbmParams {
     double inv_c2, inv_2c4, inv_2c2;
 };
 
-template <int D, int NV>
-__device__ __forceinline__ void lbm_feq(const double (&w)[D + 1], const LbmParams &L, double (&feq)[NV])
-{
-    const double rho = w[0];
-    const double inv = 1.0 / rho;
-    double u[D];
-    double uu = 0.0;
+// Macroscopic state at a node, prepared once; feq(i) evaluates the equilibrium of velocity i.
+template <int D>
+struct LbmNode {
+    double rho, u[D], base;
+    __device__ __forceinline__ LbmNode(const double (&w)[D + 1], const LbmParams &L)
+    {
+        rho = w[0];
+        const double inv = 1.0 / rho;
+        double uu = 0.0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-        u[d] = w[1 + d] * inv;
-        uu = fma(u[d], u[d], uu);
+        for (int d = 0; d < D; ++d) {
+            u[d] = w[1 + d] * inv;
+            uu = fma(u[d], u[d], uu);
+        }
+        base = 1.0 - uu * L.inv_2c2;
     }
-    const double base = 1.0 - uu * L.inv_2c2;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
+    __device__ __forceinline__ double feq(int i, const LbmParams &L) const
+    {
         double uv = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) uv = fma(u[d], L.v[i][d], uv);
         const double poly = fma(uv, fma(uv, L.inv_2c4, L.inv_c2), base);
-        feq[i] = L.wgt[i] * rho * poly;
+        return L.wgt[i] * rho * poly;
     }
+};
+
+template <int D, int NV>
+__device__ __forceinline__ void lbm_feq(const double (&w)[D + 1], const LbmParams &L, double (&feq)[NV])
+{
+    const LbmNode<D> nd(w, L);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) feq[i] = nd.feq(i, L);
 }
 
 template <int D, int NV>
@@ -446,17 +482,19 @@ template <int D, int NV>
 __global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
                                                         const __grid_constant__ LbmParams L, double ca, double cb)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
+    // instead of being hoisted into registers)
+    {
+        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (x >= nnodes) return;
         double fv[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
         double w[D + 1];
         lbm_moments<D, NV>(fv, L, w);
-        double feq[NV];
-        lbm_feq<D, NV>(w, L, feq);
+        const LbmNode<D> nd(w, L);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fma(cb, feq[i], ca * fv[i]));
+        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fma(cb, nd.feq(i, L), ca * fv[i]));
     }
 }
 
@@ -466,8 +504,11 @@ __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *
                                                                   int64_t nnodes, int v0, int nvl,
                                                                   const __grid_constant__ LbmParams L)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
+    // instead of being hoisted into registers)
+    {
+        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (x >= nnodes) return;
         double fv[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) fv[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
@@ -485,8 +526,11 @@ __global__ void __launch_bounds__(256) relax_from_w_lbm_kernel(double *__restric
                                                                const __grid_constant__ LbmParams L, double ca,
                                                                double cb)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
+    // instead of being hoisted into registers)
+    {
+        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (x >= nnodes) return;
         double wl[D + 1];
 #pragma unroll
         for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
@@ -507,8 +551,11 @@ __global__ void __launch_bounds__(256) equilibrium_lbm_kernel(double *__restrict
                                                               int64_t nnodes, int v0, int nvl,
                                                               const __grid_constant__ LbmParams L)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
+    // instead of being hoisted into registers)
+    {
+        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (x >= nnodes) return;
         double wl[D + 1];
 #pragma unroll
         for (int c = 0; c <= D; ++c) wl[c] = w[(int64_t)c * nnodes + x];
