@@ -94,10 +94,21 @@ typedef enum {
 typedef enum {
     PDG_SCHEME_M2 = 0,    /* T2(dt/2) C2(dt) T2(dt/2), the hot path */
     PDG_SCHEME_M2KIN = 1, /* T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) */
-    PDG_SCHEME_M4 = 2     /* M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1:
+    PDG_SCHEME_M4 = 2,    /* M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1:
                              palindromic composition raising the order to 4; needs
                              2 tau + g2 dt/2 > 0 when tau > 0 */
+    PDG_SCHEME_M2S = 3    /* T2(dt/2) S2(dt/2) C2(dt) S2(dt/2) T2(dt/2): the Strang scheme with the source
+                             step (NEXT-3); needs a source (pdg_problem.source) */
 } pdg_scheme;
+
+typedef enum {
+    PDG_SOURCE_NONE = 0,
+    PDG_SOURCE_GRAVITY = 1  /* Euler with gravity, PDG_FLUX_LBM only: macroscopic source
+                               s(w) = (0, rho G), source_params = G[dim] (e.g. (0, -g) in 2-D), lifted to
+                               g_i = w_i v_i.(rho G)/c^2 (reading C24: P g = s); S2(h) = (I + h/2 G_h)
+                               (I - h/2 G_h)^{-1} is exact in closed form, f <- f + h g(f) (one Picard
+                               iteration) */
+} pdg_source_kind;
 
 typedef enum {
     PDG_DECOMP_VELOCITY = 0, /* rank r owns velocities [r nv/G, (r+1) nv/G) on the whole grid; one NCCL
@@ -161,6 +172,9 @@ typedef struct {
     int32_t decomposition;       /* pdg_decomposition: how nranks > 1 split the work */
     int32_t slabs_per_rank;      /* PDG_DECOMP_ZSLAB: sub-slabs per rank (>= 1; > 1 emulates more ranks
                                     on one GPU with the same arithmetic) */
+    int32_t source;              /* pdg_source_kind (PDG_SOURCE_NONE: no source) */
+    const double *source_params; /* host, n_source_params values (see pdg_source_kind); copied */
+    int32_t n_source_params;
 } pdg_problem;
 
 typedef struct {
@@ -217,6 +231,11 @@ pdg_status pdg_transport(pdg_ctx *c, double dtp);
  * f <- ((2 tau - dt) f + 2 dt f^eq)/(2 tau + dt)   (= 2 f^eq - f at tau = 0).
  * With nranks > 1: partial moments, NCCL sum, then relaxation of local velocities. */
 pdg_status pdg_collide(pdg_ctx *c, double dt);
+
+/* One source operator S2(h) on every node (NEXT-3): f <- f + h g(f) for the gravity
+ * source (exact CN solution, see PDG_SOURCE_GRAVITY).  PDG_E_INVALID_ARGUMENT without a source.
+ * With nranks > 1 the density comes from the reduced moments (partial moments, NCCL sum). */
+pdg_status pdg_source(pdg_ctx *c, double h);
 
 /* The two halves of the sharded collision (row a4), exposed for testing:
  * pdg_partial_moments writes w_dev = sum over LOCAL velocities of each component

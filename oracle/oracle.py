@@ -69,6 +69,7 @@ def lib():
             "or_collide": [ctypes.c_int, ctypes.c_int, pd, pi32, ctypes.c_int, d, ctypes.c_int, pd, d, d, i64, pd],
             "or_equilibrium_field": [ctypes.c_int, ctypes.c_int, pd, pi32, ctypes.c_int, d, ctypes.c_int, pd,
                                      i64, pd, pd],
+            "or_source": [ctypes.c_int, ctypes.c_int, pd, pd, pd, d, i64, pd],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -104,7 +105,7 @@ def _check(rc: int, what: str):
 class Problem:
     """Everything the paper's problem statement fixes."""
 
-    def __init__(self, dim, N, p, vel, comp, m, lam, flux, fparams, dt, tau=0.0, lo=None, hi=None):
+    def __init__(self, dim, N, p, vel, comp, m, lam, flux, fparams, dt, tau=0.0, lo=None, hi=None, gravity=None):
         self.dim, self.p, self.m = int(dim), int(p), int(m)
         self.N = [int(N)] * dim if np.isscalar(N) else [int(x) for x in N]
         self.vel = np.ascontiguousarray(np.asarray(vel, dtype=np.float64).reshape(-1, 3))
@@ -119,6 +120,9 @@ class Problem:
         self.hi = list(hi) if hi is not None else [1.0] * 3
         self.n = self.p + 1
         self.Nd = self.n ** self.dim
+        # gravity vector G of the Euler-with-gravity source, or None
+        self.gravity = None if gravity is None else np.ascontiguousarray(
+            (list(gravity) + [0.0, 0.0, 0.0])[:3], dtype=np.float64)
         self.ncell = int(np.prod(self.N))
         self.nnodes = self.ncell * self.Nd
 
@@ -126,7 +130,7 @@ class Problem:
     def from_config(cls, cfg, tau=0.0):
         vel, comp = cfg.velocities()
         return cls(cfg.dim, cfg.N, cfg.p, vel, comp, cfg.m, cfg.lam, cfg.flux, cfg.flux_params(), cfg.dt, tau,
-                   lo=cfg.lo, hi=cfg.hi)
+                   lo=cfg.lo, hi=cfg.hi, gravity=cfg.gravity or None)
 
     def mesh(self) -> Mesh:
         m = Mesh()
@@ -312,6 +316,17 @@ def collide(pb: Problem, f_nodes: np.ndarray, dt: float, tau: float | None = Non
                             _pd(pb.fparams), tau, dt, nn, _pd(f_nodes)), "collide")
 
 
+def source(pb: Problem, f_nodes: np.ndarray, h: float) -> int:
+    """S2(h) in place on f [nv, nodes...] (gravity source of P:1101-1160, reading C24).
+    Returns the number of Picard iterations the worst node needed."""
+    assert f_nodes.flags["C_CONTIGUOUS"] and pb.flux == FLUX_LBM and pb.gravity is not None
+    nn = f_nodes[0].size
+    it = lib().or_source(pb.dim, pb.nv, _pd(pb.vel), _pd(pb.fparams), _pd(pb.gravity), h, nn, _pd(f_nodes))
+    if it < 1:
+        raise RuntimeError("oracle source failed")
+    return it
+
+
 # ----------------------------------------------------------------------------
 # Palindromic step M2 (P:486-492) on the whole mesh
 # ----------------------------------------------------------------------------
@@ -340,9 +355,10 @@ def m2kin_substep(pb: Problem, fc, fbc, h: float):
 
 
 def scheme_run(pb: Problem, f_grid: np.ndarray, fb_grid: np.ndarray, nsteps: int, scheme: str) -> np.ndarray:
-    """nsteps of 'm2', 'm2kin' or 'm4': the symmetric triple-jump
+    """nsteps of 'm2', 'm2kin', 'm4': the symmetric triple-jump
     composition M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1
-    (palindromic composition to higher even order)."""
+    (palindromic composition to higher even order), or 'm2s': the Strang scheme
+    with source M2s(dt) = T2(dt/2) S2(dt/2) C2(dt) S2(dt/2) T2(dt/2)."""
     fc = pb.grid_to_cells(np.asarray(f_grid, dtype=np.float64))
     fbc = pb.grid_to_cells(np.asarray(fb_grid, dtype=np.float64))
     g1 = 1.0 / (2.0 - 2.0 ** (1.0 / 3.0))
@@ -354,6 +370,12 @@ def scheme_run(pb: Problem, f_grid: np.ndarray, fb_grid: np.ndarray, nsteps: int
             t2_all(pb, 0.5 * pb.dt, fc, fbc)
         elif scheme == "m2kin":
             m2kin_substep(pb, fc, fbc, pb.dt)
+        elif scheme == "m2s":
+            t2_all(pb, 0.5 * pb.dt, fc, fbc)
+            source(pb, fc, 0.5 * pb.dt)
+            collide(pb, fc, pb.dt)
+            source(pb, fc, 0.5 * pb.dt)
+            t2_all(pb, 0.5 * pb.dt, fc, fbc)
         elif scheme == "m4":
             m2kin_substep(pb, fc, fbc, g1 * pb.dt)
             m2kin_substep(pb, fc, fbc, g2 * pb.dt)

@@ -709,3 +709,65 @@ int or_equilibrium_field(int dim, int nv, const double *vel, const int32_t *comp
     }
     return rc;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Source step S2 (NEXT-3): the Euler-with-gravity case of P:1101-1194.       */
+/* ------------------------------------------------------------------------- */
+/*
+ * Kinetic source g(f) for the LBM model: the macroscopic source of eq
+ * macro_limit_system is s(w) = (0, rho G) with G the gravity vector (P:1104-1108:
+ * d_t(rho u) + div Pi = rho g, g = -g e_y), lifted to the kinetic level "on the
+ * equilibrium part" by the standard moment-exact forcing
+ *   g_i = w_i (s_rho + v_i . s_m / c^2)          (reading C24)
+ * so that P g = s (sum w_i = 1, sum w_i v_i = 0, sum w_i v_i v_i^T = c^2 I).
+ * fp = {c, w_0 .. w_{nv-1}} as for the LBM model, G[dim] the gravity vector.
+ */
+static void lbm_source(int dim, int nv, const double *vel, const double *fp, const double *G, const double *fnode,
+                       double *g)
+{
+    const double c = fp[0], c2 = c * c;
+    double w[4];
+    lbm_moments(dim, nv, vel, fnode, w);
+    double sm[3] = { 0, 0, 0 };
+    for (int d = 0; d < dim; d++) sm[d] = w[0] * G[d];   /* s = (0, rho G) */
+    for (int i = 0; i < nv; i++) {
+        double vs = 0.0;
+        for (int d = 0; d < dim; d++) vs += vel[3 * i + d] * sm[d];
+        g[i] = fp[1 + i] * (0.0 + vs / c2);
+    }
+}
+
+/*
+ * S2(h) = (I + h/2 G_h)(I - h/2 G_h)^{-1} at every node: the
+ * theta = 1/2 implicit local equation f* = f + h/2 (g(f) + g(f*)) solved by Picard
+ * iteration from f* = f ("converges in one Picard iteration" for the
+ * gravity source).  Iterates until the update is below 1e-15 relative, at most 16.
+ * f : [nv][nnodes] in/out.  Returns the largest number of Picard iterations used.
+ */
+int or_source(int dim, int nv, const double *vel, const double *fp, const double *G, double h, int64_t nnodes,
+              double *f)
+{
+    int itmax = 0;
+#pragma omp parallel for schedule(static) reduction(max : itmax)
+    for (int64_t x = 0; x < nnodes; x++) {
+        double f0[64], fs[64], g0[64], gs[64], fn[64];
+        for (int i = 0; i < nv; i++) f0[i] = f[(int64_t)i * nnodes + x];
+        lbm_source(dim, nv, vel, fp, G, f0, g0);
+        for (int i = 0; i < nv; i++) fs[i] = f0[i];
+        int it = 0;
+        for (it = 1; it <= 16; it++) {
+            lbm_source(dim, nv, vel, fp, G, fs, gs);
+            double diff = 0.0, scale = 0.0;
+            for (int i = 0; i < nv; i++) {
+                fn[i] = f0[i] + 0.5 * h * (g0[i] + gs[i]);
+                diff = fmax(diff, fabs(fn[i] - fs[i]));
+                scale = fmax(scale, fabs(fn[i]));
+            }
+            for (int i = 0; i < nv; i++) fs[i] = fn[i];
+            if (diff <= 1e-15 * scale) break;
+        }
+        if (it > itmax) itmax = it;
+        for (int i = 0; i < nv; i++) f[(int64_t)i * nnodes + x] = fs[i];
+    }
+    return itmax;
+}

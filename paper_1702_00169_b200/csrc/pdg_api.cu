@@ -156,8 +156,19 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     if (!(p->lambda > 0.0) || !std::isfinite(p->lambda)) return fail(PDG_E_INVALID_ARGUMENT, "lambda must be > 0");
     if (!(p->dt != 0.0) || !std::isfinite(p->dt)) return fail(PDG_E_INVALID_ARGUMENT, "dt must be finite and != 0");
     if (!(p->tau >= 0.0) || !std::isfinite(p->tau)) return fail(PDG_E_INVALID_ARGUMENT, "tau must be >= 0");
-    if (p->scheme != PDG_SCHEME_M2 && p->scheme != PDG_SCHEME_M2KIN && p->scheme != PDG_SCHEME_M4)
+    if (p->scheme != PDG_SCHEME_M2 && p->scheme != PDG_SCHEME_M2KIN && p->scheme != PDG_SCHEME_M4 &&
+        p->scheme != PDG_SCHEME_M2S)
         return fail(PDG_E_INVALID_ARGUMENT, "unknown scheme");
+    if (p->source != PDG_SOURCE_NONE) {
+        if (p->source != PDG_SOURCE_GRAVITY) return fail(PDG_E_INVALID_ARGUMENT, "unknown source kind");
+        if (p->flux != PDG_FLUX_LBM) return fail(PDG_E_UNSUPPORTED, "the gravity source is implemented for PDG_FLUX_LBM");
+        if (!p->source_params || p->n_source_params < p->dim)
+            return fail(PDG_E_INVALID_ARGUMENT, "gravity needs source_params = G[dim]");
+        for (int d = 0; d < p->dim; ++d)
+            if (!std::isfinite(p->source_params[d])) return fail(PDG_E_INVALID_ARGUMENT, "G must be finite");
+    }
+    if (p->scheme == PDG_SCHEME_M2S && p->source == PDG_SOURCE_NONE)
+        return fail(PDG_E_INVALID_ARGUMENT, "PDG_SCHEME_M2S needs a source");
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
     g->dim = p->dim;
     g->p = p->degree;
@@ -752,11 +763,11 @@ void launch_equilibrium_t(pdg_ctx *c, const double *w, const double *wb)
 unsigned grid_all(int64_t work, int threads) { return (unsigned)std::max<int64_t>(1, (work + threads - 1) / threads); }
 
 template <int D, int NV>
-void launch_relax_lbm_t(pdg_ctx *c, double ca, double cb)
+void launch_relax_lbm_t(pdg_ctx *c, pdg::LocalOps op)
 {
     const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
-    pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, ca, cb);
+    pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
 }
 
@@ -771,12 +782,12 @@ void launch_partial_lbm_t(pdg_ctx *c)
 }
 
 template <int D, int NV>
-void launch_relax_from_w_lbm_t(pdg_ctx *c, double ca, double cb)
+void launch_relax_from_w_lbm_t(pdg_ctx *c, pdg::LocalOps op)
 {
     const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
     pdg::relax_from_w_lbm_kernel<D, NV>
-        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm, ca, cb);
+        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm, op);
     prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)c->g.nnodes);
 }
 
@@ -850,19 +861,37 @@ pdg_status partial_and_reduce(pdg_ctx *c)
     return PDG_OK;
 }
 
-pdg_status collide(pdg_ctx *c, double dt)
+// One pass of the local operators of a lattice set: S2(hs1), C2(dt) (if with_c), S2(hs2).
+pdg_status local_pass_lbm(pdg_ctx *c, double hs1, bool with_c, double dt, double hs2)
 {
-    double ca, cb;
-    collision_coeffs(c, dt, &ca, &cb);
+    pdg::LocalOps op;
+    op.hs1 = hs1;
+    op.hs2 = hs2;
+    op.ca = 1.0;
+    op.cb = 0.0;
+    if (with_c) collision_coeffs(c, dt, &op.ca, &op.cb);
     if (!sharded(c)) {
-        if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_lbm_t, c, ca, cb);
-        else PDG_DISPATCH(launch_relax_t, c, ca, cb);
+        PDG_LBM_DISPATCH(launch_relax_lbm_t, c, op);
         return post_launch(c, "relax");
     }
     pdg_status s = partial_and_reduce(c);
     if (s != PDG_OK) return s;
-    if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, ca, cb);
-    else PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, op);
+    return post_launch(c, "relax_from_w");
+}
+
+pdg_status collide(pdg_ctx *c, double dt)
+{
+    if (c->g.lattice) return local_pass_lbm(c, 0.0, true, dt, 0.0);
+    double ca, cb;
+    collision_coeffs(c, dt, &ca, &cb);
+    if (!sharded(c)) {
+        PDG_DISPATCH(launch_relax_t, c, ca, cb);
+        return post_launch(c, "relax");
+    }
+    pdg_status s = partial_and_reduce(c);
+    if (s != PDG_OK) return s;
+    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
     return post_launch(c, "relax_from_w");
 }
 
@@ -903,7 +932,7 @@ bool use_relax_x(const pdg_ctx *c)
 // operator: two consecutive T(h) with the same h into one pass over f (two sweeps), and a
 // C followed by T's into the collision + x-sweep kernel plus one y/z sweep pass.
 struct Op {
-    int kind;  // 0: T, 1: C
+    int kind;  // 0: T, 1: C, 2: S (source)
     double h;
 };
 
@@ -926,6 +955,13 @@ void append_scheme(std::vector<Op> &ops, int scheme, double dt)
         ops.push_back({0, 0.5 * dt});
     } else if (scheme == PDG_SCHEME_M2KIN) {
         append_m2kin(ops, dt);
+    } else if (scheme == PDG_SCHEME_M2S) {
+        // M2s(dt) = T2(dt/2) S2(dt/2) C2(dt) S2(dt/2) T2(dt/2)
+        ops.push_back({0, 0.5 * dt});
+        ops.push_back({2, 0.5 * dt});
+        ops.push_back({1, dt});
+        ops.push_back({2, 0.5 * dt});
+        ops.push_back({0, 0.5 * dt});
     } else {
         // M4 = M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt): symmetric triple jump, a palindromic
         // composition of M2kin raising the order to 4; g1 = 1/(2 - 2^{1/3}).
@@ -946,6 +982,23 @@ pdg_status execute_ops(pdg_ctx *c, const std::vector<Op> &ops)
     size_t i = 0;
     pdg_status s = PDG_OK;
     while (i < n && s == PDG_OK) {
+        if (c->g.lattice && ops[i].kind != 0) {
+            // a run of local operators: [S] [C] [S] fused in one pass over f
+            double hs1 = 0.0, hs2 = 0.0, hc = 0.0;
+            bool with_c = false;
+            if (ops[i].kind == 2) hs1 = ops[i++].h;
+            if (i < n && ops[i].kind == 1) {
+                with_c = true;
+                hc = ops[i++].h;
+                if (i < n && ops[i].kind == 2) hs2 = ops[i++].h;
+            }
+            s = local_pass_lbm(c, hs1, with_c, hc, hs2);
+            continue;
+        }
+        if (ops[i].kind == 2) {
+            s = fail(PDG_E_UNSUPPORTED, "source step without a lattice model");
+            break;
+        }
         if (ops[i].kind == 1) {
             int np = 0;
             if (i + 1 < n && ops[i + 1].kind == 0) {
@@ -1228,6 +1281,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     c->prob.comp = c->comp.data();
     c->prob.flux_params = c->fparams;
     c->prob.nccl_id = nullptr;
+    c->prob.source_params = nullptr;  // copied into c->lbm.G
     c->f = f_dev;
     c->fb = fb_dev;
     c->w = w_dev;
@@ -1251,6 +1305,8 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         c->lbm.inv_c2 = 1.0 / (cc * cc);
         c->lbm.inv_2c4 = 1.0 / (2.0 * cc * cc * cc * cc);
         c->lbm.inv_2c2 = 1.0 / (2.0 * cc * cc);
+        if (p->source == PDG_SOURCE_GRAVITY)
+            for (int d = 0; d < p->dim; ++d) c->lbm.G[d] = p->source_params[d];
         char *base = static_cast<char *>(work_dev) + 256;
         c->lat_ints = reinterpret_cast<int *>(base);
         c->lat_xbuf = reinterpret_cast<double *>(base + lat_ints_bytes(c->g));
@@ -1395,6 +1451,15 @@ pdg_status pdg_collide(pdg_ctx *c, double dt)
     return collide(c, dt);
 }
 
+pdg_status pdg_source(pdg_ctx *c, double h)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
+    if (c->prob.source == PDG_SOURCE_NONE) return fail(PDG_E_INVALID_ARGUMENT, "the problem has no source");
+    if (!std::isfinite(h)) return fail(PDG_E_INVALID_ARGUMENT, "h must be finite");
+    return local_pass_lbm(c, h, false, 0.0, 0.0);
+}
+
 pdg_status pdg_partial_moments(pdg_ctx *c)
 {
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
@@ -1408,8 +1473,12 @@ pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
-    if (c->g.lattice) PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, ca, cb);
-    else PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    if (c->g.lattice) {
+        pdg::LocalOps op{0.0, ca, cb, 0.0};
+        PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, op);
+    } else {
+        PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+    }
     return post_launch(c, "relax_from_w");
 }
 

@@ -429,6 +429,16 @@ struct LbmParams {
     double v[kLbmMaxVel][3];
     double wgt[kLbmMaxVel];
     double inv_c2, inv_2c4, inv_2c2;
+    double G[3];      // gravity vector of the source step (NEXT-3; zeros without a source)
+};
+
+// The local operators of one fused pass: S2(hs1), then C2 (f <- ca f + cb f^eq), then S2(hs2).
+// S2(h) for the gravity source g_i = w_i v_i.(rho G)/c^2 (reading C24) is exact in closed form:
+// g depends on f only through rho, which the source does not change (P g = (0, rho G)), so the
+// CN equation f* = f + h/2 (g(f) + g(f*)) has the solution f* = f + h g(f) (one Picard
+// iteration); it adds h rho G to the momentum.
+struct LocalOps {
+    double hs1, ca, cb, hs2;
 };
 
 // Macroscopic state at a node, prepared once; feq(i) evaluates the equilibrium of velocity i.
@@ -478,9 +488,46 @@ __device__ __forceinline__ void lbm_moments(const double (&fv)[NV], const LbmPar
     }
 }
 
+// S2(hs1) C2 S2(hs2) at one node from its (full) moments w; fv in/out (local velocities only
+// matter: entries outside [v0, v0 + nvl) are left as they are).
+template <int D, int NV>
+__device__ __forceinline__ void lbm_local_ops(double (&fv)[NV], double (&w)[D + 1], const LbmParams &L,
+                                              const LocalOps &op)
+{
+    // source on the equilibrium part: g_i = w_i v_i.(rho G)/c^2, S2(h): f += h g, rho u += h rho G
+    double gs[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) gs[d] = w[0] * L.G[d] * L.inv_c2;
+    if (op.hs1 != 0.0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double vg = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+            fv[i] = fma(op.hs1 * L.wgt[i], vg, fv[i]);
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
+    }
+    if (op.cb != 0.0 || op.ca != 1.0) {
+        const LbmNode<D> nd(w, L);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = fma(op.cb, nd.feq(i, L), op.ca * fv[i]);
+    }
+    if (op.hs2 != 0.0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double vg = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+            fv[i] = fma(op.hs2 * L.wgt[i], vg, fv[i]);
+        }
+    }
+}
+
 template <int D, int NV>
 __global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
-                                                        const __grid_constant__ LbmParams L, double ca, double cb)
+                                                        const __grid_constant__ LbmParams L, const LocalOps op)
 {
     // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
     // instead of being hoisted into registers)
@@ -492,9 +539,9 @@ __global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, 
         for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
         double w[D + 1];
         lbm_moments<D, NV>(fv, L, w);
-        const LbmNode<D> nd(w, L);
+        lbm_local_ops<D, NV>(fv, w, L, op);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fma(cb, nd.feq(i, L), ca * fv[i]));
+        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fv[i]);
     }
 }
 
@@ -523,8 +570,7 @@ __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *
 template <int D, int NV>
 __global__ void __launch_bounds__(256) relax_from_w_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
                                                                int64_t nnodes, int v0, int nvl,
-                                                               const __grid_constant__ LbmParams L, double ca,
-                                                               double cb)
+                                                               const __grid_constant__ LbmParams L, const LocalOps op)
 {
     // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
     // instead of being hoisted into registers)
@@ -534,14 +580,13 @@ __global__ void __launch_bounds__(256) relax_from_w_lbm_kernel(double *__restric
         double wl[D + 1];
 #pragma unroll
         for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
-        double feq[NV];
-        lbm_feq<D, NV>(wl, L, feq);
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
+        lbm_local_ops<D, NV>(fv, wl, L, op);
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-            if (i >= v0 && i < v0 + nvl) {
-                double *p = f + (int64_t)(i - v0) * nnodes + x;
-                *p = fma(cb, feq[i], ca * __ldcs(p));
-            }
+            if (i >= v0 && i < v0 + nvl) __stcs(f + (int64_t)(i - v0) * nnodes + x, fv[i]);
     }
 }
 

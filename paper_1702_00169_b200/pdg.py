@@ -34,6 +34,9 @@ PDG_FLUX_LBM = 3
 PDG_SCHEME_M2 = 0
 PDG_SCHEME_M2KIN = 1
 PDG_SCHEME_M4 = 2
+PDG_SCHEME_M2S = 3
+PDG_SOURCE_NONE = 0
+PDG_SOURCE_GRAVITY = 1
 PDG_CHECK_STATE = 0x1
 PDG_SYNC_ERRORS = 0x2
 PDG_NO_FUSION = 0x4
@@ -45,7 +48,7 @@ PDG_DECOMP_ZSLAB = 1
 
 EXPORTED = [
     "pdg_query_sizes", "pdg_create", "pdg_set_state", "pdg_set_equilibrium", "pdg_get_state", "pdg_step",
-    "pdg_transport", "pdg_collide", "pdg_partial_moments", "pdg_relax_from_w", "pdg_moments",
+    "pdg_transport", "pdg_collide", "pdg_source", "pdg_partial_moments", "pdg_relax_from_w", "pdg_moments",
     "pdg_check_state", "pdg_cell_block", "pdg_synchronize", "pdg_destroy", "pdg_nccl_unique_id",
     "pdg_status_string", "pdg_last_error", "pdg_version", "pdg_profile_read",
 ]
@@ -61,6 +64,8 @@ class pdg_problem(ctypes.Structure):
         ("scheme", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_uint32),
         ("decomposition", ctypes.c_int32), ("slabs_per_rank", ctypes.c_int32),
+        ("source", ctypes.c_int32), ("source_params", ctypes.POINTER(ctypes.c_double)),
+        ("n_source_params", ctypes.c_int32),
     ]
 
 
@@ -101,6 +106,7 @@ def load() -> ctypes.CDLL:
         "pdg_step": ([ctx, i64], st),
         "pdg_transport": ([ctx, d], st),
         "pdg_collide": ([ctx, d], st),
+        "pdg_source": ([ctx, d], st),
         "pdg_partial_moments": ([ctx], st),
         "pdg_relax_from_w": ([ctx, d], st),
         "pdg_moments": ([ctx, vp, ctypes.c_int], st),
@@ -141,7 +147,7 @@ def version() -> str:
 
 def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, tau=0.0, scheme=PDG_SCHEME_M2,
                  rank=0, nranks=1, nccl_id=None, stream=None, flags=0, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
-                 decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1):
+                 decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1, gravity=None):
     """Build a pdg_problem; the returned object keeps its host arrays alive."""
     pb = pdg_problem()
     pb.dim = dim
@@ -170,6 +176,11 @@ def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, t
     pb.flags = flags
     pb.decomposition = decomposition
     pb.slabs_per_rank = slabs_per_rank
+    if gravity:
+        pb._src = (ctypes.c_double * len(gravity))(*gravity)
+        pb.source = PDG_SOURCE_GRAVITY
+        pb.source_params = ctypes.cast(pb._src, ctypes.POINTER(ctypes.c_double))
+        pb.n_source_params = len(gravity)
     return pb
 
 
@@ -255,6 +266,9 @@ class Solver:
     def collide(self, dt: float):
         _check(self.lib.pdg_collide(self.ctx, float(dt)), "pdg_collide")
 
+    def source(self, h: float):
+        _check(self.lib.pdg_source(self.ctx, float(h)), "pdg_source")
+
     def partial_moments(self):
         _check(self.lib.pdg_partial_moments(self.ctx), "pdg_partial_moments")
 
@@ -311,4 +325,4 @@ def problem_from_config(cfg, tau=0.0, scheme=PDG_SCHEME_M2, rank=0, nranks=1, nc
     return make_problem(cfg.dim, cfg.N, cfg.p, cfg.m, vel, comp, cfg.lam, cfg.flux, list(cfg.flux_params()), cfg.dt,
                         tau=tau, scheme=scheme, rank=rank, nranks=nranks, nccl_id=nccl_id, flags=flags,
                         stream=stream, lo=cfg.lo, hi=cfg.hi, decomposition=decomposition,
-                        slabs_per_rank=slabs_per_rank)
+                        slabs_per_rank=slabs_per_rank, gravity=getattr(cfg, "gravity", None) or None)

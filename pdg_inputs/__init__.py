@@ -117,6 +117,8 @@ class Config:
     lo: tuple = (0.0, 0.0, 0.0)
     hi: tuple = (1.0, 1.0, 1.0)
     lattice: str = ""       # LBM lattice name (flux == FLUX_LBM); fparams = (c,) then
+    gravity: tuple = ()     # gravity vector G of the Euler-with-gravity source, () if none
+    rho0_g: tuple = ()      # (rho0, g) of the hydrostatic initial state
 
     @property
     def n(self) -> int:
@@ -194,6 +196,16 @@ def lbm_config(lattice_name: str, N: int, p: int = 2, lam: float = 1.0, nu: floa
                   nu * h / lam, steps, seed, "lbm_pulse", lattice=lattice_name)
 
 
+def gravity_config(N: int, p: int = 2, lam: float = 2.0, g: float = 1.0, rho0: float = 1.0, dt: float = 0.024,
+                   t_max: float = 0.12, seed: int = 0x5EED000A) -> Config:
+    """The paper's Euler-with-gravity test: isothermal Euler in 2-D with the D2Q9
+    model (c = lambda/sqrt(3)), gravity G = -g e_y, starting from the fluid at rest
+    rho = rho0 exp(-g y / c^2), u = 0; steps = t_max / dt."""
+    steps = max(1, int(round(t_max / dt)))
+    return Config(f"gravity_D2Q9_N{N}", 2, N, p, 3, lam, FLUX_LBM, (lam / math.sqrt(3.0),), dt, steps, seed,
+                  "hydrostatic", lattice="D2Q9", gravity=(0.0, -g), rho0_g=(rho0, g))
+
+
 def node_axis(cfg: Config, axis: int, dtype=torch.float64, device="cpu") -> torch.Tensor:
     """1-D coordinates of the node grid along `axis`: X = c*n + a."""
     xh = torch.tensor(gl_sample_points(cfg.p), dtype=dtype)
@@ -241,6 +253,12 @@ def _fields(cfg: Config, X, Y, Z):
                 ud = ud + 0.02 * torch.sin(two_pi * (k + 1) * coords[(d + 1) % 3] + psi[k][d])
             vel.append(ud)
         return [rho, rho * vel[0], rho * vel[1], rho * vel[2]]
+    if cfg.recipe == "hydrostatic":
+        # fluid at rest in the gravity field: rho = rho0 exp(-g y / c^2), u = 0
+        rho0, g = cfg.rho0_g
+        c = cfg.fparams[0]
+        rho = rho0 * torch.exp(-g * Y / (c * c)) + 0.0 * X
+        return [rho, 0.0 * rho, 0.0 * rho]
     if cfg.recipe == "lbm_pulse":
         ph = phases(cfg.seed, 3)
         r2 = (X - 0.5) ** 2 + (Y - 0.5) ** 2 + ((Z - 0.5) ** 2 if cfg.dim == 3 else 0.0)
