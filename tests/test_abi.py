@@ -108,3 +108,50 @@ def test_query_sizes_zslab():
     with pytest.raises(pdg.PdgError):
         pdg.query_sizes(pdg.problem_from_config(CONFIGS[3].resized(4), decomposition=pdg.PDG_DECOMP_ZSLAB,
                                                 slabs_per_rank=8))
+
+
+# ---- lattice sets (NEXT-2) and the source step (NEXT-3): host-side validation ----------
+@pytest.mark.parametrize("lat", ["D2Q9", "D3Q15", "D3Q19", "D3Q27"])
+def test_query_sizes_lattice(lat):
+    from pdg_inputs import lbm_config
+    cfg = lbm_config(lat, 9)
+    s = pdg.query_sizes(pdg.problem_from_config(cfg))
+    assert s.f_elems == cfg.nv * cfg.nnodes and s.w_elems == cfg.m * cfg.nnodes
+    assert s.fb_elems == cfg.nv * cfg.dim * s.plane_stride  # one inflow plane per axis
+    for G in (3,) if cfg.nv % 3 == 0 else (1,):
+        for r in range(G):
+            t = pdg.query_sizes(pdg.problem_from_config(cfg, rank=r, nranks=G))
+            assert t.nv_local == cfg.nv // G and t.v_begin == r * (cfg.nv // G)
+
+
+def test_lattice_validation_errors():
+    from pdg_inputs import lbm_config
+    cfg = lbm_config("D2Q9", 4)
+    vel, comp = cfg.velocities()
+    base = dict(dim=2, ncell=4, degree=2, m=3, vel=vel, comp=comp, lam=cfg.lam, flux=pdg.PDG_FLUX_LBM,
+                flux_params=list(cfg.flux_params()), dt=cfg.dt)
+
+    def bad(**over):
+        kw = dict(base)
+        kw.update(over)
+        with pytest.raises(pdg.PdgError) as e:
+            pdg.query_sizes(pdg.make_problem(**kw))
+        return e.value.status
+
+    assert pdg.query_sizes(pdg.make_problem(**base)).f_elems == 9 * cfg.nnodes
+    v2 = [list(v) for v in vel]
+    v2[5][0] = 0.5 * cfg.lam  # component not in {0, +-lambda}
+    assert bad(vel=v2) == pdg.PDG_E_VELOCITY_SET
+    assert bad(flux_params=[cfg.flux_params()[0]]) == pdg.PDG_E_FLUX_MODEL  # weights missing
+    assert bad(m=4) == pdg.PDG_E_FLUX_MODEL
+    assert bad(vel=vel[:8], comp=comp[:8], flux_params=list(cfg.flux_params())[:9]) == pdg.PDG_E_UNSUPPORTED
+    assert bad(scheme=pdg.PDG_SCHEME_M2S) == pdg.PDG_E_INVALID_ARGUMENT  # M2s without a source
+    ok = pdg.make_problem(**base, scheme=pdg.PDG_SCHEME_M2S, gravity=(0.0, -1.0))
+    assert pdg.query_sizes(ok).nv_local == 9
+    assert bad(decomposition=pdg.PDG_DECOMP_ZSLAB, nranks=2) == pdg.PDG_E_UNSUPPORTED
+    c3 = CONFIGS[3]
+    v3, c3comp = c3.velocities()
+    with pytest.raises(pdg.PdgError) as e:  # gravity needs the LBM model
+        pdg.query_sizes(pdg.make_problem(3, 4, 2, 4, v3, c3comp, c3.lam, c3.flux, list(c3.fparams), c3.dt,
+                                         gravity=(0.0, 0.0, -1.0)))
+    assert e.value.status == pdg.PDG_E_UNSUPPORTED
