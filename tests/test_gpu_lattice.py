@@ -141,3 +141,161 @@ def test_lattice_p3_body_diagonal_unsupported():
     with pytest.raises(pdg.PdgError) as e:
         pdg.query_sizes(pdg.problem_from_config(cfg))
     assert e.value.status == pdg.PDG_E_UNSUPPORTED
+
+
+# --------------------------------------------------------------------------
+# Sharded collision, NCCL communicator path, CUDA-graph capture (lattice sets)
+# --------------------------------------------------------------------------
+def test_lattice_sharded_collision_standin():
+    """Row a4 for the LBM model: 3 velocity shards of D3Q27, partial moments (P = [1; v^T]),
+    reduction by torch, relax from the reduced w, with a source step fused."""
+    from dataclasses import replace
+    from paper_1702_00169_b200 import pdg
+    cfg = replace(lbm_config("D3Q27", 3), gravity=(0.0, 0.3, -1.0))
+    f = random_state(cfg, 4, 0.5).numpy()
+    G = 3
+    nvl = cfg.nv // G
+    shards = []
+    for r in range(G):
+        S = make_solver(cfg, rank=r, nranks=G, scheme=pdg.PDG_SCHEME_M2S)
+        S.set_state(to_dev(f[r * nvl:(r + 1) * nvl]), to_dev(np.zeros(S.sizes.fb_elems)))
+        S.partial_moments()
+        shards.append(S)
+    wsum = sum(S.w for S in shards)
+    for S in shards:
+        S.w.copy_(wsum)
+        S.relax_from_w(cfg.dt)
+    got = np.concatenate([to_np(S.get_state(), (nvl,) + cfg.grid_shape) for S in shards])
+    pb = oracle_problem(cfg)
+    ref = np.ascontiguousarray(f.copy())
+    O.collide(pb, ref, cfg.dt)
+    assert rel_maxnorm(got, ref) <= TOL_OP
+    with pytest.raises(Exception):
+        shards[0].collide(cfg.dt)  # no communicator: fails loudly
+    for S in shards:
+        S.destroy()
+
+
+def test_lattice_nccl_single_rank_m2s():
+    """M2s steps through libpdg's NCCL communicator with one rank (partial moments, ncclAllReduce,
+    relax_from_w with the fused source steps)."""
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import gravity_config
+    cfg = gravity_config(8, dt=0.006, t_max=0.024)
+    w0 = w0_grid(cfg)
+    S = make_solver(cfg, scheme=pdg.PDG_SCHEME_M2S, nccl_id=pdg.nccl_unique_id(), flags=pdg.PDG_PROFILE)
+    S.set_equilibrium(w0.reshape(-1).cuda())
+    S.step(cfg.steps)
+    got = to_np(S.get_state(), (cfg.nv,) + cfg.grid_shape)
+    prof = S.profile_read()
+    S.destroy()
+    assert prof["allreduce"][1] == cfg.steps and prof["relax_from_w"][1] == cfg.steps
+    pb = oracle_problem(cfg)
+    f0, fb = O.initial_data(pb, w0.numpy(), w0.numpy())
+    assert rel_maxnorm(got, O.scheme_run(pb, f0, fb, cfg.steps, "m2s")) <= TOL_STEP
+
+
+def test_lattice_cuda_graph_capture():
+    """pdg_step of a lattice set (ticket/progress memsets + persistent sweep kernels) is capturable."""
+    cfg = lbm_config("D3Q15", 6, steps=4)
+    w0 = w0_grid(cfg)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        S = make_solver(cfg, stream=stream.cuda_stream)
+        S.set_equilibrium(w0.reshape(-1).cuda())
+        f0 = S.get_state().clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            S.step(2)
+        S.set_state(f0)
+        g.replay()
+        g.replay()
+        stream.synchronize()
+    got = to_np(S.get_state(), (cfg.nv,) + cfg.grid_shape)
+    S.destroy()
+    pb = oracle_problem(cfg)
+    f0n, fb = O.initial_data(pb, w0.numpy(), w0.numpy())
+    assert rel_maxnorm(got, O.scheme_run(pb, f0n, fb, 4, "m2")) <= TOL_STEP
+
+
+# --------------------------------------------------------------------------
+# Bench sizes (the launch configuration bench.py times): properties that hold at any size
+# --------------------------------------------------------------------------
+def _perp_basis(v):
+    v = np.asarray(v[:3], dtype=np.float64)
+    n = v / np.linalg.norm(v)
+    a = np.array([1.0, 0.0, 0.0]) if abs(n[0]) < 0.9 else np.array([0.0, 1.0, 0.0])
+    u1 = np.cross(n, a)
+    u1 /= np.linalg.norm(u1)
+    u2 = np.cross(n, u1)
+    return u1, u2
+
+
+@pytest.mark.parametrize("lat,N", [("D3Q27", 128), ("D2Q9", 1024)])
+def test_lattice_fullsize_transport_of_invariant_data(lat, N):
+    """At the bench size: data of degree <= p that is constant along each velocity, with matching
+    inflow data, is a steady state of the exact transport and lies in the DG space, where L_h is
+    exact: T2 must leave it unchanged.  Exercises every wavefront class,
+    the warp scans and the cross-CTA hand-over in bench.py's launch configuration."""
+    from pdg_inputs import node_axis
+    cfg = lbm_config(lat, N, nu=2.0)
+    vel, _ = cfg.velocities()
+    S = make_solver(cfg)
+    dev = torch.device("cuda")
+    xs = [node_axis(cfg, a, device=dev) for a in range(cfg.dim)]
+    if cfg.dim == 3:
+        X, Y, Z = xs[0].view(1, 1, -1), xs[1].view(1, -1, 1), xs[2].view(-1, 1, 1)
+    else:
+        X, Y, Z = xs[0].view(1, -1), xs[1].view(-1, 1), torch.zeros((), dtype=torch.float64, device=dev)
+    f = S.f.view((cfg.nv,) + cfg.grid_shape)
+    fbv = S.fb.view(cfg.nv, cfg.dim, -1)
+    rng = np.random.default_rng(5)
+    for i, v in enumerate(vel):
+        if not any(v[:cfg.dim]):
+            u1, u2 = np.array([1.0, 0, 0]), np.array([0, 1.0, 0])
+        else:
+            vv = list(v[:cfg.dim]) + [0.0] * (3 - cfg.dim)
+            if cfg.dim == 2:
+                u1 = np.array([-vv[1], vv[0], 0.0]) / np.hypot(vv[0], vv[1])
+                u2 = u1
+            else:
+                u1, u2 = _perp_basis(vv)
+        c = rng.random(3)
+        s1 = u1[0] * X + u1[1] * Y + u1[2] * Z
+        s2 = u2[0] * X + u2[1] * Y + u2[2] * Z
+        val = (1.0 + c[0] * s1 + c[1] * s2 * s2 + c[2] * s1 * s2).expand(cfg.grid_shape)
+        f[i].copy_(val)
+        for k in range(cfg.dim):
+            if v[k] == 0:
+                continue
+            ax = cfg.dim - 1 - k
+            idx = [slice(None)] * cfg.dim
+            idx[ax] = 0 if v[k] > 0 else cfg.grid_shape[ax] - 1
+            pl = val[tuple(idx)].reshape(-1)
+            fbv[i, k, :pl.numel()].copy_(pl)
+    f0 = S.f.clone()
+    S.set_state(f0)
+    S.transport(cfg.dt)
+    err = float((S.f - f0).abs().max() / f0.abs().max())
+    S.destroy()
+    assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("lat", ["D3Q19", "D3Q15"])
+def test_lattice_fullsize_equilibrium_fixed_point(lat):
+    """At the bench size (128^3, p = 2): a constant equilibrium state with f^b = f^eq(w) is a fixed
+    point of the whole M2 step (constants are transported exactly, the collision of an equilibrium
+    is the identity)."""
+    cfg = lbm_config(lat, 128, nu=2.0)
+    S = make_solver(cfg)
+    w = torch.empty((cfg.m, cfg.nnodes), dtype=torch.float64, device="cuda")
+    w[0].fill_(1.1)
+    for d in range(cfg.dim):
+        w[1 + d].fill_(1.1 * 0.03 * (d + 1))
+    S.set_equilibrium(w.reshape(-1))
+    f0 = S.f.clone()
+    S.step(1)
+    err = float((S.f - f0).abs().max() / f0.abs().max())
+    S.destroy()
+    assert err <= 1e-13, err
