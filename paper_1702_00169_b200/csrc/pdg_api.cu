@@ -66,8 +66,9 @@ struct Geometry {
     // lattice velocity sets (PDG_FLUX_LBM, NEXT-2)
     int lattice = 0;                          // 1: general velocities, fb = [nvl][dim][plane_stride]
     int nplanes = 1;                          // inflow planes per velocity in fb
-    size_t lat_ints = 0;                      // ticket + progress counters (max over classes)
-    size_t lat_xbuf = 0, lat_ybuf = 0;        // boundary trace buffers (doubles, max over classes)
+    size_t lat_ints = 0;                      // ticket + progress counters (sum over classes)
+    size_t lat_xbuf = 0, lat_ybuf = 0;        // boundary trace buffers (doubles, sum over classes: the
+                                              // classes run concurrently on their own streams)
 };
 
 // Work decomposition of one active-axis class of lattice velocities (pdg_lattice.cuh).
@@ -76,6 +77,7 @@ struct LatPlan {
     int vel[pdg::kLatMaxVel] = {0};  // local velocity indices
     int Wx = 1, Wy = 1, ngx = 1, ngy = 1, nlane = 1, nw = 1, nc = 1, ntasks = 0;
     size_t xbuf = 0, ybuf = 0;       // doubles
+    size_t ints_off = 0, xbuf_off = 0, ybuf_off = 0;  // this class's slices of the work buffers
 };
 
 int popcount3(int a) { return (a & 1) + ((a >> 1) & 1) + ((a >> 2) & 1); }
@@ -143,7 +145,16 @@ void lattice_classes(const Geometry &g, const double *vel, std::vector<LatPlan> 
         }
         pl->vel[pl->nvel++] = j;
     }
-    for (auto &q : out) plan_lattice(g, q);
+    size_t io = 0, xo = 0, yo = 0;
+    for (auto &q : out) {
+        plan_lattice(g, q);
+        q.ints_off = io;
+        q.xbuf_off = xo;
+        q.ybuf_off = yo;
+        io += (((size_t)q.ntasks + 1 + 63) / 64) * 64;
+        xo += q.xbuf;
+        yo += q.ybuf;
+    }
 }
 
 constexpr int kMaxTables = 16;
@@ -266,9 +277,9 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
             std::vector<LatPlan> cls;
             lattice_classes(*g, p->vel, cls);
             for (const auto &q : cls) {
-                g->lat_ints = std::max(g->lat_ints, (size_t)q.ntasks + 1);
-                g->lat_xbuf = std::max(g->lat_xbuf, q.xbuf);
-                g->lat_ybuf = std::max(g->lat_ybuf, q.ybuf);
+                g->lat_ints = std::max(g->lat_ints, q.ints_off + (((size_t)q.ntasks + 1 + 63) / 64) * 64);
+                g->lat_xbuf = std::max(g->lat_xbuf, q.xbuf_off + q.xbuf);
+                g->lat_ybuf = std::max(g->lat_ybuf, q.ybuf_off + q.ybuf);
             }
         }
         return PDG_OK;
@@ -381,6 +392,9 @@ struct pdg_ctx {
     pdg::LbmParams lbm{};
     int *lat_ints = nullptr;                   // ticket + progress counters
     double *lat_xbuf = nullptr, *lat_ybuf = nullptr;
+    std::vector<cudaStream_t> lat_streams;     // one per class: the classes' wavefronts overlap
+    cudaEvent_t lat_fork = nullptr;
+    std::vector<cudaEvent_t> lat_join;
     std::map<std::pair<int, double>, pdg::LatticeBlockLD> lat_blocks;  // (act, dt') -> block
 };
 
@@ -400,19 +414,19 @@ pdg_status post_launch(pdg_ctx *c, const char *what)
 }
 
 // PDG_PROFILE: CUDA events bracketing each launch on the context stream.
-int prof_begin(pdg_ctx *c)
+int prof_begin(pdg_ctx *c, cudaStream_t st = nullptr)
 {
     if (!c->prof.on || c->prof.next + 2 > (int)c->prof.ev.size()) return -1;
     const int i = c->prof.next;
     c->prof.next += 2;
-    cudaEventRecord(c->prof.ev[i], c->stream);
+    cudaEventRecord(c->prof.ev[i], st ? st : c->stream);
     return i;
 }
 
-void prof_end(pdg_ctx *c, int i, int kind, double bytes)
+void prof_end(pdg_ctx *c, int i, int kind, double bytes, cudaStream_t st = nullptr)
 {
     if (i < 0) return;
-    cudaEventRecord(c->prof.ev[i + 1], c->stream);
+    cudaEventRecord(c->prof.ev[i + 1], st ? st : c->stream);
     c->prof.recs.push_back({kind, i, bytes});
 }
 
@@ -514,7 +528,7 @@ const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
 }
 
 template <int D, int N, int ACT>
-pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B)
+pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
 {
     using PP = pdg::LatParams<D, N, ACT>;
     using TB = pdg::LatTab<N, pdg::LatShape<D, ACT>::DA>;
@@ -524,10 +538,10 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     const Geometry &g = c->g;
     P.f = c->f;
     P.fb = c->fb;
-    P.ticket = c->lat_ints;
-    P.progress = c->lat_ints + 1;
-    P.xbuf = c->lat_xbuf;
-    P.ybuf = c->lat_ybuf;
+    P.ticket = c->lat_ints + pl.ints_off;
+    P.progress = c->lat_ints + pl.ints_off + 1;
+    P.xbuf = c->lat_xbuf + pl.xbuf_off;
+    P.ybuf = c->lat_ybuf + pl.ybuf_off;
     for (int k = 0; k < 3; ++k) {
         P.g.L[k] = g.L[k];
         P.g.stride[k] = g.stride[k];
@@ -550,48 +564,54 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
         P.v[q].fb_off = (int64_t)j * g.dim * g.plane_stride;
         for (int k = 0; k < 3; ++k) P.v[q].sign[k] = (v[k] < 0.0) ? -1 : 1;
     }
-    for (int t = 0; t < DA; ++t) {
-        for (int i = 0; i < N * N; ++i) P.tab.KG[t][i] = (double)(B.kappa[t] * B.G[i]);
-        P.tab.cin[t] = (double)(B.kappa[t] / B.w0);
-    }
-    for (int i = 0; i < TB::NB * TB::NB; ++i) P.tab.Ainv[i] = (double)B.Ainv[i];
-    for (int i = 0; i < TB::NB * TB::MF; ++i) P.tab.Qx[i] = (double)B.Qx[i];
+    constexpr int NB = TB::NB, MF = TB::MF;
+    for (int q = 0; q < NB; ++q)  // column-major (pdg_lattice.cuh LatTab)
+        for (int c = 0; c < NB; ++c) P.tab.M[c * NB + q] = (double)B.M[(size_t)q * NB + c];
+    for (int t = 0; t < DA; ++t)
+        for (int q = 0; q < NB; ++q)
+            for (int j = 0; j < MF; ++j) P.tab.Q[t][j * NB + q] = (double)B.Q[((size_t)t * NB + q) * MF + j];
     for (int s = 0; s < 5; ++s)
-        for (int i = 0; i < TB::MF * TB::MF; ++i) P.tab.Bp[s][i] = (double)B.Bpow[(size_t)s * TB::MF * TB::MF + i];
+        for (int i = 0; i < MF; ++i)
+            for (int j = 0; j < MF; ++j) P.tab.Bp[s][j * MF + i] = (double)B.Bpow[((size_t)s * MF + i) * MF + j];
     const int threads = 32 * pl.Wx * pl.Wy;
-    const size_t smem = sizeof(double) * (size_t)(threads / 32) * 2 * TB::NB * 32;  // cp.async row buffers
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             160 * 1024);
-        attr_set = true;
+    constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
+    // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
+    const size_t smem = sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? 2 * 32 * TB::MF : 0)) +
+                                          pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
+    static size_t smem_attr = 0;  // largest dynamic shared memory opted in so far
+    if (smem > smem_attr) {
+        const cudaError_t ea = cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess)
+            return fail(PDG_E_CUDA, std::string("lattice sweep shared memory opt-in: ") + cudaGetErrorString(ea));
+        smem_attr = smem;
     }
-    static std::map<int, int> occ_cache;
+    static std::map<std::pair<int, size_t>, int> occ_cache;
     int occ = 0;
-    auto oc = occ_cache.find(threads);
+    auto oc = occ_cache.find(std::make_pair(threads, smem));
     if (oc != occ_cache.end()) occ = oc->second;
     else {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT>, threads, smem) !=
             cudaSuccess)
             occ = 1;
         occ = std::max(1, occ);
-        occ_cache[threads] = occ;
+        occ_cache[std::make_pair(threads, smem)] = occ;
     }
     const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
-    PDG_CUDA_TRY(cudaMemsetAsync(c->lat_ints, 0, sizeof(int) * ((size_t)pl.ntasks + 1), c->stream));
-    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, smem, c->stream>>>(P);
+    PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)pl.ntasks + 1), st));
+    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, smem, st>>>(P);
     return PDG_OK;
 }
 
-pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp)
+pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_t st)
 {
     const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, dtp);
     if (!B) return fail(PDG_E_INVALID_ARGUMENT, "singular lattice block for this dt");
     const int D = c->g.dim, n = c->g.n, a = pl.act;
-    const int e = prof_begin(c);
+    const int e = prof_begin(c, st);
     pdg_status s = PDG_E_UNSUPPORTED;
 #define PDG_LAT(DD, NN, AA) \
-    else if (D == DD && n == NN && a == AA) s = launch_lattice_t<DD, NN, AA>(c, pl, *B)
+    else if (D == DD && n == NN && a == AA) s = launch_lattice_t<DD, NN, AA>(c, pl, *B, st)
     if (false) {}
     PDG_LAT(2, 2, 3); PDG_LAT(2, 3, 3); PDG_LAT(2, 4, 3);
     PDG_LAT(3, 2, 3); PDG_LAT(3, 3, 3); PDG_LAT(3, 4, 3);
@@ -601,13 +621,27 @@ pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp)
 #undef PDG_LAT
     if (s == PDG_E_UNSUPPORTED) return fail(s, "lattice sweep not compiled for this (dim, degree, axes)");
     if (s != PDG_OK) return s;
-    prof_end(c, e, PDG_K_LATTICE, 16.0 * (double)pl.nvel * (double)c->g.nnodes);
+    prof_end(c, e, PDG_K_LATTICE, 16.0 * (double)pl.nvel * (double)c->g.nnodes, st);
     return post_launch(c, "lattice_sweep");
 }
 
 // One pass over f applying T2(dtp) npass times (npass in {1, 2}) to the selected velocities.
 pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_ALL)
 {
+    // lattice classes: forked onto their own streams (joined below), so that their wavefront
+    // ramps overlap with each other and with the axis-aligned sweeps on the context stream
+    const bool lat = which != SWEEP_X && !c->lat_plans.empty();
+    if (lat) {
+        PDG_CUDA_TRY(cudaEventRecord(c->lat_fork, c->stream));
+        for (size_t k = 0; k < c->lat_plans.size(); ++k) {
+            PDG_CUDA_TRY(cudaStreamWaitEvent(c->lat_streams[k], c->lat_fork, 0));
+            for (int q = 0; q < npass; ++q) {
+                pdg_status ls = launch_lattice(c, c->lat_plans[k], dtp, c->lat_streams[k]);
+                if (ls != PDG_OK) return ls;
+            }
+            PDG_CUDA_TRY(cudaEventRecord(c->lat_join[k], c->lat_streams[k]));
+        }
+    }
     pdg::SweepParams xp = c->x_params, yzp = c->yz_params;
     pdg::DevBlock blk[3];
     if (!fill_blocks(c, dtp, blk)) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block for this dt");
@@ -642,12 +676,8 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_A
     }
     pdg_status s = post_launch(c, "sweep");
     if (s == PDG_OK && outer) s = zslab_resolve(c, dtp, npass);
-    if (which != SWEEP_X)
-        for (int q = 0; q < npass && s == PDG_OK; ++q)
-            for (const LatPlan &pl : c->lat_plans) {
-                s = launch_lattice(c, pl, dtp);
-                if (s != PDG_OK) break;
-            }
+    if (lat)
+        for (size_t k = 0; k < c->lat_plans.size(); ++k) PDG_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->lat_join[k], 0));
     return s;
 }
 
@@ -1318,6 +1348,25 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         c->ztables = c->zinflow + c->g.carry_doubles;
     }
     build_sweep_params(c);
+    if (!c->lat_plans.empty()) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        int prio = 0;
+        cudaStreamGetPriority(c->stream, &prio);
+        bool ok = cudaEventCreateWithFlags(&c->lat_fork, cudaEventDisableTiming) == cudaSuccess;
+        for (size_t k = 0; k < c->lat_plans.size() && ok; ++k) {
+            cudaStream_t st = nullptr;
+            cudaEvent_t ev = nullptr;
+            ok = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+            c->lat_streams.push_back(st);
+            c->lat_join.push_back(ev);
+        }
+        if (!ok) {
+            pdg_destroy(c);
+            return fail(PDG_E_CUDA, "cannot create the lattice class streams");
+        }
+    }
     if (c->g.zslab) {  // tables of the scheme's sweeps (single and fused double passes)
         std::vector<Op> ops;
         append_scheme(ops, p->scheme, p->dt);
@@ -1556,6 +1605,11 @@ void pdg_destroy(pdg_ctx *c)
 {
     if (!c) return;
     c->comm.destroy();
+    for (auto st : c->lat_streams)
+        if (st) cudaStreamDestroy(st);
+    for (auto ev : c->lat_join)
+        if (ev) cudaEventDestroy(ev);
+    if (c->lat_fork) cudaEventDestroy(c->lat_fork);
     for (auto &e : c->prof.ev)
         if (e) cudaEventDestroy(e);
     delete c;

@@ -64,11 +64,11 @@ template <int N, int DA>
 struct LatTab {
     static constexpr int NB = ipow(N, DA);
     static constexpr int MF = NB / N;
-    double KG[DA][N * N];   // kappa_t G (flow order)
-    double cin[DA];         // kappa_t / omega_0
-    double Ainv[NB * NB];
-    double Qx[NB * MF];
-    double Bp[5][MF * MF];  // Bx^(2^j)
+    // stored column-major ([column][row]): the kernels stream one column at a time into NB
+    // independent accumulators, so consecutive rows are adjacent (LDCU.128 loads two at once)
+    double M[NB * NB];      // A^{-1} (I + sum_t kappa_t G^(t)),                  M[c * NB + q]
+    double Q[DA][NB * MF];  // A^{-1} E_in^(t) kappa_t / omega_0 (in-traces of axis t), Q[t][j * NB + q]
+    double Bp[5][MF * MF];  // Bx^(2^j), Bx = rows of Q[0] on the x-out face,     Bp[s][j * MF + i]
 };
 
 struct LatVel {
@@ -118,6 +118,33 @@ __device__ __forceinline__ void st_release(int *p, int v)
 {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+
+// D = A B + D on the fp64 tensor cores (DMMA.8x8x4).  Fragments (PTX ISA, mma.m8n8k4.f64):
+// A[8x4] row-major: lane holds A[lane/4][lane%4]; B[4x8] col: lane holds B[lane%4][lane/4];
+// C/D[8x8]: lane holds D[lane/4][2(lane%4)], D[lane/4][2(lane%4)+1].
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b)
+{
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
+// Tensor-core path of the lattice sweep: used for the body diagonals (3 active axes), whose
+// n^3 x n^3 block makes the unit update fp64-bound.
+template <int D, int N, int ACT>
+struct LatMma {
+    using S = LatShape<D, ACT>;
+    static constexpr int NB = ipow(N, S::DA), MF = NB / N;
+    static constexpr bool USE = (S::DA == 3);
+    static constexpr int MT = (NB + 7) / 8;                     // 8-row tiles of the block
+    static constexpr int KE = NB + (S::PIPE ? 2 : 1) * MF;      // [f_old; chain in-trace; pipe in-trace]
+    static constexpr int KS = (KE + 3) / 4;                     // k-steps of the first product
+    static constexpr int KSX = (MF + 3) / 4;                    // k-steps of Q_x s_x
+    static constexpr size_t smem_doubles(int nwarps)
+    {
+        return USE ? (size_t)nwarps * NB * 32 + (size_t)MT * 8 * (KS + KSX) * 4 : 0;
+    }
+};
 
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc)
 {
@@ -170,22 +197,53 @@ __device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const 
     }
 }
 
+// registers capped for two CTAs per SM on the FMA path (the f_old of a unit is read from shared
+// memory and the block is streamed column by column, so ~NB + 3 MF doubles are live); the tensor
+// path needs ~218 KB of shared memory and runs one CTA per SM
 template <int D, int N, int ACT>
-__global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
+__global__ void __launch_bounds__(256, LatMma<D, N, ACT>::USE ? 1 : 2)
+    lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
     using S = LatShape<D, ACT>;
     using TB = LatTab<N, S::DA>;
     constexpr int DA = S::DA, NB = TB::NB, MF = TB::MF;
     constexpr int XA = S::XA, PIPE = S::PIPE, CA = S::CA, TC = S::TC;
     constexpr int TY = S::T1;
+    using MMA = LatMma<D, N, ACT>;
+    constexpr bool USE_MMA = MMA::USE;
+    constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
     const unsigned FULL = 0xffffffffu;
 
     __shared__ double xs[2][8][XA ? MF : 1];
-    __shared__ double ys[2][8][PIPE ? 32 : 1][PIPE ? MF : 1];
     __shared__ int s_task;
-    // per-warp double buffer of the unit values of the current and the next row (cp.async
-    // prefetch: the loads of row r+1 do not depend on the carries and overlap row r's math)
+    // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
+    // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
+    // math), then the y hand-over buffers [2][warps][32][MF] (PIPE)
     extern __shared__ double sfo[];  // [warp][2][NB][32]
+    const int nwarps = blockDim.x >> 5;
+    double *ysb = sfo + (size_t)nwarps * 2 * NB * 32;
+    auto YS = [&](int buf, int w, int l) -> double * { return ysb + (((size_t)buf * nwarps + w) * 32 + l) * MF; };
+    // (tensor path) per-warp staging rows [NB][32], then the A operands [M|Qc|Qp] and Qx
+    double *stg_base = ysb + (PIPE ? (size_t)2 * nwarps * 32 * MF : 0);
+    double *sA = stg_base + (USE_MMA ? (size_t)nwarps * NB * 32 : 0);
+    double *sAx = sA + (size_t)MT * 8 * KS * 4;
+    if constexpr (USE_MMA) {
+        for (int i = threadIdx.x; i < MT * 8 * KS * 4; i += blockDim.x) {
+            const int q = i / (KS * 4), k = i % (KS * 4);
+            double v = 0.0;
+            if (q < NB) {
+                if (k < NB) v = P.tab.M[k * NB + q];
+                else if (k < NB + MF) v = P.tab.Q[TC][(k - NB) * NB + q];
+                else if (PIPE && k < KE) v = P.tab.Q[TY][(k - NB - MF) * NB + q];
+            }
+            sA[i] = v;
+        }
+        for (int i = threadIdx.x; i < MT * 8 * KSX * 4; i += blockDim.x) {
+            const int q = i / (KSX * 4), k = i % (KSX * 4);
+            sAx[i] = (q < NB && k < MF && XA) ? P.tab.Q[0][k * NB + q] : 0.0;
+        }
+        __syncthreads();
+    }
 
     const LatGeom &g = P.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -264,90 +322,51 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                 if (r == 0) prefetch(0);
                 prefetch(r + 1);
                 cp_async_wait<1>();  // row r has landed (row r+1 may still be in flight)
-                double fo[NB];
+                // f_old of the unit stays in shared memory (per-lane column: conflict-free)
                 const double *src = wbuf + (r & 1) * NB * 32 + lane;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) fo[q] = valid ? src[q * 32] : 0.0;
                 // pipe (y) in-trace
                 double sy[PIPE ? MF : 1];
                 if constexpr (PIPE) {
                     if (wy > 0) {
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) sy[j] = ys[(t - 1) & 1][warp - g.Wx][lane][j];
+                        for (int j = 0; j < MF; ++j) sy[j] = YS((t - 1) & 1, warp - g.Wx, lane)[j];
                     } else if (gy > 0) {
                         wait_progress(P.progress + task - per_gy, r + 1);
-                        const double *src = P.ybuf + ((((int64_t)(task - per_gy) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
+                        const double *ysrc = P.ybuf + ((((int64_t)(task - per_gy) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) sy[j] = __ldcg(src + j);
+                        for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
                     } else {
 #pragma unroll
                         for (int j = 0; j < MF; ++j) sy[j] = 0.0;
                         if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
                     }
                 }
-                // rhs = (I + sum_t kappa_t G^(t)) f_old + inflows of the chain and pipe axes
-                // (loops ordered so that the NB accumulators are independent chains: ILP for the DFMA pipe)
-                double rhs[NB];
+                // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
+                double s0[XA ? MF : 1];
 #pragma unroll
-                for (int q = 0; q < NB; ++q) rhs[q] = fo[q];
-#pragma unroll
-                for (int tt = 0; tt < DA; ++tt)
-#pragma unroll
-                    for (int b = 0; b < N; ++b)
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) {
-                            const int a = (q / ipow(N, tt)) % N;
-                            rhs[q] = fma(P.tab.KG[tt][a * N + b], fo[q + (b - a) * ipow(N, tt)], rhs[q]);
-                        }
-#pragma unroll
-                for (int j = 0; j < MF; ++j) {
-                    const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1);
-                    rhs[q] = fma(P.tab.cin[TC], sc[j], rhs[q]);
-                }
-                if constexpr (PIPE) {
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) {
-                        const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1);
-                        rhs[q] = fma(P.tab.cin[TY], sy[j], rhs[q]);
-                    }
-                }
-                double fn[NB];
-#pragma unroll
-                for (int q = 0; q < NB; ++q) fn[q] = P.tab.Ainv[q * NB] * rhs[0];
-#pragma unroll
-                for (int c = 1; c < NB; ++c)
-#pragma unroll
-                    for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Ainv[q * NB + c], rhs[c], fn[q]);
+                for (int j = 0; j < (XA ? MF : 1); ++j) s0[j] = 0.0;
                 if constexpr (XA) {
-                    // x in-trace of the warp (lane 0's cell)
-                    double s0[MF];
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) s0[j] = 0.0;
                     if (qx > 0) {
 #pragma unroll
                         for (int j = 0; j < MF; ++j) s0[j] = xs[(t - 1) & 1][warp - 1][j];
                     } else if (gx > 0) {
                         wait_progress(P.progress + task - 1, r + 1);
-                        const double *src = P.xbuf + (((int64_t)(task - 1) * g.nc + r) * g.Wy + wy) * MF;
+                        const double *xsrc = P.xbuf + (((int64_t)(task - 1) * g.nc + r) * g.Wy + wy) * MF;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) s0[j] = __ldcg(src + j);
+                        for (int j = 0; j < MF; ++j) s0[j] = __ldcg(xsrc + j);
                     } else if (lane == 0 && valid) {
                         ghost_face<D, N, ACT, 0>(P, V, ucell, s0);
                     }
-                    // zero-inflow x out-trace of every cell; lane 0 adds Bx s0
-                    double a[MF];
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) a[j] = valid ? fo[j * N + N - 1] + fn[j * N + N - 1] : 0.0;
+                }
+                // x scan: in a[] the zero-inflow x out-traces of the lanes' cells; returns the
+                // inclusive out-traces in a[] and every lane's true x in-trace in sin_[]
+                auto xscan = [&](double (&a)[MF], double (&sin_)[MF]) {
                     if (lane == 0) {
 #pragma unroll
-                        for (int i = 0; i < MF; ++i) {
-                            double acc = a[i];
+                        for (int j = 0; j < MF; ++j)
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) acc = fma(P.tab.Bp[0][i * MF + j], s0[j], acc);
-                            a[i] = acc;
-                        }
+                            for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[0][j * MF + i], s0[j], a[i]);
                     }
-                    // inclusive scan y_l = a_l + Bx y_{l-1}
 #pragma unroll
                     for (int sidx = 0; sidx < 5; ++sidx) {
                         const int o = 1 << sidx;
@@ -358,19 +377,14 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
 #pragma unroll
-                                for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[sidx][i * MF + j], pv[j], a[i]);
+                                for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[sidx][j * MF + i], pv[j], a[i]);
                         }
                     }
-                    double sin_[MF];
 #pragma unroll
                     for (int j = 0; j < MF; ++j) {
                         const double up = __shfl_up_sync(FULL, a[j], 1);
                         sin_[j] = (lane == 0) ? s0[j] : up;
                     }
-#pragma unroll
-                    for (int j = 0; j < MF; ++j)
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Qx[q * MF + j], sin_[j], fn[q]);
                     // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
                     if (lane == 31) {
 #pragma unroll
@@ -381,6 +395,123 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
                             for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
                             __threadfence();
                         }
+                    }
+                };
+                double fn[NB];
+                if constexpr (USE_MMA) {
+                    // fp64 tensor cores (DMMA 8x8x4): the warp's 32 units are the N dimension.
+                    //   F0 = [M | Q_chain | Q_pipe] [F_old; S_chain; S_pipe]     (NB x K) (K x 32)
+                    //   F  = F0 + Q_x S_x_in                                     after the x scan
+                    // B operands come from shared memory: F_old from the cp.async row buffer, the
+                    // in-traces from the warp's staging rows; A operands from the CTA's tables.
+                    const double *fsrc = wbuf + (r & 1) * NB * 32;
+                    double *stg = stg_base + (size_t)warp * NB * 32;
+#pragma unroll
+                    for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sc[j];
+                    if constexpr (PIPE) {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) stg[(MF + j) * 32 + lane] = sy[j];
+                    }
+                    __syncwarp();
+                    double acc[MT][4][2];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+                    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        const int k = ks * 4 + tq;
+                        double b[4];
+#pragma unroll
+                        for (int nt = 0; nt < 4; ++nt) {
+                            const int u = nt * 8 + gq;
+                            if (ks * 4 + 3 < NB) b[nt] = fsrc[k * 32 + u];
+                            else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[(k - NB) * 32 + u];
+                            else b[nt] = (k < NB) ? fsrc[k * 32 + u] : ((k < KE) ? stg[(k - NB) * 32 + u] : 0.0);
+                        }
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const double av = sA[(mt * 8 + gq) * (KS * 4) + k];
+#pragma unroll
+                            for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
+                        }
+                    }
+                    auto spill = [&]() {  // accumulators -> staging rows [q][unit]
+                        __syncwarp();
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int nt = 0; nt < 4; ++nt) {
+                                const int q = mt * 8 + gq;
+                                if (q < NB) {
+                                    stg[q * 32 + nt * 8 + 2 * tq] = acc[mt][nt][0];
+                                    stg[q * 32 + nt * 8 + 2 * tq + 1] = acc[mt][nt][1];
+                                }
+                            }
+                        __syncwarp();
+                    };
+                    spill();
+                    if constexpr (XA) {
+                        double a[MF], sin_[MF];
+#pragma unroll
+                        for (int j = 0; j < MF; ++j)
+                            a[j] = valid ? fsrc[(j * N + N - 1) * 32 + lane] + stg[(j * N + N - 1) * 32 + lane] : 0.0;
+                        xscan(a, sin_);
+                        __syncwarp();
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sin_[j];
+                        __syncwarp();
+#pragma unroll
+                        for (int ks = 0; ks < KSX; ++ks) {
+                            const int k = ks * 4 + tq;
+                            double b[4];
+#pragma unroll
+                            for (int nt = 0; nt < 4; ++nt) b[nt] = (k < MF) ? stg[k * 32 + nt * 8 + gq] : 0.0;
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                const double av = sAx[(mt * 8 + gq) * (KSX * 4) + k];
+#pragma unroll
+                                for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
+                            }
+                        }
+                        spill();
+                    }
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) fn[q] = stg[q * 32 + lane];
+                } else {
+                    // FMA pipe: f_new (without the x inflow) = M f_old + Q_chain s_chain + Q_pipe s_pipe,
+                    // streamed column by column: NB independent accumulators, one shared-memory load each
+                    {
+                        const double f0v = src[0];
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) fn[q] = P.tab.M[q] * f0v;
+                    }
+#pragma unroll
+                    for (int c = 1; c < NB; ++c) {
+                        const double fc = src[c * 32];
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.M[c * NB + q], fc, fn[q]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < MF; ++j)
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TC][j * NB + q], sc[j], fn[q]);
+                    if constexpr (PIPE) {
+#pragma unroll
+                        for (int j = 0; j < MF; ++j)
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TY][j * NB + q], sy[j], fn[q]);
+                    }
+                    if constexpr (XA) {
+                        double a[MF], sin_[MF];
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) a[j] = valid ? src[(j * N + N - 1) * 32] + fn[j * N + N - 1] : 0.0;
+                        xscan(a, sin_);
+#pragma unroll
+                        for (int j = 0; j < MF; ++j)
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[0][j * NB + q], sin_[j], fn[q]);
                     }
                 }
                 if (valid) {
@@ -396,17 +527,17 @@ __global__ void __launch_bounds__(256, 1) lattice_sweep_kernel(const __grid_cons
 #pragma unroll
                 for (int j = 0; j < MF; ++j) {
                     const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1) + (N - 1) * ipow(N, TC);
-                    sc[j] = fo[q] + fn[q];
+                    sc[j] = src[q * 32] + fn[q];
                 }
                 if constexpr (PIPE) {
                     double ty[MF];
 #pragma unroll
                     for (int j = 0; j < MF; ++j) {
                         const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1) + (N - 1) * ipow(N, TY);
-                        ty[j] = fo[q] + fn[q];
+                        ty[j] = src[q * 32] + fn[q];
                     }
 #pragma unroll
-                    for (int j = 0; j < MF; ++j) ys[t & 1][warp][lane][j] = ty[j];
+                    for (int j = 0; j < MF; ++j) YS(t & 1, warp, lane)[j] = ty[j];
                     if (wy == g.Wy - 1 && gy < g.ngy - 1) {
                         double *dst = P.ybuf + ((((int64_t)task * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
 #pragma unroll

@@ -153,7 +153,9 @@ struct LatticeBlockLD {
     long double kappa[3];                    // per active axis
     long double w0;                          // omega_0
     std::vector<long double> Ainv;           // nb x nb
-    std::vector<long double> Qx;             // nb x mf
+    std::vector<long double> M;              // nb x nb: A^{-1} (I + sum_t kappa_t G^(t))
+    std::vector<long double> Q;              // d x nb x mf: A^{-1} E_in^(t) kappa_t / omega_0
+    std::vector<long double> Qx;             // nb x mf (= Q of t = 0)
     std::vector<long double> Bpow;           // 5 x mf x mf
 };
 
@@ -224,10 +226,23 @@ inline bool lattice_block(int p, int d, const long double *kappa, LatticeBlockLD
     }
     if (!invert_dense(nb, A, B.Ainv)) return false;
     const int mf = B.mf;
-    B.Qx.assign((size_t)nb * mf, 0.0L);
-    // x-in face node j (digits of the other active axes) = reduced node j * n (a_0 = 0)
+    // M = A^{-1} (2 I - A): the explicit half (I + sum kappa G) pre-multiplied
+    B.M.assign((size_t)nb * nb, 0.0L);
     for (int r = 0; r < nb; ++r)
-        for (int j = 0; j < mf; ++j) B.Qx[(size_t)r * mf + j] = B.Ainv[(size_t)r * nb + j * n] * B.kappa[0] / B.w0;
+        for (int c = 0; c < nb; ++c) {
+            long double acc = 0.0L;
+            for (int k = 0; k < nb; ++k) acc += B.Ainv[(size_t)r * nb + k] * (((k == c) ? 2.0L : 0.0L) - A[(size_t)k * nb + c]);
+            B.M[(size_t)r * nb + c] = acc;
+        }
+    // inflow responses: in-face node j of axis t = reduced node with digit t = 0
+    B.Q.assign((size_t)d * nb * mf, 0.0L);
+    for (int t = 0; t < d; ++t)
+        for (int r = 0; r < nb; ++r)
+            for (int j = 0; j < mf; ++j) {
+                const int q = (j % pw[t]) + (j / pw[t]) * pw[t + 1];
+                B.Q[((size_t)t * nb + r) * mf + j] = B.Ainv[(size_t)r * nb + q] * B.kappa[t] / B.w0;
+            }
+    B.Qx.assign(B.Q.begin(), B.Q.begin() + (size_t)nb * mf);
     std::vector<long double> Bx((size_t)mf * mf), T((size_t)mf * mf);
     for (int i = 0; i < mf; ++i)
         for (int j = 0; j < mf; ++j) Bx[(size_t)i * mf + j] = B.Qx[(size_t)(i * n + n - 1) * mf + j];
