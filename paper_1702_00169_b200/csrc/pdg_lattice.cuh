@@ -135,7 +135,11 @@ template <int D, int N, int ACT>
 struct LatMma {
     using S = LatShape<D, ACT>;
     static constexpr int NB = ipow(N, S::DA), MF = NB / N;
+#ifdef PDG_LATTICE_MMA_ALL
+    static constexpr bool USE = true;
+#else
     static constexpr bool USE = (S::DA == 3);
+#endif
     static constexpr int MT = (NB + 7) / 8;                     // 8-row tiles of the block
     static constexpr int KE = NB + (S::PIPE ? 2 : 1) * MF;      // [f_old; chain in-trace; pipe in-trace]
     static constexpr int KS = (KE + 3) / 4;                     // k-steps of the first product
@@ -201,7 +205,7 @@ __device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const 
 // memory and the block is streamed column by column, so ~NB + 3 MF doubles are live); the tensor
 // path needs ~218 KB of shared memory and runs one CTA per SM
 template <int D, int N, int ACT>
-__global__ void __launch_bounds__(256, LatMma<D, N, ACT>::USE ? 1 : 2)
+__global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
     using S = LatShape<D, ACT>;
