@@ -53,13 +53,20 @@ def random_lattice_inputs(cfg, seed):
     return f, fb_full
 
 
-@pytest.mark.parametrize("warps", [None, "1,1", "2,2"], indirect=True)
-@pytest.mark.parametrize("lat,N,p", cases())
-@pytest.mark.parametrize("dtp_nu", [0.5, -0.05, 2.0])
+def _transport_params():
+    """Every case with the default CTA shape; the grids large enough for several CTAs along x or
+    the pipe axis also with 1x1 and 2x2 warps per CTA (cross-CTA hand-over)."""
+    out = []
+    for lat, N, p in cases():
+        for warps in ([None, "1,1", "2,2"] if (N >= 30 or lat == "D2Q9") else [None]):
+            for nu in (0.5, -0.05, 2.0):
+                out.append(pytest.param(lat, N, p, nu, warps, id=f"{lat}-N{N}-p{p}-nu{nu}-w{warps}"))
+    return out
+
+
+@pytest.mark.parametrize("lat,N,p,dtp_nu,warps", _transport_params(), indirect=["warps"])
 def test_lattice_transport_parity(lat, N, p, dtp_nu, warps):
     """One T2(dt') of every velocity (rows a1/a3 for lattice sets) == the oracle's Kahn sweep."""
-    if warps and N < 30 and lat != "D2Q9":
-        pytest.skip("hand-over variants are exercised on the larger grids")
     cfg = lbm_config(lat, N, p=p)
     f, fb_full = random_lattice_inputs(cfg, 11 + N + p)
     S = make_solver(cfg)
