@@ -116,8 +116,9 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     P.ntasks = P.nvel * P.ngx * P.ngy;
     int mf = 1;
     for (int t = 1; t < P.d; ++t) mf *= g.n;
-    P.xbuf = (XA && P.ngx > 1) ? (size_t)P.ntasks * P.nc * P.Wy * mf : 0;
-    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)P.ntasks * P.nc * P.Wx * 32 * mf : 0;
+    // boundary traces of up to two sweeps per launch
+    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wy * mf : 0;
+    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * mf : 0;
 }
 
 // Active-axis mask of a lattice velocity (bit k set if v_k != 0).
@@ -527,7 +528,7 @@ const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
     return &(c->lat_blocks[key] = std::move(B));
 }
 
-template <int D, int N, int ACT>
+template <int D, int N, int ACT, int NPASS>
 pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
 {
     using PP = pdg::LatParams<D, N, ACT>;
@@ -576,11 +577,12 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     const int threads = 32 * pl.Wx * pl.Wy;
     constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
-    const size_t smem = sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? 2 * 32 * TB::MF : 0)) +
-                                          pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
+    const size_t smem =
+        sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
+                          pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
     static size_t smem_attr = 0;  // largest dynamic shared memory opted in so far
     if (smem > smem_attr) {
-        const cudaError_t ea = cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT>,
+        const cudaError_t ea = cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT, NPASS>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess)
             return fail(PDG_E_CUDA, std::string("lattice sweep shared memory opt-in: ") + cudaGetErrorString(ea));
@@ -591,7 +593,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     auto oc = occ_cache.find(std::make_pair(threads, smem));
     if (oc != occ_cache.end()) occ = oc->second;
     else {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT>, threads, smem) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT, NPASS>, threads, smem) !=
             cudaSuccess)
             occ = 1;
         occ = std::max(1, occ);
@@ -599,30 +601,41 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     }
     const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
     PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)pl.ntasks + 1), st));
-    pdg::lattice_sweep_kernel<D, N, ACT><<<grid, threads, smem, st>>>(P);
+    pdg::lattice_sweep_kernel<D, N, ACT, NPASS><<<grid, threads, smem, st>>>(P);
     return PDG_OK;
 }
 
-pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_t st)
+// One pass over the velocities of class `pl` applying T2(dtp) npass times: the FMA-path classes
+// (two active axes) take both sweeps in one launch, the body diagonals (tensor path) one each.
+pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_t st, int npass)
 {
     const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, dtp);
     if (!B) return fail(PDG_E_INVALID_ARGUMENT, "singular lattice block for this dt");
     const int D = c->g.dim, n = c->g.n, a = pl.act;
-    const int e = prof_begin(c, st);
-    pdg_status s = PDG_E_UNSUPPORTED;
-#define PDG_LAT(DD, NN, AA) \
-    else if (D == DD && n == NN && a == AA) s = launch_lattice_t<DD, NN, AA>(c, pl, *B, st)
-    if (false) {}
-    PDG_LAT(2, 2, 3); PDG_LAT(2, 3, 3); PDG_LAT(2, 4, 3);
-    PDG_LAT(3, 2, 3); PDG_LAT(3, 3, 3); PDG_LAT(3, 4, 3);
-    PDG_LAT(3, 2, 5); PDG_LAT(3, 3, 5); PDG_LAT(3, 4, 5);
-    PDG_LAT(3, 2, 6); PDG_LAT(3, 3, 6); PDG_LAT(3, 4, 6);
-    PDG_LAT(3, 2, 7); PDG_LAT(3, 3, 7);
+    // (2-D grids are latency-bound: one sweep per launch keeps the per-row chain short)
+    const bool fused = (npass == 2 && popcount3(a) < 3 && D == 3);
+    for (int q = 0; q < (fused ? 1 : npass); ++q) {
+        const int e = prof_begin(c, st);
+        pdg_status s = PDG_E_UNSUPPORTED;
+#define PDG_LAT(DD, NN, AA, NP) \
+    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_t<DD, NN, AA, NP>(c, pl, *B, st)
+        if (false) {}
+        PDG_LAT(2, 2, 3, 1); PDG_LAT(2, 3, 3, 1); PDG_LAT(2, 4, 3, 1);
+        PDG_LAT(3, 2, 3, 1); PDG_LAT(3, 3, 3, 1); PDG_LAT(3, 4, 3, 1);
+        PDG_LAT(3, 2, 5, 1); PDG_LAT(3, 3, 5, 1); PDG_LAT(3, 4, 5, 1);
+        PDG_LAT(3, 2, 6, 1); PDG_LAT(3, 3, 6, 1); PDG_LAT(3, 4, 6, 1);
+        PDG_LAT(3, 2, 7, 1); PDG_LAT(3, 3, 7, 1);
+        PDG_LAT(3, 2, 3, 2); PDG_LAT(3, 3, 3, 2); PDG_LAT(3, 4, 3, 2);
+        PDG_LAT(3, 2, 5, 2); PDG_LAT(3, 3, 5, 2); PDG_LAT(3, 4, 5, 2);
+        PDG_LAT(3, 2, 6, 2); PDG_LAT(3, 3, 6, 2); PDG_LAT(3, 4, 6, 2);
 #undef PDG_LAT
-    if (s == PDG_E_UNSUPPORTED) return fail(s, "lattice sweep not compiled for this (dim, degree, axes)");
-    if (s != PDG_OK) return s;
-    prof_end(c, e, PDG_K_LATTICE, 16.0 * (double)pl.nvel * (double)c->g.nnodes, st);
-    return post_launch(c, "lattice_sweep");
+        if (s == PDG_E_UNSUPPORTED) return fail(s, "lattice sweep not compiled for this (dim, degree, axes)");
+        if (s != PDG_OK) return s;
+        prof_end(c, e, PDG_K_LATTICE, 16.0 * (double)pl.nvel * (double)c->g.nnodes, st);
+        s = post_launch(c, "lattice_sweep");
+        if (s != PDG_OK) return s;
+    }
+    return PDG_OK;
 }
 
 // One pass over f applying T2(dtp) npass times (npass in {1, 2}) to the selected velocities.
@@ -635,10 +648,8 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_A
         PDG_CUDA_TRY(cudaEventRecord(c->lat_fork, c->stream));
         for (size_t k = 0; k < c->lat_plans.size(); ++k) {
             PDG_CUDA_TRY(cudaStreamWaitEvent(c->lat_streams[k], c->lat_fork, 0));
-            for (int q = 0; q < npass; ++q) {
-                pdg_status ls = launch_lattice(c, c->lat_plans[k], dtp, c->lat_streams[k]);
-                if (ls != PDG_OK) return ls;
-            }
+            pdg_status ls = launch_lattice(c, c->lat_plans[k], dtp, c->lat_streams[k], npass);
+            if (ls != PDG_OK) return ls;
             PDG_CUDA_TRY(cudaEventRecord(c->lat_join[k], c->lat_streams[k]));
         }
     }

@@ -201,10 +201,13 @@ __device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const 
     }
 }
 
-// registers capped for two CTAs per SM on the FMA path (the f_old of a unit is read from shared
-// memory and the block is streamed column by column, so ~NB + 3 MF doubles are live); the tensor
-// path needs ~218 KB of shared memory and runs one CTA per SM
-template <int D, int N, int ACT>
+// NPASS = 2 applies T2 twice in one pass over f (step n's trailing and step n+1's leading
+// T2(dt/2), as the line sweeps do; both sweeps keep their own traces and hand-overs, the
+// second sweep reads the first one's output from registers).  Registers are capped for two
+// CTAs per SM on the FMA path (the two-sweep variant spills a few bytes, measured faster than
+// one CTA per SM without spills); the tensor path (body diagonals, NPASS = 1) needs ~218 KB of
+// shared memory and runs one CTA per SM.
+template <int D, int N, int ACT, int NPASS>
 __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
@@ -216,19 +219,22 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     using MMA = LatMma<D, N, ACT>;
     constexpr bool USE_MMA = MMA::USE;
     constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
+    static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     const unsigned FULL = 0xffffffffu;
 
-    __shared__ double xs[2][8][XA ? MF : 1];
+    __shared__ double xs[NPASS][2][8][XA ? MF : 1];
     __shared__ int s_task;
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
     // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
-    // math), then the y hand-over buffers [2][warps][32][MF] (PIPE)
+    // math), then the y hand-over buffers [pass][2][warps][32][MF] (PIPE)
     extern __shared__ double sfo[];  // [warp][2][NB][32]
     const int nwarps = blockDim.x >> 5;
     double *ysb = sfo + (size_t)nwarps * 2 * NB * 32;
-    auto YS = [&](int buf, int w, int l) -> double * { return ysb + (((size_t)buf * nwarps + w) * 32 + l) * MF; };
+    auto YS = [&](int ps, int buf, int w, int l) -> double * {
+        return ysb + ((((size_t)ps * 2 + buf) * nwarps + w) * 32 + l) * MF;
+    };
     // (tensor path) per-warp staging rows [NB][32], then the A operands [M|Qc|Qp] and Qx
-    double *stg_base = ysb + (PIPE ? (size_t)2 * nwarps * 32 * MF : 0);
+    double *stg_base = ysb + (PIPE ? (size_t)NPASS * 2 * nwarps * 32 * MF : 0);
     double *sA = stg_base + (USE_MMA ? (size_t)nwarps * NB * 32 : 0);
     double *sAx = sA + (size_t)MT * 8 * KS * 4;
     if constexpr (USE_MMA) {
@@ -296,10 +302,18 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         const int64_t cstep = (int64_t)V.sign[CA] * g.stride[CA] * N;                        // one chain cell
         const int64_t cbase = (V.sign[CA] > 0) ? 0 : (g.L[CA] - 1) * g.stride[CA];          // chain cell 0
 
-        double sc[MF];
+        // chain in-traces of every sweep (the ghost f^b is constant in time: same for both)
+        double sc[NPASS][MF];
+        {
+            double s0c[MF];
 #pragma unroll
-        for (int j = 0; j < MF; ++j) sc[j] = 0.0;
-        if (valid) ghost_face<D, N, ACT, CA>(P, V, ucell, sc);
+            for (int j = 0; j < MF; ++j) s0c[j] = 0.0;
+            if (valid) ghost_face<D, N, ACT, CA>(P, V, ucell, s0c);
+#pragma unroll
+            for (int ps = 0; ps < NPASS; ++ps)
+#pragma unroll
+                for (int j = 0; j < MF; ++j) sc[ps][j] = s0c[j];
+        }
 
         double *wbuf = sfo + (size_t)warp * 2 * NB * 32;
         // issue the copies of row rr into buffer rr & 1 (one commit group per row)
@@ -328,195 +342,227 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 cp_async_wait<1>();  // row r has landed (row r+1 may still be in flight)
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
                 const double *src = wbuf + (r & 1) * NB * 32 + lane;
-                // pipe (y) in-trace
-                double sy[PIPE ? MF : 1];
-                if constexpr (PIPE) {
-                    if (wy > 0) {
+                double fprev[NB];  // input of the second sweep (output of the first)
+                double fn[NB];
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) sy[j] = YS((t - 1) & 1, warp - g.Wx, lane)[j];
-                    } else if (gy > 0) {
-                        wait_progress(P.progress + task - per_gy, r + 1);
-                        const double *ysrc = P.ybuf + ((((int64_t)(task - per_gy) * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
+                for (int ps = 0; ps < NPASS; ++ps) {
+                    // f_old of this sweep: the row buffer (first) or the first sweep's result
+                    auto fold = [&](int c) -> double { return (ps == 0) ? src[c * 32] : fprev[c]; };
+                    // pipe (y) in-trace
+                    double sy[PIPE ? MF : 1];
+                    if constexpr (PIPE) {
+                        if (wy > 0) {
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
-                    } else {
+                            for (int j = 0; j < MF; ++j) sy[j] = YS(ps, (t - 1) & 1, warp - g.Wx, lane)[j];
+                        } else if (gy > 0) {
+                            if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
+                            const double *ysrc =
+                                P.ybuf + (((((int64_t)(task - per_gy) * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MF;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) sy[j] = 0.0;
-                        if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
+                            for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) sy[j] = 0.0;
+                            if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
+                        }
                     }
-                }
-                // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
-                double s0[XA ? MF : 1];
+                    // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
+                    double s0[XA ? MF : 1];
 #pragma unroll
-                for (int j = 0; j < (XA ? MF : 1); ++j) s0[j] = 0.0;
-                if constexpr (XA) {
-                    if (qx > 0) {
+                    for (int j = 0; j < (XA ? MF : 1); ++j) s0[j] = 0.0;
+                    if constexpr (XA) {
+                        if (qx > 0) {
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) s0[j] = xs[(t - 1) & 1][warp - 1][j];
-                    } else if (gx > 0) {
-                        wait_progress(P.progress + task - 1, r + 1);
-                        const double *xsrc = P.xbuf + (((int64_t)(task - 1) * g.nc + r) * g.Wy + wy) * MF;
+                            for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) & 1][warp - 1][j];
+                        } else if (gx > 0) {
+                            if (ps == 0) wait_progress(P.progress + task - 1, r + 1);
+                            const double *xsrc = P.xbuf + ((((int64_t)(task - 1) * g.nc + r) * NPASS + ps) * g.Wy + wy) * MF;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) s0[j] = __ldcg(xsrc + j);
-                    } else if (lane == 0 && valid) {
-                        ghost_face<D, N, ACT, 0>(P, V, ucell, s0);
+                            for (int j = 0; j < MF; ++j) s0[j] = __ldcg(xsrc + j);
+                        } else if (lane == 0 && valid) {
+                            ghost_face<D, N, ACT, 0>(P, V, ucell, s0);
+                        }
                     }
-                }
-                // x scan: in a[] the zero-inflow x out-traces of the lanes' cells; returns the
-                // inclusive out-traces in a[] and every lane's true x in-trace in sin_[]
-                auto xscan = [&](double (&a)[MF], double (&sin_)[MF]) {
-                    if (lane == 0) {
-#pragma unroll
-                        for (int j = 0; j < MF; ++j)
-#pragma unroll
-                            for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[0][j * MF + i], s0[j], a[i]);
-                    }
-#pragma unroll
-                    for (int sidx = 0; sidx < 5; ++sidx) {
-                        const int o = 1 << sidx;
-                        double pv[MF];
-#pragma unroll
-                        for (int j = 0; j < MF; ++j) pv[j] = __shfl_up_sync(FULL, a[j], o);
-                        if (lane >= o) {
+                    // x scan: in a[] the zero-inflow x out-traces of the lanes' cells; returns the
+                    // inclusive out-traces in a[] and every lane's true x in-trace in sin_[]
+                    auto xscan = [&](double (&a)[MF], double (&sin_)[MF]) {
+                        if (lane == 0) {
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
 #pragma unroll
-                                for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[sidx][j * MF + i], pv[j], a[i]);
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) {
-                        const double up = __shfl_up_sync(FULL, a[j], 1);
-                        sin_[j] = (lane == 0) ? s0[j] : up;
-                    }
-                    // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
-                    if (lane == 31) {
-#pragma unroll
-                        for (int j = 0; j < MF; ++j) xs[t & 1][warp][j] = a[j];
-                        if (qx == g.Wx - 1 && gx < g.ngx - 1) {
-                            double *dst = P.xbuf + (((int64_t)task * g.nc + r) * g.Wy + wy) * MF;
-#pragma unroll
-                            for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
-                            __threadfence();
-                        }
-                    }
-                };
-                double fn[NB];
-                if constexpr (USE_MMA) {
-                    // fp64 tensor cores (DMMA 8x8x4): the warp's 32 units are the N dimension.
-                    //   F0 = [M | Q_chain | Q_pipe] [F_old; S_chain; S_pipe]     (NB x K) (K x 32)
-                    //   F  = F0 + Q_x S_x_in                                     after the x scan
-                    // B operands come from shared memory: F_old from the cp.async row buffer, the
-                    // in-traces from the warp's staging rows; A operands from the CTA's tables.
-                    const double *fsrc = wbuf + (r & 1) * NB * 32;
-                    double *stg = stg_base + (size_t)warp * NB * 32;
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sc[j];
-                    if constexpr (PIPE) {
-#pragma unroll
-                        for (int j = 0; j < MF; ++j) stg[(MF + j) * 32 + lane] = sy[j];
-                    }
-                    __syncwarp();
-                    double acc[MT][4][2];
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-                    const int gq = lane >> 2, tq = lane & 3;
-#pragma unroll
-                    for (int ks = 0; ks < KS; ++ks) {
-                        const int k = ks * 4 + tq;
-                        double b[4];
-#pragma unroll
-                        for (int nt = 0; nt < 4; ++nt) {
-                            const int u = nt * 8 + gq;
-                            if (ks * 4 + 3 < NB) b[nt] = fsrc[k * 32 + u];
-                            else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[(k - NB) * 32 + u];
-                            else b[nt] = (k < NB) ? fsrc[k * 32 + u] : ((k < KE) ? stg[(k - NB) * 32 + u] : 0.0);
+                                for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[0][j * MF + i], s0[j], a[i]);
                         }
 #pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) {
-                            const double av = sA[(mt * 8 + gq) * (KS * 4) + k];
+                        for (int sidx = 0; sidx < 5; ++sidx) {
+                            const int o = 1 << sidx;
+                            double pv[MF];
 #pragma unroll
-                            for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
+                            for (int j = 0; j < MF; ++j) pv[j] = __shfl_up_sync(FULL, a[j], o);
+                            if (lane >= o) {
+#pragma unroll
+                                for (int j = 0; j < MF; ++j)
+#pragma unroll
+                                    for (int i = 0; i < MF; ++i) a[i] = fma(P.tab.Bp[sidx][j * MF + i], pv[j], a[i]);
+                            }
                         }
-                    }
-                    auto spill = [&]() {  // accumulators -> staging rows [q][unit]
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) {
+                            const double up = __shfl_up_sync(FULL, a[j], 1);
+                            sin_[j] = (lane == 0) ? s0[j] : up;
+                        }
+                        // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
+                        if (lane == 31) {
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) xs[ps][t & 1][warp][j] = a[j];
+                            if (qx == g.Wx - 1 && gx < g.ngx - 1) {
+                                double *dst = P.xbuf + ((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wy + wy) * MF;
+#pragma unroll
+                                for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
+                                __threadfence();
+                            }
+                        }
+                    };
+                    if constexpr (USE_MMA) {
+                        // fp64 tensor cores (DMMA 8x8x4): the warp's 32 units are the N dimension.
+                        //   F0 = [M | Q_chain | Q_pipe] [F_old; S_chain; S_pipe]     (NB x K) (K x 32)
+                        //   F  = F0 + Q_x S_x_in                                     after the x scan
+                        // B operands come from shared memory: F_old from the cp.async row buffer, the
+                        // in-traces from the warp's staging rows; A operands from the CTA's tables.
+                        const double *fsrc = wbuf + (r & 1) * NB * 32;
+                        double *stg = stg_base + (size_t)warp * NB * 32;
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sc[ps][j];
+                        if constexpr (PIPE) {
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) stg[(MF + j) * 32 + lane] = sy[j];
+                        }
                         __syncwarp();
+                        double acc[MT][4][2];
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                            for (int nt = 0; nt < 4; ++nt) {
-                                const int q = mt * 8 + gq;
-                                if (q < NB) {
-                                    stg[q * 32 + nt * 8 + 2 * tq] = acc[mt][nt][0];
-                                    stg[q * 32 + nt * 8 + 2 * tq + 1] = acc[mt][nt][1];
-                                }
-                            }
-                        __syncwarp();
-                    };
-                    spill();
-                    if constexpr (XA) {
-                        double a[MF], sin_[MF];
+                            for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+                        const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j)
-                            a[j] = valid ? fsrc[(j * N + N - 1) * 32 + lane] + stg[(j * N + N - 1) * 32 + lane] : 0.0;
-                        xscan(a, sin_);
-                        __syncwarp();
-#pragma unroll
-                        for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sin_[j];
-                        __syncwarp();
-#pragma unroll
-                        for (int ks = 0; ks < KSX; ++ks) {
+                        for (int ks = 0; ks < KS; ++ks) {
                             const int k = ks * 4 + tq;
                             double b[4];
 #pragma unroll
-                            for (int nt = 0; nt < 4; ++nt) b[nt] = (k < MF) ? stg[k * 32 + nt * 8 + gq] : 0.0;
+                            for (int nt = 0; nt < 4; ++nt) {
+                                const int u = nt * 8 + gq;
+                                if (ks * 4 + 3 < NB) b[nt] = fsrc[k * 32 + u];
+                                else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[(k - NB) * 32 + u];
+                                else b[nt] = (k < NB) ? fsrc[k * 32 + u] : ((k < KE) ? stg[(k - NB) * 32 + u] : 0.0);
+                            }
 #pragma unroll
                             for (int mt = 0; mt < MT; ++mt) {
-                                const double av = sAx[(mt * 8 + gq) * (KSX * 4) + k];
+                                const double av = sA[(mt * 8 + gq) * (KS * 4) + k];
 #pragma unroll
                                 for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
                             }
                         }
+                        auto spill = [&]() {  // accumulators -> staging rows [q][unit]
+                            __syncwarp();
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                                for (int nt = 0; nt < 4; ++nt) {
+                                    const int q = mt * 8 + gq;
+                                    if (q < NB) {
+                                        stg[q * 32 + nt * 8 + 2 * tq] = acc[mt][nt][0];
+                                        stg[q * 32 + nt * 8 + 2 * tq + 1] = acc[mt][nt][1];
+                                    }
+                                }
+                            __syncwarp();
+                        };
                         spill();
+                        if constexpr (XA) {
+                            double a[MF], sin_[MF];
+#pragma unroll
+                            for (int j = 0; j < MF; ++j)
+                                a[j] = valid ? fsrc[(j * N + N - 1) * 32 + lane] + stg[(j * N + N - 1) * 32 + lane] : 0.0;
+                            xscan(a, sin_);
+                            __syncwarp();
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sin_[j];
+                            __syncwarp();
+#pragma unroll
+                            for (int ks = 0; ks < KSX; ++ks) {
+                                const int k = ks * 4 + tq;
+                                double b[4];
+#pragma unroll
+                                for (int nt = 0; nt < 4; ++nt) b[nt] = (k < MF) ? stg[k * 32 + nt * 8 + gq] : 0.0;
+#pragma unroll
+                                for (int mt = 0; mt < MT; ++mt) {
+                                    const double av = sAx[(mt * 8 + gq) * (KSX * 4) + k];
+#pragma unroll
+                                    for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
+                                }
+                            }
+                            spill();
+                        }
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) fn[q] = stg[q * 32 + lane];
+                    } else {
+                        // FMA pipe: f_new (without the x inflow) = M f_old + Q_chain s_chain + Q_pipe s_pipe,
+                        // streamed column by column: NB independent accumulators
+                        {
+                            const double f0v = fold(0);
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) fn[q] = P.tab.M[q] * f0v;
+                        }
+#pragma unroll
+                        for (int c = 1; c < NB; ++c) {
+                            const double fc = fold(c);
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.M[c * NB + q], fc, fn[q]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < MF; ++j)
+#pragma unroll
+                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TC][j * NB + q], sc[ps][j], fn[q]);
+                        if constexpr (PIPE) {
+#pragma unroll
+                            for (int j = 0; j < MF; ++j)
+#pragma unroll
+                                for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TY][j * NB + q], sy[j], fn[q]);
+                        }
+                        if constexpr (XA) {
+                            double a[MF], sin_[MF];
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) a[j] = valid ? fold(j * N + N - 1) + fn[j * N + N - 1] : 0.0;
+                            xscan(a, sin_);
+#pragma unroll
+                            for (int j = 0; j < MF; ++j)
+#pragma unroll
+                                for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[0][j * NB + q], sin_[j], fn[q]);
+                        }
                     }
+                    // chain out-trace -> next row (registers)
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) fn[q] = stg[q * 32 + lane];
-                } else {
-                    // FMA pipe: f_new (without the x inflow) = M f_old + Q_chain s_chain + Q_pipe s_pipe,
-                    // streamed column by column: NB independent accumulators, one shared-memory load each
-                    {
-                        const double f0v = src[0];
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = P.tab.M[q] * f0v;
+                    for (int j = 0; j < MF; ++j) {
+                        const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1) + (N - 1) * ipow(N, TC);
+                        sc[ps][j] = fold(q) + fn[q];
                     }
-#pragma unroll
-                    for (int c = 1; c < NB; ++c) {
-                        const double fc = src[c * 32];
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.M[c * NB + q], fc, fn[q]);
-                    }
-#pragma unroll
-                    for (int j = 0; j < MF; ++j)
-#pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TC][j * NB + q], sc[j], fn[q]);
                     if constexpr (PIPE) {
+                        double ty[MF];
 #pragma unroll
-                        for (int j = 0; j < MF; ++j)
+                        for (int j = 0; j < MF; ++j) {
+                            const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1) + (N - 1) * ipow(N, TY);
+                            ty[j] = fold(q) + fn[q];
+                        }
 #pragma unroll
-                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TY][j * NB + q], sy[j], fn[q]);
+                        for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
+                        if (wy == g.Wy - 1 && gy < g.ngy - 1) {
+                            double *dst =
+                                P.ybuf + (((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MF;
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
+                            __threadfence();
+                        }
                     }
-                    if constexpr (XA) {
-                        double a[MF], sin_[MF];
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) a[j] = valid ? src[(j * N + N - 1) * 32] + fn[j * N + N - 1] : 0.0;
-                        xscan(a, sin_);
-#pragma unroll
-                        for (int j = 0; j < MF; ++j)
-#pragma unroll
-                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[0][j * NB + q], sin_[j], fn[q]);
-                    }
+                    for (int q = 0; q < NB; ++q) fprev[q] = fn[q];
                 }
                 if (valid) {
 #pragma unroll
@@ -524,29 +570,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         int64_t off = 0;
 #pragma unroll
                         for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
-                        __stcs(P.f + ub + off, fn[q]);
-                    }
-                }
-                // chain out-trace -> next row (registers)
-#pragma unroll
-                for (int j = 0; j < MF; ++j) {
-                    const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1) + (N - 1) * ipow(N, TC);
-                    sc[j] = src[q * 32] + fn[q];
-                }
-                if constexpr (PIPE) {
-                    double ty[MF];
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) {
-                        const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1) + (N - 1) * ipow(N, TY);
-                        ty[j] = src[q * 32] + fn[q];
-                    }
-#pragma unroll
-                    for (int j = 0; j < MF; ++j) YS(t & 1, warp, lane)[j] = ty[j];
-                    if (wy == g.Wy - 1 && gy < g.ngy - 1) {
-                        double *dst = P.ybuf + ((((int64_t)task * g.nc + r) * g.Wx + qx) * 32 + lane) * MF;
-#pragma unroll
-                        for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
-                        __threadfence();
+                        __stcs(P.f + ub + off, fprev[q]);
                     }
                 }
             }
