@@ -415,3 +415,49 @@ def test_zslab_m2kin_and_unfused():
         Z.step(2)
         ref = O.scheme_run(pb, f0, fbg, 2, "m2kin" if "scheme" in kw else "m2")
         assert rel_maxnorm(to_np(Z.get_state(), f0.shape), ref) < TOL_STEP
+
+
+# --------------------------------------------------------------------------
+# Anisotropic boxes (vectorial sets): different cell counts and sizes per axis
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,ncell,p,flux,fparams,m,hi", [
+    (3, (37, 5, 9), 2, 2, (1.0,), 4, (1.0, 0.4, 0.7)),
+    (3, (4, 33, 3), 3, 2, (1.0,), 4, (0.5, 1.0, 0.3)),
+    (2, (40, 7), 2, 1, (1.4,), 4, (1.0, 0.25, 1.0)),
+    (2, (3, 70), 1, 0, (1.0, -0.5), 1, (1.0, 1.0, 1.0)),
+])
+def test_anisotropic_transport_and_steps(dim, ncell, p, flux, fparams, m, hi):
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import velocity_set
+    lam = 3.5
+    vel, comp = velocity_set(dim, m, lam)
+    h = min(hi[d] / ncell[d] for d in range(dim))
+    dt = 0.6 * h / lam
+    pb = pdg.make_problem(dim, list(ncell), p, m, vel, comp, lam, flux, list(fparams), dt, hi=tuple(hi))
+    ob = O.Problem(dim, list(ncell), p, vel, comp, m, lam, flux, list(fparams), dt, hi=list(hi))
+    S = pdg.Solver(pb)
+    shape = ob.grid_shape()
+    rng = np.random.default_rng(sum(ncell))
+    # positive density state near equilibrium-like magnitudes (Euler needs positive pressure)
+    base = {0: 0.5, 1: 1.0, 2: 1.0}[flux]
+    f = base * (1.0 + 0.05 * (rng.random((ob.nv,) + shape) - 0.5)) / (2 * dim)
+    if flux == 1:  # energy component: keep E large enough for p > 0
+        f[3 * 2 * dim:] *= 3.0
+    fb_full = base * (1.0 + 0.05 * rng.random((ob.nv,) + shape)) / (2 * dim)
+
+    class _C:
+        pass
+    cv = _C()
+    cv.dim, cv.grid_shape = dim, shape
+    S.set_state(to_dev(f), to_dev(full_grid_to_planes(cv, fb_full, S.sizes.plane_stride)))
+    S.transport(dt)
+    got = to_np(S.get_state(), f.shape)
+    fc = ob.grid_to_cells(f)
+    fbc = ob.grid_to_cells(fb_full)
+    O.t2_all(ob, dt, fc, fbc)
+    assert rel_maxnorm(got, ob.cells_to_grid(fc)) < TOL_OP
+    S.step(3)
+    got3 = to_np(S.get_state(), f.shape)
+    ref3 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 3)
+    S.destroy()
+    assert rel_maxnorm(got3, ref3) < TOL_STEP
