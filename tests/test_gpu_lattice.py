@@ -43,6 +43,7 @@ def cases():
         ("D2Q9", 37, 2), ("D2Q9", 8, 1), ("D2Q9", 9, 3),
         ("D3Q15", 5, 2), ("D3Q19", 5, 2), ("D3Q27", 5, 2),
         ("D3Q19", 4, 3), ("D3Q27", 3, 1), ("D3Q15", 33, 2),
+        ("D3Q27", 1, 2), ("D2Q9", 1, 2), ("D3Q19", 2, 3),   # degenerate: one / two cells per axis
     ]
 
 
