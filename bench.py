@@ -376,8 +376,8 @@ def main():
     if args.lattice:
         args.cpu_cells = min(args.cpu_cells, 24 if cfg.dim == 3 else 256)
         args.ref_cells = min(args.ref_cells, 16 if cfg.dim == 3 else 128)
-    if args.decomp is None:
-        args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "velocity"
+    if args.decomp is None:  # the z-slab decomposition is implemented for axis-aligned sets only
+        args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not args.lattice else "velocity"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

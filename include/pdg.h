@@ -64,7 +64,7 @@ typedef struct pdg_ctx pdg_ctx; /* opaque, owned by the library */
 
 typedef enum {
     PDG_OK = 0,
-    PDG_E_INVALID_ARGUMENT = 1, /* NULL pointer, bad size, dt == 0, lambda <= 0, tau < 0, nv % nranks != 0 */
+    PDG_E_INVALID_ARGUMENT = 1, /* NULL pointer, bad size, dt == 0, lambda <= 0, tau < 0, nranks > nv */
     PDG_E_DIMENSION = 2,        /* dim not in {2, 3}                                   (SPEC DimensionOutOfRange) */
     PDG_E_DEGREE = 3,           /* degree not in the compiled set {1, 2, 3}            (SPEC DegreeOutOfRange) */
     PDG_E_VELOCITY_SET = 4,     /* velocities not the canonical +-lambda e_k per component set, or comp[] wrong */
@@ -111,8 +111,9 @@ typedef enum {
 } pdg_source_kind;
 
 typedef enum {
-    PDG_DECOMP_VELOCITY = 0, /* rank r owns velocities [r nv/G, (r+1) nv/G) on the whole grid; one NCCL
-                                sum of the m moment fields per collision (north star) */
+    PDG_DECOMP_VELOCITY = 0, /* rank r owns a contiguous block of velocities (sizes nv/G or nv/G + 1, the
+                                first nv % G ranks one more) on the whole grid; one NCCL sum of the m
+                                moment fields per collision (north star) */
     PDG_DECOMP_ZSLAB = 1     /* rank r owns the cell planes [r N/G, (r+1) N/G) of the slowest axis (z in 3-D,
                                 y in 2-D) with every velocity; sweeps along that axis run per slab with zero
                                 inflow, the exact inflows follow from an affine scan of the slabs' outgoing
@@ -160,7 +161,7 @@ typedef struct {
     double tau;                  /* relaxation time; 0 => f <- 2 f^eq - f */
     double dt;                   /* time step of one palindromic step (may be negative) */
     int32_t scheme;              /* pdg_scheme */
-    int32_t rank, nranks;        /* velocity shard: contiguous block of nv/nranks velocity indices */
+    int32_t rank, nranks;        /* shard of this process (see pdg_decomposition) */
     const void *nccl_id;         /* 128-byte ncclUniqueId (identical on all ranks).  Non-NULL: the context
                                     owns an NCCL communicator and the collision takes the sharded path
                                     (partial moments, NCCL sum, relax) -- also with nranks == 1.

@@ -270,9 +270,11 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     g->nv = p->nv;
     g->gnnodes = g->nnodes;
     if (p->decomposition == PDG_DECOMP_VELOCITY) {
-        if (p->nv % p->nranks != 0) return fail(PDG_E_INVALID_ARGUMENT, "nv must be divisible by nranks");
-        g->nvl = p->nv / p->nranks;
-        g->v0 = p->rank * g->nvl;
+        // contiguous velocity blocks; sizes differ by at most one (the lattice sets have odd n_v)
+        if (p->nranks > p->nv) return fail(PDG_E_INVALID_ARGUMENT, "more ranks than velocities");
+        const int base = p->nv / p->nranks, extra = p->nv % p->nranks;
+        g->nvl = base + (p->rank < extra ? 1 : 0);
+        g->v0 = p->rank * base + std::min(p->rank, extra);
         g->gncell_outer = g->ncell[p->dim - 1];
         if (g->lattice) {
             std::vector<LatPlan> cls;

@@ -118,10 +118,13 @@ def test_query_sizes_lattice(lat):
     s = pdg.query_sizes(pdg.problem_from_config(cfg))
     assert s.f_elems == cfg.nv * cfg.nnodes and s.w_elems == cfg.m * cfg.nnodes
     assert s.fb_elems == cfg.nv * cfg.dim * s.plane_stride  # one inflow plane per axis
-    for G in (3,) if cfg.nv % 3 == 0 else (1,):
+    for G in (2, 3, 4, 8):  # contiguous blocks, sizes nv//G or nv//G + 1 (first nv % G ranks)
+        begin = 0
         for r in range(G):
             t = pdg.query_sizes(pdg.problem_from_config(cfg, rank=r, nranks=G))
-            assert t.nv_local == cfg.nv // G and t.v_begin == r * (cfg.nv // G)
+            assert t.v_begin == begin and t.nv_local == cfg.nv // G + (1 if r < cfg.nv % G else 0)
+            begin += t.nv_local
+        assert begin == cfg.nv
 
 
 def test_lattice_validation_errors():

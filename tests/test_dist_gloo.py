@@ -67,8 +67,8 @@ def test_max_over_ranks():
 
 def _shards(rank, world):
     from paper_1702_00169_b200 import dist as pd
-    from pdg_inputs import CONFIGS
-    return [pd.shard(CONFIGS[k], rank, world) for k in (2, 5)]
+    from pdg_inputs import CONFIGS, lbm_config
+    return [pd.shard(c, rank, world) for c in (CONFIGS[2], CONFIGS[5], lbm_config("D3Q27", 4))]
 
 
 def test_shards_partition_the_velocities():
@@ -76,6 +76,8 @@ def test_shards_partition_the_velocities():
     for k, nv in enumerate((16, 24)):
         got = sorted(r[k] for r in res)
         assert got == [(0, nv // 2), (nv // 2, nv // 2)]
+    # odd lattice set: uneven contiguous blocks (14 + 13)
+    assert sorted(r[2] for r in res) == [(0, 14), (14, 13)]
 
 
 def _sharded_collision(rank, world):

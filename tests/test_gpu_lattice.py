@@ -155,25 +155,26 @@ def test_lattice_p3_body_diagonal_unsupported():
 # Sharded collision, NCCL communicator path, CUDA-graph capture (lattice sets)
 # --------------------------------------------------------------------------
 def test_lattice_sharded_collision_standin():
-    """Row a4 for the LBM model: 3 velocity shards of D3Q27, partial moments (P = [1; v^T]),
+    """Row a4 for the LBM model: 4 uneven velocity shards of D3Q27, partial moments (P = [1; v^T]),
     reduction by torch, relax from the reduced w, with a source step fused."""
     from dataclasses import replace
     from paper_1702_00169_b200 import pdg
     cfg = replace(lbm_config("D3Q27", 3), gravity=(0.0, 0.3, -1.0))
     f = random_state(cfg, 4, 0.5).numpy()
-    G = 3
-    nvl = cfg.nv // G
+    G = 4  # uneven shards: 7, 7, 7, 6 velocities
     shards = []
     for r in range(G):
         S = make_solver(cfg, rank=r, nranks=G, scheme=pdg.PDG_SCHEME_M2S)
-        S.set_state(to_dev(f[r * nvl:(r + 1) * nvl]), to_dev(np.zeros(S.sizes.fb_elems)))
+        v0, nvl = S.sizes.v_begin, S.sizes.nv_local
+        assert nvl == (7 if r < 3 else 6) and v0 == 7 * r
+        S.set_state(to_dev(f[v0:v0 + nvl]), to_dev(np.zeros(S.sizes.fb_elems)))
         S.partial_moments()
         shards.append(S)
     wsum = sum(S.w for S in shards)
     for S in shards:
         S.w.copy_(wsum)
         S.relax_from_w(cfg.dt)
-    got = np.concatenate([to_np(S.get_state(), (nvl,) + cfg.grid_shape) for S in shards])
+    got = np.concatenate([to_np(S.get_state(), (S.sizes.nv_local,) + cfg.grid_shape) for S in shards])
     pb = oracle_problem(cfg)
     ref = np.ascontiguousarray(f.copy())
     O.collide(pb, ref, cfg.dt)
