@@ -20,6 +20,7 @@
 
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <utility>
 
 #ifndef PDG_VERSION
@@ -399,6 +400,7 @@ struct pdg_ctx {
     cudaEvent_t lat_fork = nullptr;
     std::vector<cudaEvent_t> lat_join;
     std::map<std::pair<int, double>, pdg::LatticeBlockLD> lat_blocks;  // (act, dt') -> block
+    std::map<std::tuple<const void *, int, size_t>, int> launch_cache;  // (kernel, threads, smem) -> CTAs/SM
 };
 
 namespace {
@@ -582,24 +584,21 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     const size_t smem =
         sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
-    static size_t smem_attr = 0;  // largest dynamic shared memory opted in so far
-    if (smem > smem_attr) {
-        const cudaError_t ea = cudaFuncSetAttribute(pdg::lattice_sweep_kernel<D, N, ACT, NPASS>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy
+    const void *kfn = reinterpret_cast<const void *>(pdg::lattice_sweep_kernel<D, N, ACT, NPASS>);
+    const auto key = std::make_tuple(kfn, threads, smem);
+    auto oc = c->launch_cache.find(key);
+    int occ = 0;
+    if (oc != c->launch_cache.end()) occ = oc->second;
+    else {
+        const cudaError_t ea = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess)
             return fail(PDG_E_CUDA, std::string("lattice sweep shared memory opt-in: ") + cudaGetErrorString(ea));
-        smem_attr = smem;
-    }
-    static std::map<std::pair<int, size_t>, int> occ_cache;
-    int occ = 0;
-    auto oc = occ_cache.find(std::make_pair(threads, smem));
-    if (oc != occ_cache.end()) occ = oc->second;
-    else {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT, NPASS>, threads, smem) !=
-            cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT, NPASS>, threads,
+                                                          smem) != cudaSuccess)
             occ = 1;
         occ = std::max(1, occ);
-        occ_cache[std::make_pair(threads, smem)] = occ;
+        c->launch_cache[key] = occ;
     }
     const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
     PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)pl.ntasks + 1), st));
@@ -714,11 +713,11 @@ size_t relax_x_smem(const pdg_ctx *c)
 template <int DIM, int MODEL, int N, int NPASS, int K>
 void launch_relax_x_k(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
 {
-    static bool attr_set = false;
     auto kern = pdg::relax_xsweep_kernel<DIM, MODEL, N, NPASS, K>;
-    if (!attr_set) {
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
+    if (c->launch_cache.find(key) == c->launch_cache.end()) {  // per context: attributes are per device
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+        c->launch_cache[key] = 1;
     }
     const unsigned nlines = (unsigned)(c->g.nnodes / (c->g.ncell[0] * N));
     kern<<<nlines, 256, smem, c->stream>>>(P);
