@@ -648,38 +648,38 @@ __device__ __forceinline__ void lbm_moments(const double (&fv)[NV], const LbmPar
 }
 
 // S2(hs1) C2 S2(hs2) at one node from its (full) moments w; fv in/out (local velocities only
-// matter: entries outside [v0, v0 + nvl) are left as they are).
+// matter: entries outside [v0, v0 + nvl) are left as they are).  Composed into one update per
+// velocity so that every velocity constant is used once (the compiler then keeps them as
+// constant operands instead of hoisting ~4 nv of them into registers):
+//   S2(h): f += h g, g_i = w_i v_i.(rho G)/c^2, rho u += h rho G   (rho unchanged)
+//   => f <- ca f + (ca hs1 + hs2) g + cb f^eq(w + hs1 (0, rho G))
 template <int D, int NV>
 __device__ __forceinline__ void lbm_local_ops(double (&fv)[NV], double (&w)[D + 1], const LbmParams &L,
                                               const LocalOps &op)
 {
-    // source on the equilibrium part: g_i = w_i v_i.(rho G)/c^2, S2(h): f += h g, rho u += h rho G
     double gs[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) gs[d] = w[0] * L.G[d] * L.inv_c2;
-    if (op.hs1 != 0.0) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            double vg = 0.0;
-#pragma unroll
-            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
-            fv[i] = fma(op.hs1 * L.wgt[i], vg, fv[i]);
-        }
-#pragma unroll
-        for (int d = 0; d < D; ++d) w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
+    for (int d = 0; d < D; ++d) {
+        gs[d] = w[0] * L.G[d] * L.inv_c2;
+        w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
     }
-    if (op.cb != 0.0 || op.ca != 1.0) {
+    const double hg = fma(op.ca, op.hs1, op.hs2);
+    if (op.cb != 0.0) {
         const LbmNode<D> nd(w, L);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) fv[i] = fma(op.cb, nd.feq(i, L), op.ca * fv[i]);
-    }
-    if (op.hs2 != 0.0) {
+        for (int i = 0; i < NV; ++i) {
+            double vg = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+            fv[i] = fma(op.cb, nd.feq(i, L), fma(hg * L.wgt[i], vg, op.ca * fv[i]));
+        }
+    } else {
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             double vg = 0.0;
 #pragma unroll
             for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
-            fv[i] = fma(op.hs2 * L.wgt[i], vg, fv[i]);
+            fv[i] = fma(hg * L.wgt[i], vg, op.ca * fv[i]);
         }
     }
 }
@@ -698,9 +698,24 @@ __global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, 
         for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
         double w[D + 1];
         lbm_moments<D, NV>(fv, L, w);
-        lbm_local_ops<D, NV>(fv, w, L, op);
+        // lbm_local_ops, with every velocity stored as soon as it is updated (fewer live registers)
+        double gs[D];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) __stcs(f + (int64_t)i * nnodes + x, fv[i]);
+        for (int d = 0; d < D; ++d) {
+            gs[d] = w[0] * L.G[d] * L.inv_c2;
+            w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
+        }
+        const double hg = fma(op.ca, op.hs1, op.hs2);
+        const LbmNode<D> nd(w, L);
+        const double cb = op.cb;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double vg = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+            const double fs = fma(hg * L.wgt[i], vg, op.ca * fv[i]);
+            __stcs(f + (int64_t)i * nnodes + x, (cb != 0.0) ? fma(cb, nd.feq(i, L), fs) : fs);
+        }
     }
 }
 
