@@ -77,6 +77,7 @@ struct LatPlan {
     int act = 0, d = 0, nvel = 0;
     int vel[pdg::kLatMaxVel] = {0};  // local velocity indices
     int Wx = 1, Wy = 1, ngx = 1, ngy = 1, nlane = 1, nw = 1, nc = 1, ntasks = 0;
+    int cs = 1, ntasks_c = 0;  // cluster size along the pipe axis, cluster-level tasks
     size_t xbuf = 0, ybuf = 0;       // doubles
     size_t ints_off = 0, xbuf_off = 0, ybuf_off = 0;  // this class's slices of the work buffers
 };
@@ -114,7 +115,20 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     }
     P.ngx = (P.nlane + 32 * P.Wx - 1) / (32 * P.Wx);
     P.ngy = (P.nw + P.Wy - 1) / P.Wy;
-    P.ntasks = P.nvel * P.ngx * P.ngy;
+    // pipe classes may use clusters of CTAs along the pipe axis (y traces through DSMEM, one
+    // cluster barrier per row); measured slower than independent CTAs on B200,
+    // so the default is 1 and PDG_LATTICE_CLUSTER=2|4|8 selects them
+    P.cs = 1;
+    if (PIPE) {
+        if (const char *e = std::getenv("PDG_LATTICE_CLUSTER")) {
+            const int v = std::atoi(e);
+            if (v == 1 || v == 2 || v == 4 || v == 8) P.cs = std::min(v, std::max(1, P.ngy));
+            if (P.cs == 3) P.cs = 2;
+        }
+    }
+    const int ngyc = (P.ngy + P.cs - 1) / P.cs;
+    P.ntasks_c = P.nvel * P.ngx * ngyc;
+    P.ntasks = P.ntasks_c * P.cs;  // CTA-level tasks incl. the padding of the last cluster group
     int mf = 1;
     for (int t = 1; t < P.d; ++t) mf *= g.n;
     // boundary traces of up to two sweeps per launch
@@ -532,7 +546,7 @@ const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
     return &(c->lat_blocks[key] = std::move(B));
 }
 
-template <int D, int N, int ACT, int NPASS>
+template <int D, int N, int ACT, int NPASS, int CS>
 pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
 {
     using PP = pdg::LatParams<D, N, ACT>;
@@ -561,6 +575,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.g.nw = pl.nw;
     P.g.nc = pl.nc;
     P.g.ntasks = pl.ntasks;
+    P.g.ntasks_c = pl.ntasks_c;
     P.g.nvel = pl.nvel;
     for (int q = 0; q < pl.nvel; ++q) {
         const int j = pl.vel[q];
@@ -585,29 +600,59 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
         sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
     // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy
-    const void *kfn = reinterpret_cast<const void *>(pdg::lattice_sweep_kernel<D, N, ACT, NPASS>);
+    auto kern = pdg::lattice_sweep_kernel<D, N, ACT, NPASS, CS>;
+    const void *kfn = reinterpret_cast<const void *>(kern);
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute la[1];
+    lc.blockDim = dim3((unsigned)threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = CS;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.attrs = la;
+    lc.numAttrs = (CS > 1) ? 1 : 0;
     const auto key = std::make_tuple(kfn, threads, smem);
     auto oc = c->launch_cache.find(key);
-    int occ = 0;
+    int occ = 0;  // resident CTAs (CS = 1) or clusters (CS > 1) on the whole GPU
     if (oc != c->launch_cache.end()) occ = oc->second;
     else {
         const cudaError_t ea = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess)
             return fail(PDG_E_CUDA, std::string("lattice sweep shared memory opt-in: ") + cudaGetErrorString(ea));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdg::lattice_sweep_kernel<D, N, ACT, NPASS>, threads,
-                                                          smem) != cudaSuccess)
-            occ = 1;
+        if (CS > 1) {
+            lc.gridDim = dim3((unsigned)(CS * c->sms));
+            if (cudaOccupancyMaxActiveClusters(&occ, kern, &lc) != cudaSuccess) occ = 1;
+        } else {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
+            occ *= c->sms;
+        }
+        cudaGetLastError();
         occ = std::max(1, occ);
         c->launch_cache[key] = occ;
     }
-    const int grid = std::max(1, std::min(pl.ntasks, c->sms * occ));
+    const int units = std::max(1, std::min(pl.ntasks_c, occ));
+    lc.gridDim = dim3((unsigned)(units * CS));
     PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)pl.ntasks + 1), st));
-    pdg::lattice_sweep_kernel<D, N, ACT, NPASS><<<grid, threads, smem, st>>>(P);
+    PDG_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, P));
     return PDG_OK;
 }
 
+// cluster size dispatch (pipe classes only: 3-D with y and z active)
+template <int D, int N, int ACT, int NPASS>
+pdg_status launch_lattice_cs(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
+{
+    if constexpr (pdg::LatShape<D, ACT>::PIPE) {
+        if (pl.cs == 2) return launch_lattice_t<D, N, ACT, NPASS, 2>(c, pl, B, st);
+        if (pl.cs == 4) return launch_lattice_t<D, N, ACT, NPASS, 4>(c, pl, B, st);
+        if (pl.cs == 8) return launch_lattice_t<D, N, ACT, NPASS, 8>(c, pl, B, st);
+    }
+    return launch_lattice_t<D, N, ACT, NPASS, 1>(c, pl, B, st);
+}
+
 // One pass over the velocities of class `pl` applying T2(dtp) npass times: the FMA-path classes
-// (two active axes) take both sweeps in one launch, the body diagonals (tensor path) one each.
+// (two active axes in 3-D) take both sweeps in one launch, the others one each.
 pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_t st, int npass)
 {
     const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, dtp);
@@ -619,7 +664,7 @@ pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_
         const int e = prof_begin(c, st);
         pdg_status s = PDG_E_UNSUPPORTED;
 #define PDG_LAT(DD, NN, AA, NP) \
-    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_t<DD, NN, AA, NP>(c, pl, *B, st)
+    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_cs<DD, NN, AA, NP>(c, pl, *B, st)
         if (false) {}
         PDG_LAT(2, 2, 3, 1); PDG_LAT(2, 3, 3, 1); PDG_LAT(2, 4, 3, 1);
         PDG_LAT(3, 2, 3, 1); PDG_LAT(3, 3, 3, 1); PDG_LAT(3, 4, 3, 1);

@@ -28,6 +28,7 @@
 //  P = [1; v^T], f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2))
 //  (P:1138-1145), f <- ca f + cb f^eq (eq collision_cn).
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -88,9 +89,9 @@ struct LatGeom {
     int32_t nlane;       // x cells (x active) or x nodes
     int32_t nw;          // pipe cells, batch nodes or 1
     int32_t nc;          // chain cells
-    int32_t ntasks;
+    int32_t ntasks;      // CTA-level tasks (pipe groups padded to a multiple of the cluster size)
     int32_t nvel;
-    int32_t pad;
+    int32_t ntasks_c;    // cluster-level tasks (== ntasks without clusters)
 };
 
 template <int D, int N, int ACT>
@@ -207,10 +208,15 @@ __device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const 
 // CTAs per SM on the FMA path (the two-sweep variant spills a few bytes, measured faster than
 // one CTA per SM without spills); the tensor path (body diagonals, NPASS = 1) needs ~218 KB of
 // shared memory and runs one CTA per SM.
-template <int D, int N, int ACT, int NPASS>
+// CS > 1: thread-block clusters of CS CTAs along the pipe axis (consecutive pipe groups): the
+// y hand-over between the cluster's CTAs goes through distributed shared memory and the
+// cluster advances in lockstep (one cluster barrier per row); global traces and progress
+// flags remain only at cluster boundaries.
+template <int D, int N, int ACT, int NPASS, int CS>
 __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
+    namespace cg = cooperative_groups;
     using S = LatShape<D, ACT>;
     using TB = LatTab<N, S::DA>;
     constexpr int DA = S::DA, NB = TB::NB, MF = TB::MF;
@@ -258,20 +264,36 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     const LatGeom &g = P.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qx = warp % g.Wx, wy = warp / g.Wx;
-    const int skew = (XA ? qx : 0) + (PIPE ? wy : 0);
-    const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? g.Wy - 1 : 0);
+    const int crank = (CS > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    const int skew = (XA ? qx : 0) + (PIPE ? crank * g.Wy + wy : 0);
+    const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? CS * g.Wy - 1 : 0);
+    auto step_sync = [&]() {
+        if constexpr (CS > 1) cg::this_cluster().sync();
+        else __syncthreads();
+    };
 
     for (;;) {
-        if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
-        __syncthreads();
-        const int task = s_task;
-        __syncthreads();
-        if (task >= g.ntasks) return;
-        // ticket order (gy, velocity, gx): every velocity's pipeline advances together, and the
-        // tasks a task waits on (gx - 1: ticket - 1; gy - 1: ticket - nvel ngx) come earlier
+        int ctask;
+        if constexpr (CS > 1) {
+            if (crank == 0 && threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
+            cg::this_cluster().sync();
+            ctask = *cg::this_cluster().map_shared_rank(&s_task, 0);
+            cg::this_cluster().sync();
+        } else {
+            if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
+            __syncthreads();
+            ctask = s_task;
+            __syncthreads();
+        }
+        if (ctask >= g.ntasks_c) return;
+        // ticket order (pipe group, velocity, gx): every velocity's pipeline advances together, and
+        // the tasks a task waits on (gx - 1: ticket - 1; previous pipe group: ticket - nvel ngx)
+        // come earlier.  A cluster task covers CS consecutive pipe groups (one per CTA).
         const int per_gy = g.nvel * g.ngx;
-        const int gy = task / per_gy, rem = task - gy * per_gy;
+        const int gyc = ctask / per_gy, rem = ctask - gyc * per_gy;
         const int vi = rem / g.ngx, gx = rem - vi * g.ngx;
+        const int gy = gyc * CS + crank;
+        const int task = (gy * g.nvel + vi) * g.ngx + gx;  // CTA-level task: progress and traces
         const LatVel &V = P.v[vi];
         const int ux = (gx * g.Wx + qx) * 32 + lane;  // x cell (XA) or x node
         const int uw = gy * g.Wy + wy;                // pipe cell, batch node or 0
@@ -354,6 +376,12 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         if (wy > 0) {
 #pragma unroll
                             for (int j = 0; j < MF; ++j) sy[j] = YS(ps, (t - 1) & 1, warp - g.Wx, lane)[j];
+                        } else if (CS > 1 && crank > 0) {
+                            // the previous CTA of the cluster: its last pipe warp, through DSMEM
+                            const double *rsy = cg::this_cluster().map_shared_rank(
+                                YS(ps, (t - 1) & 1, (g.Wy - 1) * g.Wx + qx, lane), crank - 1);
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) sy[j] = rsy[j];
                         } else if (gy > 0) {
                             if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
                             const double *ysrc =
@@ -553,7 +581,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         }
 #pragma unroll
                         for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
-                        if (wy == g.Wy - 1 && gy < g.ngy - 1) {
+                        if (wy == g.Wy - 1 && crank == CS - 1 && gy < g.ngy - 1) {
                             double *dst =
                                 P.ybuf + (((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MF;
 #pragma unroll
@@ -574,7 +602,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     }
                 }
             }
-            __syncthreads();
+            step_sync();
             if (threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
         }
         cp_async_wait<0>();
