@@ -9,8 +9,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdg.so")
 SOURCES = [os.path.join(SRC, "pdg_api.cu")]
-DEPS = SOURCES + [os.path.join(SRC, f) for f in ("pdg_kernels.cuh", "pdg_tables.hpp", "pdg_comm.hpp")] + \
-    [os.path.join(os.path.dirname(HERE), "include", "pdg.h")]
+# every file under csrc/ (kernels, tables, NCCL plumbing) and the public header
+DEPS = sorted(set(SOURCES + [os.path.join(SRC, f) for f in os.listdir(SRC)
+                             if f.endswith((".cu", ".cuh", ".hpp", ".h"))] +
+                  [os.path.join(os.path.dirname(HERE), "include", "pdg.h")]))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

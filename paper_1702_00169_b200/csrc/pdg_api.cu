@@ -133,7 +133,8 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     for (int t = 1; t < P.d; ++t) mf *= g.n;
     // boundary traces of up to two sweeps per launch
     P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wy * mf : 0;
-    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * mf : 0;
+    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * ((mf + 1) & ~1) : 0;  // even stride
+    P.xbuf = (P.xbuf + 1) & ~(size_t)1;  // keep every slice 16-byte aligned
 }
 
 // Active-axis mask of a lattice velocity (bit k set if v_k != 0).
@@ -576,6 +577,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.g.nc = pl.nc;
     P.g.ntasks = pl.ntasks;
     P.g.ntasks_c = pl.ntasks_c;
+    P.g.ypf = std::getenv("PDG_LATTICE_NOYPF") ? 0 : 1;
     P.g.nvel = pl.nvel;
     for (int q = 0; q < pl.nvel; ++q) {
         const int j = pl.vel[q];
@@ -598,7 +600,8 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
     const size_t smem =
         sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
-                          pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32));
+                          pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32) +
+                          (PIPE ? (size_t)NPASS * pl.Wx * 32 * ((TB::MF + 1) & ~1) : 0));
     // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy
     auto kern = pdg::lattice_sweep_kernel<D, N, ACT, NPASS, CS>;
     const void *kfn = reinterpret_cast<const void *>(kern);

@@ -92,6 +92,8 @@ struct LatGeom {
     int32_t ntasks;      // CTA-level tasks (pipe groups padded to a multiple of the cluster size)
     int32_t nvel;
     int32_t ntasks_c;    // cluster-level tasks (== ntasks without clusters)
+    int32_t ypf;         // 1: prefetch the previous CTA's y traces one row ahead
+    int32_t pad2;
 };
 
 template <int D, int N, int ACT>
@@ -102,7 +104,8 @@ struct LatParams {
     int *ticket;     // [0]; progress counters follow: progress[task] = rows published
     int *progress;
     double *xbuf;    // [task][row][Wy][MF]       x out-traces at CTA boundaries
-    double *ybuf;    // [task][row][Wx][32][MF]   y out-traces at CTA boundaries
+    double *ybuf;    // [task][row][pass][Wx][32][MFP] y out-traces at CTA boundaries (MFP = MF rounded up to
+                     // an even count: 16-byte cp.async.cg copies)
     LatGeom g;
     LatVel v[kLatMaxVel];
     LatTab<N, S::DA> tab;
@@ -155,6 +158,11 @@ __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc)
 {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(double *sdst, const double *gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int K>
@@ -225,6 +233,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     using MMA = LatMma<D, N, ACT>;
     constexpr bool USE_MMA = MMA::USE;
     constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
+    constexpr int MFP = (MF + 1) & ~1;  // per-lane stride of the global y traces (16-byte multiple)
     static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     const unsigned FULL = 0xffffffffu;
 
@@ -243,6 +252,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     double *stg_base = ysb + (PIPE ? (size_t)NPASS * 2 * nwarps * 32 * MF : 0);
     double *sA = stg_base + (USE_MMA ? (size_t)nwarps * NB * 32 : 0);
     double *sAx = sA + (size_t)MT * 8 * KS * 4;
+    // (pipe classes) y traces of the previous CTA prefetched for the next row: [pass][Wx][32][MFP]
+    double *spy = USE_MMA ? sAx + (size_t)MT * 8 * KSX * 4 : stg_base;
     if constexpr (USE_MMA) {
         for (int i = threadIdx.x; i < MT * 8 * KS * 4; i += blockDim.x) {
             const int q = i / (KS * 4), k = i % (KS * 4);
@@ -338,6 +349,10 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         }
 
         double *wbuf = sfo + (size_t)warp * 2 * NB * 32;
+        // y traces of the previous CTA for row rr, if already published (speculative: the
+        // producer normally runs ahead, so the global hand-over leaves the critical path)
+        const bool ycons = PIPE && g.ypf && wy == 0 && gy > 0 && (CS == 1 || crank == 0);
+        bool ypf = false;  // this lane's y traces for the current row sit in spy
         // issue the copies of row rr into buffer rr & 1 (one commit group per row)
         auto prefetch = [&](int rr) {
             if (valid && rr < g.nc) {
@@ -351,6 +366,20 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     cp_async8(dst + q * 32, P.f + ubr + off);
                 }
             }
+            if constexpr (PIPE) {
+                ypf = false;
+                if (ycons && rr < g.nc && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
+#pragma unroll
+                    for (int ps = 0; ps < NPASS; ++ps) {
+                        const double *ysrc =
+                            P.ybuf + (((((int64_t)(task - per_gy) * g.nc + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                        double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * MFP;
+#pragma unroll
+                        for (int h = 0; h < MFP; h += 2) cp_async16_cg(yd + h, ysrc + h);
+                    }
+                    ypf = true;
+                }
+            }
             cp_async_commit();
         };
 
@@ -360,8 +389,18 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 ucell[CA] = r;
                 const int64_t ub = ibase + cbase + (int64_t)r * cstep;
                 if (r == 0) prefetch(0);
-                prefetch(r + 1);
-                cp_async_wait<1>();  // row r has landed (row r+1 may still be in flight)
+                cp_async_wait<0>();  // row r (and its prefetched y traces) have landed
+                double sy_pf[(PIPE ? NPASS : 1)][PIPE ? MF : 1];
+                const bool have_sy = ypf;
+                if constexpr (PIPE) {
+                    if (have_sy) {
+#pragma unroll
+                        for (int ps = 0; ps < NPASS; ++ps)
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) sy_pf[ps][j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
+                    }
+                }
+                prefetch(r + 1);  // overlaps the rest of the row
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
                 const double *src = wbuf + (r & 1) * NB * 32 + lane;
                 double fprev[NB];  // input of the second sweep (output of the first)
@@ -383,11 +422,16 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int j = 0; j < MF; ++j) sy[j] = rsy[j];
                         } else if (gy > 0) {
-                            if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
-                            const double *ysrc =
-                                P.ybuf + (((((int64_t)(task - per_gy) * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MF;
+                            if (have_sy) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
+                                for (int j = 0; j < MF; ++j) sy[j] = sy_pf[ps][j];
+                            } else {
+                                if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
+                                const double *ysrc =
+                                    P.ybuf + (((((int64_t)(task - per_gy) * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+#pragma unroll
+                                for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
+                            }
                         } else {
 #pragma unroll
                             for (int j = 0; j < MF; ++j) sy[j] = 0.0;
@@ -583,7 +627,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
                         if (wy == g.Wy - 1 && crank == CS - 1 && gy < g.ngy - 1) {
                             double *dst =
-                                P.ybuf + (((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MF;
+                                P.ybuf + (((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                             for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
                             __threadfence();
