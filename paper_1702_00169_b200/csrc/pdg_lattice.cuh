@@ -757,7 +757,7 @@ __device__ __forceinline__ void lbm_local_ops(double (&fv)[NV], double (&w)[D + 
 }
 
 template <int D, int NV>
-__global__ void __launch_bounds__(256) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
+__global__ void __launch_bounds__(256, 2) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
                                                         const __grid_constant__ LbmParams L, const LocalOps op)
 {
     // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
@@ -812,28 +812,37 @@ __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *
     }
 }
 
-// Collision of the local velocities from reduced moments w (sharded path).
+// Collision of the local velocities from reduced moments w (sharded path): w comes from memory,
+// so every local velocity is loaded, updated and stored in turn (no per-node f array).
 template <int D, int NV>
-__global__ void __launch_bounds__(256) relax_from_w_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
-                                                               int64_t nnodes, int v0, int nvl,
-                                                               const __grid_constant__ LbmParams L, const LocalOps op)
+__global__ void __launch_bounds__(256, 2) relax_from_w_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
+                                                                  int64_t nnodes, int v0, int nvl,
+                                                                  const __grid_constant__ LbmParams L, const LocalOps op)
 {
-    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
-    // instead of being hoisted into registers)
-    {
-        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (x >= nnodes) return;
-        double wl[D + 1];
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nnodes) return;
+    double wl[D + 1];
 #pragma unroll
-        for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
-        double fv[NV];
+    for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);
+    // S2(hs1) C2 S2(hs2) composed (lbm_local_ops): f <- ca f + (ca hs1 + hs2) g + cb f^eq(w')
+    double gs[D];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) fv[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
-        lbm_local_ops<D, NV>(fv, wl, L, op);
-#pragma unroll
-        for (int i = 0; i < NV; ++i)
-            if (i >= v0 && i < v0 + nvl) __stcs(f + (int64_t)(i - v0) * nnodes + x, fv[i]);
+    for (int d = 0; d < D; ++d) {
+        gs[d] = wl[0] * L.G[d] * L.inv_c2;
+        wl[1 + d] = fma(op.hs1 * wl[0], L.G[d], wl[1 + d]);
     }
+    const double hg = fma(op.ca, op.hs1, op.hs2);
+    const LbmNode<D> nd(wl, L);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+        if (i >= v0 && i < v0 + nvl) {
+            double *p = f + (int64_t)(i - v0) * nnodes + x;
+            double vg = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+            const double fs = fma(hg * L.wgt[i], vg, op.ca * __ldcs(p));
+            __stcs(p, (op.cb != 0.0) ? fma(op.cb, nd.feq(i, L), fs) : fs);
+        }
 }
 
 // f_i = f^eq_i(w) for the local velocities.
