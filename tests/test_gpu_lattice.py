@@ -366,3 +366,26 @@ def test_lattice_anisotropic_transport_and_steps(lat, ncell, p, hi, warps):
     ref2 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 2)
     S.destroy()
     assert rel_maxnorm(got2, ref2) <= TOL_STEP
+
+
+def test_lattice_check_state_counts_nonpositive_density():
+    """pdg_check_state for a lattice set: rho = sum of all n_v populations (P = [1; v^T])."""
+    from paper_1702_00169_b200 import pdg
+    cfg = lbm_config("D2Q9", 4)
+    w0 = w0_grid(cfg)
+    S = make_solver(cfg)
+    S.set_equilibrium(w0.reshape(-1).cuda())
+    assert S.check_state() == 0
+    state = S.get_state()
+    f = state.view((cfg.nv,) + cfg.grid_shape)
+    f[:, 2, 3] = -0.1          # one node with rho < 0
+    f[4, 5, 6] = float("nan")  # one node with a non-finite population
+    S.set_state(state)
+    assert S.check_state() == 2
+    S.destroy()
+    cfgc = lbm_config("D2Q9", 4)
+    pb = pdg.problem_from_config(cfgc, flags=pdg.PDG_CHECK_STATE)
+    S2 = pdg.Solver(pb)
+    S2.set_equilibrium(w0.reshape(-1).cuda())
+    S2.step(1)  # healthy: no error
+    S2.destroy()
