@@ -49,8 +49,9 @@ def sharded_solver(cfg, device, flags=0, stream=None, tau=0.0, scheme=pdg.PDG_SC
     """A libpdg context for this rank's share (velocity block or z-slab), with its NCCL communicator."""
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
-    # under a process group the collision always takes the communicator path (also for 1 rank)
-    nccl_id = bootstrap_nccl_id(device=device) if dist.is_initialized() else None
+    # a communicator only with several ranks: one rank keeps the fused single-GPU path
+    # (collision fused with the x sweeps, no partial-moment round trip through HBM)
+    nccl_id = bootstrap_nccl_id(device=device) if dist.is_initialized() and world > 1 else None
     pb = pdg.problem_from_config(cfg, tau=tau, scheme=scheme, rank=rank, nranks=world, nccl_id=nccl_id,
                                  flags=flags, stream=stream, decomposition=decomposition,
                                  slabs_per_rank=slabs_per_rank)
