@@ -599,7 +599,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
     const size_t smem =
-        sizeof(double) * ((size_t)(threads / 32) * (2 * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
+        sizeof(double) * ((size_t)(threads / 32) * (pdg::LatRing<D>::RING * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32) +
                           (PIPE ? (size_t)NPASS * pl.Wx * 32 * ((TB::MF + 1) & ~1) : 0));
     // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy

@@ -133,6 +133,12 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b)
         : "d"(a), "d"(b));
 }
 
+template <int D>
+struct LatRing {
+    static constexpr int PFA = (D == 2) ? 3 : 1;  // rows prefetched ahead
+    static constexpr int RING = PFA + 1;          // row buffers per warp
+};
+
 // Tensor-core path of the lattice sweep: used for the body diagonals (3 active axes), whose
 // n^3 x n^3 block makes the unit update fp64-bound.
 template <int D, int N, int ACT>
@@ -234,6 +240,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     constexpr bool USE_MMA = MMA::USE;
     constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
     constexpr int MFP = (MF + 1) & ~1;  // per-lane stride of the global y traces (16-byte multiple)
+    // rows prefetched ahead with cp.async: 2-D diagonals are latency-bound (short rows, one warp
+    // per SM sub-partition), so they look three rows ahead; 3-D classes one row
+    constexpr int PFA = LatRing<D>::PFA, RING = LatRing<D>::RING;
     static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     const unsigned FULL = 0xffffffffu;
 
@@ -242,9 +251,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
     // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
     // math), then the y hand-over buffers [pass][2][warps][32][MF] (PIPE)
-    extern __shared__ double sfo[];  // [warp][2][NB][32]
+    extern __shared__ double sfo[];  // [warp][RING][NB][32]
     const int nwarps = blockDim.x >> 5;
-    double *ysb = sfo + (size_t)nwarps * 2 * NB * 32;
+    double *ysb = sfo + (size_t)nwarps * RING * NB * 32;
     auto YS = [&](int ps, int buf, int w, int l) -> double * {
         return ysb + ((((size_t)ps * 2 + buf) * nwarps + w) * 32 + l) * MF;
     };
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 for (int j = 0; j < MF; ++j) sc[ps][j] = s0c[j];
         }
 
-        double *wbuf = sfo + (size_t)warp * 2 * NB * 32;
+        double *wbuf = sfo + (size_t)warp * RING * NB * 32;
         // y traces of the previous CTA for row rr, if already published (speculative: the
         // producer normally runs ahead, so the global hand-over leaves the critical path)
         const bool ycons = PIPE && g.ypf && wy == 0 && gy > 0 && (CS == 1 || crank == 0);
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         auto prefetch = [&](int rr) {
             if (valid && rr < g.nc) {
                 const int64_t ubr = ibase + cbase + (int64_t)rr * cstep;
-                double *dst = wbuf + (rr & 1) * NB * 32 + lane;
+                double *dst = wbuf + (rr % RING) * NB * 32 + lane;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) {
                     int64_t off = 0;
@@ -388,21 +397,26 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             if (r >= 0 && r < g.nc && wvalid) {
                 ucell[CA] = r;
                 const int64_t ub = ibase + cbase + (int64_t)r * cstep;
-                if (r == 0) prefetch(0);
-                cp_async_wait<0>();  // row r (and its prefetched y traces) have landed
+                if (r == 0)
+                    for (int k = 0; k < PFA; ++k) prefetch(k);
                 double sy_pf[(PIPE ? NPASS : 1)][PIPE ? MF : 1];
-                const bool have_sy = ypf;
-                if constexpr (PIPE) {
+                bool have_sy = false;
+                if constexpr (PIPE) {  // PFA == 1: the y-trace slot is read before the next prefetch
+                    cp_async_wait<0>();  // row r (and its prefetched y traces) have landed
+                    have_sy = ypf;
                     if (have_sy) {
 #pragma unroll
                         for (int ps = 0; ps < NPASS; ++ps)
 #pragma unroll
                             for (int j = 0; j < MF; ++j) sy_pf[ps][j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
                     }
+                    prefetch(r + 1);  // overlaps the rest of the row
+                } else {
+                    prefetch(r + PFA);
+                    cp_async_wait<PFA>();  // row r has landed, rows r+1 .. r+PFA may be in flight
                 }
-                prefetch(r + 1);  // overlaps the rest of the row
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
-                const double *src = wbuf + (r & 1) * NB * 32 + lane;
+                const double *src = wbuf + (r % RING) * NB * 32 + lane;
                 double fprev[NB];  // input of the second sweep (output of the first)
                 double fn[NB];
 #pragma unroll
@@ -500,7 +514,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         //   F  = F0 + Q_x S_x_in                                     after the x scan
                         // B operands come from shared memory: F_old from the cp.async row buffer, the
                         // in-traces from the warp's staging rows; A operands from the CTA's tables.
-                        const double *fsrc = wbuf + (r & 1) * NB * 32;
+                        const double *fsrc = wbuf + (r % RING) * NB * 32;
                         double *stg = stg_base + (size_t)warp * NB * 32;
 #pragma unroll
                         for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sc[ps][j];
