@@ -5,6 +5,7 @@
 // caller's stream.  No device allocation, no host fallback: every arithmetic step of
 // the hot path runs in these kernels.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: one range per operator pass (nsys / ncu --nvtx)
 
 #include <cmath>
 #include <cstdio>
@@ -36,6 +37,14 @@ pdg_status fail(pdg_status s, const std::string &msg)
     g_last_error = msg;
     return s;
 }
+
+// NVTX range for the duration of a scope (no-op without a profiler attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 #define PDG_CUDA_TRY(expr)                                                                             \
     do {                                                                                               \
@@ -113,6 +122,10 @@ void plan_lattice(const Geometry &g, LatPlan &P)
             P.Wy = std::min(wy, P.nw);
         }
     }
+    if (P.d == 3 && g.n == 4) {  // p = 3 body diagonals: ~90 KB of shared memory per warp
+        P.Wx = std::min(P.Wx, 2);
+        P.Wy = std::max(1, std::min(P.Wy, 2 / P.Wx));
+    }
     P.ngx = (P.nlane + 32 * P.Wx - 1) / (32 * P.Wx);
     P.ngy = (P.nw + P.Wy - 1) / P.Wy;
     // pipe classes may use clusters of CTAs along the pipe axis (y traces through DSMEM, one
@@ -175,6 +188,8 @@ void lattice_classes(const Geometry &g, const double *vel, std::vector<LatPlan> 
 }
 
 constexpr int kMaxTables = 16;
+constexpr int kMaxLatTables = 16;  // distinct (class, dt') of the large (p = 3 body-diagonal) block tables
+constexpr size_t kLatBigTableDoubles = sizeof(pdg::LatTab<4, 3>) / sizeof(double);
 
 pdg_status validate(const pdg_problem *p, Geometry *g)
 {
@@ -262,8 +277,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
                 const bool ok = (d < p->dim) ? (v == 0.0 || v == p->lambda || v == -p->lambda) : (v == 0.0);
                 if (!ok) return fail(PDG_E_VELOCITY_SET, "lattice velocity components must be 0 or +-lambda");
             }
-            if (popcount3(act_mask(p->vel + 3 * i, p->dim)) == 3 && p->degree == 3)
-                return fail(PDG_E_UNSUPPORTED, "p = 3 with body-diagonal velocities (64x64 block) is not compiled");
+
         }
         if (p->decomposition == PDG_DECOMP_ZSLAB && p->nranks * std::max(1, p->slabs_per_rank) > 1)
             return fail(PDG_E_UNSUPPORTED, "the z-slab decomposition is implemented for axis-aligned sets only");
@@ -346,6 +360,7 @@ size_t work_bytes_of(const Geometry &g)
     size_t b = 256;
     if (g.zslab) b += sizeof(double) * (2 * g.carry_doubles + kMaxTables * g.table_doubles);
     if (g.lattice) b += lat_ints_bytes(g) + sizeof(double) * (g.lat_xbuf + g.lat_ybuf);
+    if (g.lattice && g.n == 4 && g.dim == 3) b += sizeof(double) * kMaxLatTables * kLatBigTableDoubles;
     return b;
 }
 
@@ -416,6 +431,9 @@ struct pdg_ctx {
     std::vector<cudaEvent_t> lat_join;
     std::map<std::pair<int, double>, pdg::LatticeBlockLD> lat_blocks;  // (act, dt') -> block
     std::map<std::tuple<const void *, int, size_t>, int> launch_cache;  // (kernel, threads, smem) -> CTAs/SM
+    std::map<std::pair<int, double>, double *> lat_gtab;  // (act, dt') -> device copy of a large block table
+    double *lat_gtab_base = nullptr;                      // slots in the work buffer
+    int lat_gtab_used = 0;
 };
 
 namespace {
@@ -548,7 +566,7 @@ const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
 }
 
 template <int D, int N, int ACT, int NPASS, int CS>
-pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
+pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, double dtp, cudaStream_t st)
 {
     using PP = pdg::LatParams<D, N, ACT>;
     using TB = pdg::LatTab<N, pdg::LatShape<D, ACT>::DA>;
@@ -587,14 +605,39 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
         for (int k = 0; k < 3; ++k) P.v[q].sign[k] = (v[k] < 0.0) ? -1 : 1;
     }
     constexpr int NB = TB::NB, MF = TB::MF;
-    for (int q = 0; q < NB; ++q)  // column-major (pdg_lattice.cuh LatTab)
-        for (int c = 0; c < NB; ++c) P.tab.M[c * NB + q] = (double)B.M[(size_t)q * NB + c];
+    // tables in LatTab layout (column-major blocks): into the parameter space, or (too large for it)
+    // into a device slot of the work buffer, uploaded once per (class, dt')
+    std::vector<double> host(sizeof(TB) / sizeof(double), 0.0);
+    TB &T = *reinterpret_cast<TB *>(host.data());
+    for (int q = 0; q < NB; ++q)
+        for (int cc = 0; cc < NB; ++cc) T.M[cc * NB + q] = (double)B.M[(size_t)q * NB + cc];
     for (int t = 0; t < DA; ++t)
         for (int q = 0; q < NB; ++q)
-            for (int j = 0; j < MF; ++j) P.tab.Q[t][j * NB + q] = (double)B.Q[((size_t)t * NB + q) * MF + j];
+            for (int j = 0; j < MF; ++j) T.Q[t][j * NB + q] = (double)B.Q[((size_t)t * NB + q) * MF + j];
     for (int s = 0; s < 5; ++s)
         for (int i = 0; i < MF; ++i)
-            for (int j = 0; j < MF; ++j) P.tab.Bp[s][j * MF + i] = (double)B.Bpow[((size_t)s * MF + i) * MF + j];
+            for (int j = 0; j < MF; ++j) T.Bp[s][j * MF + i] = (double)B.Bpow[((size_t)s * MF + i) * MF + j];
+    if constexpr (pdg::LatTabSel<N, DA>::BIG) {
+        // uploaded at pdg_create for the scheme's steps (graph capture safe); other dt' on first use
+        const auto key = std::make_pair(pl.act, dtp);
+        auto it = c->lat_gtab.find(key);
+        double *dev = nullptr;
+        if (it != c->lat_gtab.end()) dev = it->second;
+        else {
+            if (c->lat_gtab_used >= kMaxLatTables) return fail(PDG_E_UNSUPPORTED, "too many distinct lattice steps");
+            dev = c->lat_gtab_base + (size_t)c->lat_gtab_used * kLatBigTableDoubles;
+            ++c->lat_gtab_used;
+            PDG_CUDA_TRY(cudaMemcpy(dev, host.data(), sizeof(TB), cudaMemcpyHostToDevice));
+            c->lat_gtab[key] = dev;
+        }
+        if (!st) return PDG_OK;  // table preparation only (pdg_create)
+        const TB *D_ = reinterpret_cast<const TB *>(dev);
+        P.tab.M = D_->M;
+        for (int t = 0; t < 3; ++t) P.tab.Q[t] = (t < DA) ? D_->Q[t] : nullptr;
+        for (int s = 0; s < 5; ++s) P.tab.Bp[s] = D_->Bp[s];
+    } else {
+        P.tab = T;
+    }
     const int threads = 32 * pl.Wx * pl.Wy;
     constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
@@ -644,14 +687,14 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
 
 // cluster size dispatch (pipe classes only: 3-D with y and z active)
 template <int D, int N, int ACT, int NPASS>
-pdg_status launch_lattice_cs(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, cudaStream_t st)
+pdg_status launch_lattice_cs(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, double dtp, cudaStream_t st)
 {
     if constexpr (pdg::LatShape<D, ACT>::PIPE) {
-        if (pl.cs == 2) return launch_lattice_t<D, N, ACT, NPASS, 2>(c, pl, B, st);
-        if (pl.cs == 4) return launch_lattice_t<D, N, ACT, NPASS, 4>(c, pl, B, st);
-        if (pl.cs == 8) return launch_lattice_t<D, N, ACT, NPASS, 8>(c, pl, B, st);
+        if (pl.cs == 2) return launch_lattice_t<D, N, ACT, NPASS, 2>(c, pl, B, dtp, st);
+        if (pl.cs == 4) return launch_lattice_t<D, N, ACT, NPASS, 4>(c, pl, B, dtp, st);
+        if (pl.cs == 8) return launch_lattice_t<D, N, ACT, NPASS, 8>(c, pl, B, dtp, st);
     }
-    return launch_lattice_t<D, N, ACT, NPASS, 1>(c, pl, B, st);
+    return launch_lattice_t<D, N, ACT, NPASS, 1>(c, pl, B, dtp, st);
 }
 
 // One pass over the velocities of class `pl` applying T2(dtp) npass times: the FMA-path classes
@@ -667,13 +710,13 @@ pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_
         const int e = prof_begin(c, st);
         pdg_status s = PDG_E_UNSUPPORTED;
 #define PDG_LAT(DD, NN, AA, NP) \
-    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_cs<DD, NN, AA, NP>(c, pl, *B, st)
+    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_cs<DD, NN, AA, NP>(c, pl, *B, dtp, st)
         if (false) {}
         PDG_LAT(2, 2, 3, 1); PDG_LAT(2, 3, 3, 1); PDG_LAT(2, 4, 3, 1);
         PDG_LAT(3, 2, 3, 1); PDG_LAT(3, 3, 3, 1); PDG_LAT(3, 4, 3, 1);
         PDG_LAT(3, 2, 5, 1); PDG_LAT(3, 3, 5, 1); PDG_LAT(3, 4, 5, 1);
         PDG_LAT(3, 2, 6, 1); PDG_LAT(3, 3, 6, 1); PDG_LAT(3, 4, 6, 1);
-        PDG_LAT(3, 2, 7, 1); PDG_LAT(3, 3, 7, 1);
+        PDG_LAT(3, 2, 7, 1); PDG_LAT(3, 3, 7, 1); PDG_LAT(3, 4, 7, 1);
         PDG_LAT(3, 2, 3, 2); PDG_LAT(3, 3, 3, 2); PDG_LAT(3, 4, 3, 2);
         PDG_LAT(3, 2, 5, 2); PDG_LAT(3, 3, 5, 2); PDG_LAT(3, 4, 5, 2);
         PDG_LAT(3, 2, 6, 2); PDG_LAT(3, 3, 6, 2); PDG_LAT(3, 4, 6, 2);
@@ -690,6 +733,7 @@ pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_
 // One pass over f applying T2(dtp) npass times (npass in {1, 2}) to the selected velocities.
 pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_ALL)
 {
+    NvtxRange nv(npass == 2 ? "pdg T2 x2 (fused half-steps)" : "pdg T2");
     // lattice classes: forked onto their own streams (joined below), so that their wavefront
     // ramps overlap with each other and with the axis-aligned sweeps on the context stream
     const bool lat = which != SWEEP_X && !c->lat_plans.empty();
@@ -954,6 +998,7 @@ pdg_status partial_and_reduce(pdg_ctx *c)
 // One pass of the local operators of a lattice set: S2(hs1), C2(dt) (if with_c), S2(hs2).
 pdg_status local_pass_lbm(pdg_ctx *c, double hs1, bool with_c, double dt, double hs2)
 {
+    NvtxRange nv(with_c ? ((hs1 != 0.0 || hs2 != 0.0) ? "pdg S2 C2 S2" : "pdg C2") : "pdg S2");
     pdg::LocalOps op;
     op.hs1 = hs1;
     op.hs2 = hs2;
@@ -972,6 +1017,7 @@ pdg_status local_pass_lbm(pdg_ctx *c, double hs1, bool with_c, double dt, double
 
 pdg_status collide(pdg_ctx *c, double dt)
 {
+    NvtxRange nv("pdg C2");
     if (c->g.lattice) return local_pass_lbm(c, 0.0, true, dt, 0.0);
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
@@ -988,6 +1034,7 @@ pdg_status collide(pdg_ctx *c, double dt)
 // C2(dt) followed by npass sweeps T2(dtp) of the x-velocities, in one pass over f.
 pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
 {
+    NvtxRange nv("pdg C2 + x-sweeps");
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
     pdg::DevBlock blk[3];
@@ -1271,6 +1318,7 @@ pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out
 // Exact inflows of every slab from the outgoing carries, then the correction of the local slabs.
 pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
 {
+    NvtxRange nv("pdg z-slab carries");
     const Geometry &g = c->g;
     const pdg_ctx::ZTable *zt = nullptr;
     pdg_status st = ztable(c, dtp, npass, &zt);
@@ -1401,6 +1449,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         c->lat_ints = reinterpret_cast<int *>(base);
         c->lat_xbuf = reinterpret_cast<double *>(base + lat_ints_bytes(c->g));
         c->lat_ybuf = c->lat_xbuf + c->g.lat_xbuf;
+        c->lat_gtab_base = c->lat_ybuf + c->g.lat_ybuf;
     }
     if (c->g.zslab) {
         c->zcarry = reinterpret_cast<double *>(static_cast<char *>(work_dev) + 256);
@@ -1425,6 +1474,24 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         if (!ok) {
             pdg_destroy(c);
             return fail(PDG_E_CUDA, "cannot create the lattice class streams");
+        }
+        // large block tables (p = 3 body diagonals) of the scheme's steps, uploaded now
+        if (c->g.n == 4 && c->g.dim == 3) {
+            std::vector<Op> ops;
+            append_scheme(ops, p->scheme, p->dt);
+            for (const LatPlan &pl : c->lat_plans) {
+                if (pl.act != 7) continue;
+                for (const Op &o : ops) {
+                    if (o.kind != 0) continue;
+                    const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, o.h);
+                    pdg_status ps = B ? launch_lattice_t<3, 4, 7, 1, 1>(c, pl, *B, o.h, nullptr)
+                                      : fail(PDG_E_INVALID_ARGUMENT, "singular lattice block");
+                    if (ps != PDG_OK) {
+                        pdg_destroy(c);
+                        return ps;
+                    }
+                }
+            }
         }
     }
     if (c->g.zslab) {  // tables of the scheme's sweeps (single and fused double passes)
@@ -1593,6 +1660,7 @@ pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
 
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
 {
+    NvtxRange nv("pdg_step");
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (nsteps == 0) return PDG_OK;

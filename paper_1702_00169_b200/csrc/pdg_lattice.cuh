@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace pdg {
 
@@ -72,6 +73,21 @@ struct LatTab {
     double Bp[5][MF * MF];  // Bx^(2^j), Bx = rows of Q[0] on the x-out face,     Bp[s][j * MF + i]
 };
 
+// Block tables too large for the 32 KB kernel parameter space (p = 3 body diagonals: 64 x 64
+// block): same layouts as LatTab, in device memory (read once per CTA into shared memory for
+// the tensor path; the scan's Bx powers through the L1/L2 broadcast path).
+struct LatTabRef {
+    const double *M;
+    const double *Q[3];
+    const double *Bp[5];
+};
+
+template <int N, int DA>
+struct LatTabSel {
+    static constexpr bool BIG = sizeof(LatTab<N, DA>) > 24 * 1024;
+    using type = typename std::conditional<BIG, LatTabRef, LatTab<N, DA>>::type;
+};
+
 struct LatVel {
     int64_t f_off;   // element offset of the velocity's node grid in f
     int64_t fb_off;  // element offset of its D inflow planes in fb
@@ -108,7 +124,7 @@ struct LatParams {
                      // an even count: 16-byte cp.async.cg copies)
     LatGeom g;
     LatVel v[kLatMaxVel];
-    LatTab<N, S::DA> tab;
+    typename LatTabSel<N, S::DA>::type tab;
 };
 
 __device__ __forceinline__ int ld_acquire(const int *p)

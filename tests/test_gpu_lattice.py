@@ -44,6 +44,7 @@ def cases():
         ("D3Q15", 5, 2), ("D3Q19", 5, 2), ("D3Q27", 5, 2),
         ("D3Q19", 4, 3), ("D3Q27", 3, 1), ("D3Q15", 33, 2),
         ("D3Q27", 1, 2), ("D2Q9", 1, 2), ("D3Q19", 2, 3),   # degenerate: one / two cells per axis
+        ("D3Q15", 3, 3), ("D3Q27", 2, 3),                   # p = 3 body diagonals (64 x 64 block)
     ]
 
 
@@ -106,7 +107,7 @@ def test_lbm_collision_parity(lat, tau_dt):
 
 @pytest.mark.parametrize("lat,N,p,scheme", [("D2Q9", 12, 2, "m2"), ("D2Q9", 34, 2, "m2kin"), ("D3Q15", 6, 2, "m2"),
                                             ("D3Q19", 6, 2, "m2"), ("D3Q27", 5, 2, "m2"), ("D3Q19", 4, 3, "m2"),
-                                            ("D3Q27", 5, 1, "m4")])
+                                            ("D3Q27", 5, 1, "m4"), ("D3Q15", 3, 3, "m2")])
 def test_lbm_scheme_parity(lat, N, p, scheme):
     """Free-running palindromic steps from f^eq(w0) with inflow f^eq(w0(x_b)) (readings C12/C13)."""
     from paper_1702_00169_b200 import pdg
@@ -141,14 +142,6 @@ def test_lattice_equilibrium_init_matches_oracle():
     S.destroy()
     assert rel_maxnorm(got, f0) <= TOL_OP
     assert rel_maxnorm(fb, ref_planes) <= TOL_OP
-
-
-def test_lattice_p3_body_diagonal_unsupported():
-    from paper_1702_00169_b200 import pdg
-    cfg = lbm_config("D3Q15", 3, p=3)
-    with pytest.raises(pdg.PdgError) as e:
-        pdg.query_sizes(pdg.problem_from_config(cfg))
-    assert e.value.status == pdg.PDG_E_UNSUPPORTED
 
 
 # --------------------------------------------------------------------------
