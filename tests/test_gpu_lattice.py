@@ -382,3 +382,22 @@ def test_lattice_check_state_counts_nonpositive_density():
     S2.set_equilibrium(w0.reshape(-1).cuda())
     S2.step(1)  # healthy: no error
     S2.destroy()
+
+
+def test_lattice_host_pointer_paths():
+    """pdg_set_equilibrium with HOST w and w_b (staged through w_dev), pdg_get_state and
+    pdg_moments into host memory, for a lattice set."""
+    cfg = lbm_config("D3Q19", 4)
+    w0 = w0_grid(cfg)
+    wb = 1.01 * w0
+    S = make_solver(cfg)
+    S.set_equilibrium(w0.reshape(-1).clone(), wb.reshape(-1).clone())   # host tensors
+    f = S.get_state(torch.empty(S.sizes.f_elems, dtype=torch.float64))  # host out
+    fb = S.fb.cpu().numpy().reshape(cfg.nv, cfg.dim, -1)
+    w = S.moments(torch.empty(S.sizes.w_elems, dtype=torch.float64))
+    S.destroy()
+    pb = oracle_problem(cfg)
+    f0, fbf = O.initial_data(pb, w0.numpy(), wb.numpy())
+    assert rel_maxnorm(f.numpy().reshape(f0.shape), f0) <= TOL_OP
+    assert rel_maxnorm(fb, lattice_planes(cfg, fbf, S.sizes.plane_stride)) <= TOL_OP
+    assert rel_maxnorm(w.numpy().reshape((cfg.m,) + cfg.grid_shape), O.moments(pb, f0)) <= TOL_OP
