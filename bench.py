@@ -16,7 +16,8 @@ The JSON line adds:
   cpu_baseline : the CPU oracle (oracle/, as it stands) timed on this host on a bounded
                  sample of the same workload (N=64 sub-box of config 5, same p, nu, model).
   e2e          : the same metric through the public C-ABI with HOST buffers: per step,
-                 pdg_set_equilibrium(host w0, pinned) + pdg_step(1) + pdg_moments(host w).
+                 pdg_set_equilibrium(host w0, pinned) + pdg_step(1) + pdg_moments(host w), with
+                 PDG_ASYNC_HOST so that uploads and downloads of consecutive steps overlap.
   clocks       : nvidia-smi samples taken during the timed region.
 --impl reference times the oracle (the base contract's reference arm for this tier).
 """
@@ -243,7 +244,8 @@ def run_product(args, cfg):
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
         decomp = {"velocity": pdg.PDG_DECOMP_VELOCITY, "zslab": pdg.PDG_DECOMP_ZSLAB}[args.decomp]
-        S = pdist.sharded_solver(cfg, device, flags=pdg.PDG_PROFILE, stream=stream.cuda_stream,
+        flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST)
+        S = pdist.sharded_solver(cfg, device, flags=flags, stream=stream.cuda_stream,
                                  decomposition=decomp, slabs_per_rank=args.slabs_per_rank)
         fill_w0(cfg, S.w, device, S.sizes)
         S.set_equilibrium(S.w)
@@ -318,7 +320,8 @@ def run_product(args, cfg):
             for _ in range(n_e2e):
                 S.set_equilibrium(w_host)       # H2D of the step's input (pinned host)
                 S.step(1)
-                S.moments(w_out)                # D2H of the step's result
+                S.moments(w_out)                # D2H of the step's result (library copy stream)
+            S.synchronize()                     # PDG_ASYNC_HOST: every copy of the loop has landed
             a1.record(stream)
             torch.cuda.synchronize(device)
             ems = a0.elapsed_time(a1)
@@ -327,7 +330,9 @@ def run_product(args, cfg):
             e2e = {"value": cfg.updates_per_step * n_e2e / (ems * 1e-3), "unit": UNIT,
                    "h2d_bytes_per_step": int(8 * S.sizes.w_elems), "d2h_bytes_per_step": int(8 * S.sizes.w_elems),
                    "steps": n_e2e, "ms_per_step": ems / n_e2e, "wall_s": wall,
-                   "call": "pdg_set_equilibrium(host w0) + pdg_step(1) + pdg_moments(host w) per step"}
+                   "call": "pdg_set_equilibrium(host w0) + pdg_step(1) + pdg_moments(host w) per step, "
+                           "PDG_ASYNC_HOST (upload of step k+1 overlaps the download of step k; timed to "
+                           "pdg_synchronize)"}
             S.profile_read()
             del w_host, w_out
 
@@ -357,7 +362,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=64)
     ap.add_argument("--ref-cells", type=int, default=32)

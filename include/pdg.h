@@ -129,6 +129,13 @@ typedef enum {
                                  "collapsed" scheme of P:1173-1177) */
 #define PDG_PROFILE     0x8u  /* bracket every kernel launch with CUDA events on the context stream (read with
                                  pdg_profile_read; not for use under CUDA-graph capture) */
+#define PDG_ASYNC_HOST  0x10u /* host-pointer calls (pdg_set_state, pdg_set_equilibrium without wb, pdg_get_state,
+                                 pdg_moments) return without synchronising: host buffers (pinned for true
+                                 asynchrony) must stay valid and unmodified until pdg_synchronize.  Uploads for
+                                 pdg_set_equilibrium are staged in an extra work region (pdg_sizes.work_bytes grows
+                                 by 8 m nnodes_local bytes) and pdg_moments' download runs on a library copy
+                                 stream, so the upload of step k+1's input overlaps the download of step k's
+                                 result (PCIe is full duplex) */
 
 /* kernel kinds reported by pdg_profile_read */
 typedef enum {
@@ -258,7 +265,8 @@ pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad);
  * M: n*n row-major, g: n, beta = g[n-1].  Host outputs.  For inspection/pins. */
 pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, double *g, double *beta);
 
-/* Block until all work enqueued by this context has finished; reports asynchronous faults. */
+/* Block until all work enqueued by this context has finished (including PDG_ASYNC_HOST copies);
+ * reports asynchronous faults. */
 pdg_status pdg_synchronize(pdg_ctx *c);
 
 /* Destroy the context (NULL-safe); destroys the NCCL communicator if any. Does not free caller buffers. */

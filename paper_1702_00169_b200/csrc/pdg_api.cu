@@ -74,6 +74,7 @@ struct Geometry {
     size_t carry_doubles = 0;                 // one carry/inflow buffer (doubles)
     size_t table_doubles = 0;                 // one correction table (doubles)
     // lattice velocity sets (PDG_FLUX_LBM, NEXT-2)
+    int async_host = 0;                       // PDG_ASYNC_HOST
     int lattice = 0;                          // 1: general velocities, fb = [nvl][dim][plane_stride]
     int nplanes = 1;                          // inflow planes per velocity in fb
     size_t lat_ints = 0;                      // ticket + progress counters (sum over classes)
@@ -213,6 +214,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     if (p->scheme == PDG_SCHEME_M2S && p->source == PDG_SOURCE_NONE)
         return fail(PDG_E_INVALID_ARGUMENT, "PDG_SCHEME_M2S needs a source");
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
+    g->async_host = (p->flags & PDG_ASYNC_HOST) ? 1 : 0;
     g->dim = p->dim;
     g->p = p->degree;
     g->n = p->degree + 1;
@@ -361,7 +363,17 @@ size_t work_bytes_of(const Geometry &g)
     if (g.zslab) b += sizeof(double) * (2 * g.carry_doubles + kMaxTables * g.table_doubles);
     if (g.lattice) b += lat_ints_bytes(g) + sizeof(double) * (g.lat_xbuf + g.lat_ybuf);
     if (g.lattice && g.n == 4 && g.dim == 3) b += sizeof(double) * kMaxLatTables * kLatBigTableDoubles;
+    b = ((b + 255) / 256) * 256;
+    if (g.async_host) b += sizeof(double) * (size_t)g.m * (size_t)g.nnodes;  // PDG_ASYNC_HOST upload staging
     return b;
+}
+
+// byte offset of the PDG_ASYNC_HOST staging region in the work buffer
+size_t w_stage_offset(const Geometry &g)
+{
+    Geometry h = g;
+    h.async_host = 0;
+    return ((work_bytes_of(h) + 255) / 256) * 256;
 }
 
 void fill_sizes(const Geometry &g, pdg_sizes *out)
@@ -404,6 +416,10 @@ struct pdg_ctx {
     unsigned long long *counter = nullptr;
     cudaStream_t stream = nullptr;
     bool state_set = false;
+    // PDG_ASYNC_HOST
+    double *w_stage = nullptr;             // upload staging of pdg_set_equilibrium
+    cudaStream_t copy_stream = nullptr;    // downloads of pdg_moments
+    cudaEvent_t w_ready = nullptr, d2h_done = nullptr;
     pdg::ModelParams mp{};
     pdg::SweepParams x_params{};        // velocities along x
     pdg::SweepParams yz_params{};       // velocities along y / z
@@ -977,8 +993,15 @@ bool sharded(const pdg_ctx *c)
     return c->prob.decomposition == PDG_DECOMP_VELOCITY && (c->prob.nranks > 1 || c->comm.comm != nullptr);
 }
 
+// PDG_ASYNC_HOST: w_dev may still be read by the download of the previous pdg_moments
+void wait_w_download(pdg_ctx *c)
+{
+    if (c->copy_stream) cudaStreamWaitEvent(c->stream, c->d2h_done, 0);
+}
+
 pdg_status partial_and_reduce(pdg_ctx *c)
 {
+    wait_w_download(c);
     if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
     else PDG_DISPATCH(launch_partial_t, c);
     pdg_status s = post_launch(c, "partial_moments");
@@ -1508,6 +1531,17 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
                     }
                 }
     }
+    if (c->g.async_host) {
+        c->w_stage = reinterpret_cast<double *>(static_cast<char *>(work_dev) + w_stage_offset(c->g));
+        int prio = 0;
+        cudaStreamGetPriority(c->stream, &prio);
+        if (cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->w_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming) != cudaSuccess) {
+            pdg_destroy(c);
+            return fail(PDG_E_CUDA, "cannot create the PDG_ASYNC_HOST copy stream");
+        }
+    }
     if (p->flags & PDG_PROFILE) {
         c->prof.on = true;
         c->prof.ev.resize(2 * 4096);
@@ -1543,7 +1577,8 @@ pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_d
     if (fb)
         PDG_CUDA_TRY(cudaMemcpyAsync(c->fb, fb, sizeof(double) * c->g.nvl * c->g.nplanes * c->g.plane_stride, kind,
                                      c->stream));
-    if (!on_device || (c->prob.flags & PDG_SYNC_ERRORS)) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const bool sync = (!on_device && !c->g.async_host) || (c->prob.flags & PDG_SYNC_ERRORS);
+    if (sync) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->state_set = true;
     return PDG_OK;
 }
@@ -1553,6 +1588,17 @@ pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, in
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!w) return fail(PDG_E_INVALID_ARGUMENT, "w is NULL");
     const size_t wbytes = sizeof(double) * c->g.m * c->g.nnodes;
+    if (!on_device && c->g.async_host && !wb) {
+        // PDG_ASYNC_HOST: upload into the staging region (w_dev stays free for a pending download)
+        PDG_CUDA_TRY(cudaMemcpyAsync(c->w_stage, w, wbytes, cudaMemcpyHostToDevice, c->stream));
+        if (c->g.lattice) PDG_LBM_DISPATCH(launch_equilibrium_lbm_t, c, c->w_stage, c->w_stage, false);
+        else PDG_DISPATCH(launch_equilibrium_t, c, c->w_stage, c->w_stage);
+        pdg_status s = post_launch(c, "equilibrium(async)");
+        if (s != PDG_OK) return s;
+        c->state_set = true;
+        return PDG_OK;
+    }
+    if (!on_device) wait_w_download(c);  // the host paths stage through w_dev
     if (c->g.lattice) {
         if (!on_device) {
             PDG_CUDA_TRY(cudaMemcpyAsync(c->w, wb ? wb : w, wbytes, cudaMemcpyHostToDevice, c->stream));
@@ -1608,7 +1654,7 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device)
     if (!c || !f) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     PDG_CUDA_TRY(cudaMemcpyAsync(f, c->f, sizeof(double) * c->g.nvl * c->g.nnodes,
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
-    if (!on_device) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (!on_device && !c->g.async_host) PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return PDG_OK;
 }
 
@@ -1684,6 +1730,14 @@ pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device)
     pdg_status s = partial_and_reduce(c);
     if (s != PDG_OK) return s;
     const size_t bytes = sizeof(double) * c->g.m * c->g.nnodes;
+    if (!on_device && c->g.async_host) {
+        // download on the copy stream: the context stream goes on (next upload, next step)
+        PDG_CUDA_TRY(cudaEventRecord(c->w_ready, c->stream));
+        PDG_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->w_ready, 0));
+        PDG_CUDA_TRY(cudaMemcpyAsync(w, c->w, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        PDG_CUDA_TRY(cudaEventRecord(c->d2h_done, c->copy_stream));
+        return PDG_OK;
+    }
     if (w != c->w)
         PDG_CUDA_TRY(cudaMemcpyAsync(w, c->w, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                      c->stream));
@@ -1726,12 +1780,19 @@ pdg_status pdg_synchronize(pdg_ctx *c)
 {
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->copy_stream) PDG_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
     return PDG_OK;
 }
 
 void pdg_destroy(pdg_ctx *c)
 {
     if (!c) return;
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    if (c->w_ready) cudaEventDestroy(c->w_ready);
+    if (c->d2h_done) cudaEventDestroy(c->d2h_done);
     c->comm.destroy();
     for (auto st : c->lat_streams)
         if (st) cudaStreamDestroy(st);

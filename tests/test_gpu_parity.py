@@ -461,3 +461,31 @@ def test_anisotropic_transport_and_steps(dim, ncell, p, flux, fparams, m, hi):
     ref3 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 3)
     S.destroy()
     assert rel_maxnorm(got3, ref3) < TOL_STEP
+
+
+def test_async_host_mode_equals_sync():
+    """PDG_ASYNC_HOST: host-pointer uploads staged in the extra work region, downloads on the
+    copy stream, no synchronisation until pdg_synchronize -- same results as the synchronous
+    calls, step by step (each step re-initialised from host w0, as in bench.py's e2e loop)."""
+    import torch
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import lbm_config
+    for cfg in (CONFIGS[3].resized(6).stabilised(), lbm_config("D3Q19", 5)):
+        w0 = w0_grid(cfg).reshape(-1)
+        outs = {}
+        for mode in ("sync", "async"):
+            flags = pdg.PDG_ASYNC_HOST if mode == "async" else 0
+            S = make_solver(cfg, flags=flags)
+            if mode == "async":
+                assert S.sizes.work_bytes >= 8 * cfg.m * cfg.nnodes
+            w_host = w0.clone().pin_memory()
+            res = [torch.empty(S.sizes.w_elems, dtype=torch.float64).pin_memory() for _ in range(3)]
+            for k in range(3):
+                S.set_equilibrium(w_host)
+                S.step(k + 1)
+                S.moments(res[k])
+            S.synchronize()
+            outs[mode] = [r.numpy().copy() for r in res]
+            S.destroy()
+        for a, b in zip(outs["sync"], outs["async"]):
+            assert np.array_equal(a, b)
