@@ -419,7 +419,9 @@ struct pdg_ctx {
     // PDG_ASYNC_HOST
     double *w_stage = nullptr;             // upload staging of pdg_set_equilibrium
     cudaStream_t copy_stream = nullptr;    // downloads of pdg_moments
+    cudaStream_t upload_stream = nullptr;  // uploads of pdg_set_equilibrium into w_stage
     cudaEvent_t w_ready = nullptr, d2h_done = nullptr;
+    cudaEvent_t stage_free = nullptr, stage_full = nullptr;
     pdg::ModelParams mp{};
     pdg::SweepParams x_params{};        // velocities along x
     pdg::SweepParams yz_params{};       // velocities along y / z
@@ -1536,8 +1538,11 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         int prio = 0;
         cudaStreamGetPriority(c->stream, &prio);
         if (cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&c->upload_stream, cudaStreamNonBlocking, prio) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->w_ready, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->stage_full, cudaEventDisableTiming) != cudaSuccess) {
             pdg_destroy(c);
             return fail(PDG_E_CUDA, "cannot create the PDG_ASYNC_HOST copy stream");
         }
@@ -1589,10 +1594,16 @@ pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, in
     if (!w) return fail(PDG_E_INVALID_ARGUMENT, "w is NULL");
     const size_t wbytes = sizeof(double) * c->g.m * c->g.nnodes;
     if (!on_device && c->g.async_host && !wb) {
-        // PDG_ASYNC_HOST: upload into the staging region (w_dev stays free for a pending download)
-        PDG_CUDA_TRY(cudaMemcpyAsync(c->w_stage, w, wbytes, cudaMemcpyHostToDevice, c->stream));
+        // PDG_ASYNC_HOST: upload into the staging region on the upload stream as soon as the previous
+        // equilibrium has consumed it (so it overlaps the previous step and its download; w_dev stays
+        // free for a pending download), then the equilibrium on the context stream
+        PDG_CUDA_TRY(cudaStreamWaitEvent(c->upload_stream, c->stage_free, 0));
+        PDG_CUDA_TRY(cudaMemcpyAsync(c->w_stage, w, wbytes, cudaMemcpyHostToDevice, c->upload_stream));
+        PDG_CUDA_TRY(cudaEventRecord(c->stage_full, c->upload_stream));
+        PDG_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->stage_full, 0));
         if (c->g.lattice) PDG_LBM_DISPATCH(launch_equilibrium_lbm_t, c, c->w_stage, c->w_stage, false);
         else PDG_DISPATCH(launch_equilibrium_t, c, c->w_stage, c->w_stage);
+        PDG_CUDA_TRY(cudaEventRecord(c->stage_free, c->stream));
         pdg_status s = post_launch(c, "equilibrium(async)");
         if (s != PDG_OK) return s;
         c->state_set = true;
@@ -1781,6 +1792,7 @@ pdg_status pdg_synchronize(pdg_ctx *c)
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->copy_stream) PDG_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+    if (c->upload_stream) PDG_CUDA_TRY(cudaStreamSynchronize(c->upload_stream));
     return PDG_OK;
 }
 
@@ -1791,8 +1803,12 @@ void pdg_destroy(pdg_ctx *c)
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
     }
-    if (c->w_ready) cudaEventDestroy(c->w_ready);
-    if (c->d2h_done) cudaEventDestroy(c->d2h_done);
+    if (c->upload_stream) {
+        cudaStreamSynchronize(c->upload_stream);
+        cudaStreamDestroy(c->upload_stream);
+    }
+    for (cudaEvent_t ev : {c->w_ready, c->d2h_done, c->stage_free, c->stage_full})
+        if (ev) cudaEventDestroy(ev);
     c->comm.destroy();
     for (auto st : c->lat_streams)
         if (st) cudaStreamDestroy(st);
