@@ -187,9 +187,11 @@ typedef struct {
 
 typedef struct {
     size_t f_elems;        /* doubles in f_dev  = nv_local * nnodes_local */
-    size_t fb_elems;       /* doubles in fb_dev = nv_local * plane_stride */
+    size_t fb_elems;       /* doubles in fb_dev = nv_local * plane_stride (x dim for PDG_FLUX_LBM) */
     size_t w_elems;        /* doubles in w_dev  = m * nnodes_local (moments / exchange / equilibrium init) */
-    size_t work_bytes;     /* bytes of work_dev (device scratch: counters, slab carry planes and tables) */
+    size_t work_bytes;     /* bytes of work_dev (device scratch: counters, z-slab carry planes and tables,
+                              lattice ticket/progress counters and boundary traces, large lattice block
+                              tables, the PDG_ASYNC_HOST upload staging) */
     int64_t nnodes;        /* nodes of the full grid */
     int64_t plane_stride;  /* doubles per velocity in fb */
     int32_t nv_local;      /* velocities owned by this rank */
@@ -200,14 +202,18 @@ typedef struct {
 } pdg_sizes;
 
 /* Validate *p and return the buffer sizes of this rank.  Host-only: needs no GPU.
- * Errors: PDG_E_INVALID_ARGUMENT, PDG_E_DIMENSION, PDG_E_DEGREE, PDG_E_VELOCITY_SET, PDG_E_FLUX_MODEL. */
+ * Errors: PDG_E_INVALID_ARGUMENT, PDG_E_DIMENSION, PDG_E_DEGREE, PDG_E_VELOCITY_SET, PDG_E_FLUX_MODEL,
+ * PDG_E_UNSUPPORTED (lattice sets other than D2Q9/D3Q15/D3Q19/D3Q27, lattice sets with
+ * PDG_DECOMP_ZSLAB, a source with a non-LBM model). */
 pdg_status pdg_query_sizes(const pdg_problem *p, pdg_sizes *out);
 
 /* Create a context bound to caller-owned device buffers sized by pdg_query_sizes
  * (f_dev, fb_dev, w_dev, work_dev: 256-byte aligned device pointers on the current
  * device).  Precomputes the per-axis cell blocks (the KLU refactorisation of P:769-777
- * becomes a tiny precomputed inverse: dt and v are constant).  With nranks > 1 it
- * also creates an NCCL communicator from nccl_id (collective over all ranks).
+ * becomes a tiny precomputed inverse: dt and v are constant) and, for lattice sets, the
+ * dense blocks of the scheme's steps; creates the library's own streams (one per lattice
+ * velocity class, the PDG_ASYNC_HOST copy streams).  With nccl_id it also creates an NCCL
+ * communicator (collective over all ranks).
  * Errors: as pdg_query_sizes, plus PDG_E_BUFFER, PDG_E_CUDA, PDG_E_NCCL. */
 pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, double *w_dev, void *work_dev,
                       pdg_ctx **out);
@@ -216,19 +222,21 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
  * fb_elems doubles (inflow planes, constant in time: P:183-184).
  * Either may be NULL to keep the bound buffer's content.  on_device != 0:
  * pointers are device memory, else host (copied on the context stream, then
- * the stream is synchronised before returning). */
+ * the stream is synchronised before returning, unless PDG_ASYNC_HOST). */
 pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_device);
 
 /* Equilibrium initialisation (readings C12, C13): f_i = f^eq_i(w) at every node and
  * fb_i = f^eq_i(wb) on the inflow plane of velocity i.  w, wb: [m][nodes] (w_elems
- * doubles); wb == NULL means wb = w.  Host pointers are staged through w_dev. */
+ * doubles); wb == NULL means wb = w.  Host pointers are staged through w_dev (synchronous), or
+ * with PDG_ASYNC_HOST and wb == NULL through the extra staging region (asynchronous). */
 pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, int on_device);
 
 /* Copy the current f (f_elems doubles, canonical layout) out (checkpoint/readback). */
 pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
 
 /* Advance nsteps palindromic steps (scheme of pdg_problem; nsteps == 0 is a no-op).
- * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE. */
+ * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE (lattice classes
+ * run on library streams forked from and joined back into the context stream). */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
 
 /* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):
@@ -253,7 +261,8 @@ pdg_status pdg_partial_moments(pdg_ctx *c);
 pdg_status pdg_relax_from_w(pdg_ctx *c, double dt);
 
 /* Moments w = P f of the full state ([m][nodes], w_elems doubles) into w (host or
- * device); with nranks > 1 the partial sums are reduced over ranks (every rank gets w). */
+ * device); with nranks > 1 the partial sums are reduced over ranks (every rank gets w).
+ * With PDG_ASYNC_HOST a host download runs on the library copy stream (see the flag). */
 pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device);
 
 /* Number of nodes with rho <= 0 or a non-finite f seen in the local state
