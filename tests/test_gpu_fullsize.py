@@ -120,3 +120,95 @@ def test_fullsize_fused_passes_equal_separate_steps(key):
     S.destroy()
     del S
     torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------
+# Lattice sets at the bench size: one T2 of every velocity on 128^3 cells (D3Q27: every
+# wavefront class, the warp scans, the skewed warps and the cross-CTA hand-over in
+# bench.py's launch configuration), compared with the oracle on sampled cells.  For each
+# velocity the samples lie on the three domain edges through its upstream corner (plus a
+# few cells near it): their dependency cones are single lines or small boxes, and the
+# full-length lines cross every CTA boundary along x and along the pipe axis.
+# --------------------------------------------------------------------------
+def _smooth_field(X, Y, Z, i, nv, amp):
+    sin = torch.sin if isinstance(X, torch.Tensor) else np.sin
+    return (1.0 + amp * sin(0.37 * X + 0.71 * Y + 1.13 * Z + 0.5 * i + 0.3 * X * Y / 97.0)) / nv
+
+
+@pytest.mark.parametrize("lat,N", [("D3Q27", 128), ("D2Q9", 1024)])
+def test_lattice_fullsize_sampled_transport(lat, N):
+    from pdg_inputs import lbm_config
+    cfg = lbm_config(lat, N, nu=2.0)
+    torch.cuda.empty_cache()
+    S = make_solver(cfg)
+    dev = S.f.device
+    D, n = cfg.dim, cfg.n
+    xs = [torch.arange(cfg.N * n, device=dev, dtype=torch.float64) for _ in range(D)]  # node indices
+    if D == 3:
+        X, Y, Z = xs[0].view(1, 1, -1), xs[1].view(1, -1, 1), xs[2].view(-1, 1, 1)
+    else:
+        X, Y, Z = xs[0].view(1, -1), xs[1].view(-1, 1), torch.zeros((), device=dev, dtype=torch.float64)
+    f = S.f.view((cfg.nv,) + cfg.grid_shape)
+    fbv = S.fb.view(cfg.nv, D, -1)
+    vel, _ = cfg.velocities()
+    for i in range(cfg.nv):
+        f[i].copy_(_smooth_field(X, Y, Z, i, cfg.nv, 0.3).expand(cfg.grid_shape))
+        full = _smooth_field(X, Y, Z, 100 + i, cfg.nv, 0.2).expand(cfg.grid_shape)  # one f^b field (C22)
+        for k in range(D):
+            if vel[i][k] == 0:
+                continue
+            ax = D - 1 - k
+            sl = [slice(None)] * D
+            sl[ax] = 0 if vel[i][k] > 0 else cfg.grid_shape[ax] - 1
+            pl = full[tuple(sl)].reshape(-1)
+            fbv[i, k, :pl.numel()].copy_(pl)
+    f0_full = S.f.clone()
+    S.set_state(f0_full)
+    S.transport(cfg.dt)
+    pb = O.Problem.from_config(cfg)
+    Nd = n ** D
+    errs = []
+    for i in range(cfg.nv):
+        v = vel[i]
+        if not any(v[:D]):
+            continue
+        # samples in flow coordinates -> physical cell indices
+        flow = []
+        for d in range(D):
+            for a in (1, N // 3, N - 1):
+                p = [0] * D
+                p[d] = a
+                flow.append(p)
+        flow.append([1] * D)
+        flow.append([min(2, N - 1)] * D)
+        cells = set()
+        for p in flow:
+            c = 0
+            for d in reversed(range(D)):
+                pd_ = p[d] if v[d] >= 0 else N - 1 - p[d]
+                c = c * N + pd_
+            cells.add(c)
+        samples = np.array(sorted(cells), dtype=np.int64)
+        clos = np.flatnonzero(O.upstream_closure(pb, v, samples)).astype(np.int64)
+        idx = cell_node_index(cfg, clos).to(dev)                           # [ncl, Nd] node indices
+        coords = []
+        r = idx.clone()
+        for d in range(D):
+            coords.append((r % (N * n)).double())
+            r = r // (N * n)
+        Xc, Yc = coords[0], coords[1]
+        Zc = coords[2] if D == 3 else torch.zeros_like(Xc)
+        # the same values the GPU run used: f0 gathered from its input, f^b re-evaluated by the same
+        # torch expression on the same device (elementwise, so bitwise the plane values)
+        f0c = np.ascontiguousarray(f0_full.view(cfg.nv, -1)[i][idx.view(-1)].view(idx.shape).cpu().numpy())
+        fbc = np.ascontiguousarray(_smooth_field(Xc, Yc, Zc, 100 + i, cfg.nv, 0.2).cpu().numpy())
+        O.t2_velocity(pb, v, cfg.dt, f0c, fbc, clos)
+        pos = np.searchsorted(clos, samples)
+        ref = f0c[pos]
+        sidx = cell_node_index(cfg, samples).to(dev)
+        got = S.f.view(cfg.nv, -1)[i][sidx.view(-1)].view(samples.size, Nd).cpu().numpy()
+        errs.append(rel_maxnorm(got, ref))
+    S.destroy()
+    del S
+    torch.cuda.empty_cache()
+    assert max(errs) <= 1e-13, errs
