@@ -303,8 +303,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     const int crank = (CS > 1) ? (int)cg::this_cluster().block_rank() : 0;
     const int skew = (XA ? qx : 0) + (PIPE ? crank * g.Wy + wy : 0);
     const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? CS * g.Wy - 1 : 0);
+    // Per-row synchronisation.  Without a pipe axis and with one CTA along x, the warp groups of
+    // different batch indices (wy) are independent: each group of Wx skewed x-warps syncs on its
+    // own named barrier, and no other CTA reads this task's progress.
+    const bool group_sync = !PIPE && g.ngx == 1;
+    const bool publish = (XA && g.ngx > 1) || (PIPE && g.ngy > 1);
     auto step_sync = [&]() {
         if constexpr (CS > 1) cg::this_cluster().sync();
+        else if (group_sync) asm volatile("bar.sync %0, %1;" ::"r"(1 + wy), "r"(32 * g.Wx) : "memory");
         else __syncthreads();
     };
 
@@ -677,7 +683,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 }
             }
             step_sync();
-            if (threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
+            if (publish && threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
         }
         cp_async_wait<0>();
     }
