@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 
     __shared__ double xs[NPASS][2][8][XA ? MF : 1];
     __shared__ int s_task;
+    __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
     // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
     // math), then the y hand-over buffers [pass][2][warps][32][MF] (PIPE)
@@ -308,10 +309,35 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // own named barrier, and no other CTA reads this task's progress.
     const bool group_sync = !PIPE && g.ngx == 1;
     const bool publish = (XA && g.ngx > 1) || (PIPE && g.ngy > 1);
-    auto step_sync = [&]() {
+    // Otherwise (pipe classes, CS = 1) warps sync point to point through shared-memory step
+    // counters instead of a CTA-wide barrier: before step t a warp needs its producers (x-1, y-1)
+    // and its consumers (x+1, y+1) to have finished step t-1 (the consumers have then read the
+    // double-buffered slot this step overwrites).  Warps may drift apart within that slack.
+    const bool p2p = (CS == 1) && !group_sync;
+    volatile int *vdone = s_done;
+    auto wait_done = [&](int w, int t_need) {
+        if (vdone[w] >= t_need) return;
+        while (vdone[w] < t_need) __nanosleep(16);
+    };
+    auto step_begin = [&](int t) {
+        if (!p2p || t == 0) return;
+        if (lane == 0) {
+            if (XA && qx > 0) wait_done(warp - 1, t - 1);
+            if (XA && qx < g.Wx - 1) wait_done(warp + 1, t - 1);
+            if (PIPE && wy > 0) wait_done(warp - g.Wx, t - 1);
+            if (PIPE && wy < g.Wy - 1) wait_done(warp + g.Wx, t - 1);
+        }
+        __syncwarp();
+        __threadfence_block();
+    };
+    auto step_sync = [&](int t) {
         if constexpr (CS > 1) cg::this_cluster().sync();
         else if (group_sync) asm volatile("bar.sync %0, %1;" ::"r"(1 + wy), "r"(32 * g.Wx) : "memory");
-        else __syncthreads();
+        else if (p2p) {
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) vdone[warp] = t;
+        } else __syncthreads();
     };
 
     for (;;) {
@@ -325,6 +351,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
             __syncthreads();
             ctask = s_task;
+            if ((threadIdx.x & 31) == 0) s_done[threadIdx.x >> 5] = -1;
             __syncthreads();
         }
         if (ctask >= g.ntasks_c) return;
@@ -415,6 +442,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         };
 
         for (int t = 0; t < g.nc + maxskew; ++t) {
+            step_begin(t);
             const int r = t - skew;
             if (r >= 0 && r < g.nc && wvalid) {
                 ucell[CA] = r;
@@ -682,8 +710,17 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     }
                 }
             }
-            step_sync();
-            if (publish && threadIdx.x == 0 && t >= maxskew) st_release(P.progress + task, min(g.nc, t - maxskew + 1));
+            step_sync(t);
+            if (publish && threadIdx.x == 0 && t >= maxskew) {
+                int tmin = t;  // rows finished by every warp
+                if (p2p)
+                    for (int w = 0; w < nwarps; ++w) tmin = min(tmin, vdone[w]);
+                if (tmin >= maxskew) st_release(P.progress + task, min(g.nc, tmin - maxskew + 1));
+            }
+        }
+        if (p2p) {
+            __syncthreads();  // every warp done: publish the whole task
+            if (publish && threadIdx.x == 0) st_release(P.progress + task, g.nc);
         }
         cp_async_wait<0>();
     }
