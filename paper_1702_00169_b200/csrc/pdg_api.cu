@@ -614,6 +614,22 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.g.ntasks = pl.ntasks;
     P.g.ntasks_c = pl.ntasks_c;
     P.g.ypf = std::getenv("PDG_LATTICE_NOYPF") ? 0 : 1;
+    // scan rounds: round j adds Bx^(2^j) times an earlier lane's out-trace; once the infinity
+    // norm of that power is below 2^-64 the term cannot change an fp64 result, nor can any later
+    // (smaller) power
+    P.g.nscan = 5;
+    for (int sr = 0; sr < 5; ++sr) {
+        long double nrm = 0.0L;
+        for (int i = 0; i < TB::MF; ++i) {
+            long double row = 0.0L;
+            for (int j = 0; j < TB::MF; ++j) row += fabsl(B.Bpow[((size_t)sr * TB::MF + i) * TB::MF + j]);
+            nrm = std::max(nrm, row);
+        }
+        if (nrm < 0x1p-64L) {
+            P.g.nscan = sr;
+            break;
+        }
+    }
     P.g.nvel = pl.nvel;
     for (int q = 0; q < pl.nvel; ++q) {
         const int j = pl.vel[q];

@@ -109,7 +109,7 @@ struct LatGeom {
     int32_t nvel;
     int32_t ntasks_c;    // cluster-level tasks (== ntasks without clusters)
     int32_t ypf;         // 1: prefetch the previous CTA's y traces one row ahead
-    int32_t pad2;
+    int32_t nscan;       // x-scan rounds carrying weight: round j is dropped when |Bx^(2^j)| < 2^-64
 };
 
 template <int D, int N, int ACT>
@@ -126,6 +126,20 @@ struct LatParams {
     LatVel v[kLatMaxVel];
     typename LatTabSel<N, S::DA>::type tab;
 };
+
+// Optional per-phase cycle counters of one warp (diagnostics build: -DPDG_LAT_TIMING)
+#ifdef PDG_LAT_TIMING
+#define PDG_TMARK(k)                                                                                 \
+    do {                                                                                             \
+        const long long now_ = clock64();                                                            \
+        tph[k] += now_ - tlast;                                                                      \
+        tlast = now_;                                                                                \
+    } while (0)
+#else
+#define PDG_TMARK(k) \
+    do {            \
+    } while (0)
+#endif
 
 __device__ __forceinline__ int ld_acquire(const int *p)
 {
@@ -261,6 +275,10 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     constexpr int PFA = LatRing<D>::PFA, RING = LatRing<D>::RING;
     static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     const unsigned FULL = 0xffffffffu;
+#ifdef PDG_LAT_TIMING
+    long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+#endif
 
     __shared__ double xs[NPASS][2][8][XA ? MF : 1];
     __shared__ int s_task;
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // counters instead of a CTA-wide barrier: before step t a warp needs its producers (x-1, y-1)
     // and its consumers (x+1, y+1) to have finished step t-1 (the consumers have then read the
     // double-buffered slot this step overwrites).  Warps may drift apart within that slack.
-    const bool p2p = (CS == 1) && !group_sync;
+    const bool p2p = (CS == 1) && PIPE;
     volatile int *vdone = s_done;
     auto wait_done = [&](int w, int t_need) {
         if (vdone[w] >= t_need) return;
@@ -354,7 +372,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             if ((threadIdx.x & 31) == 0) s_done[threadIdx.x >> 5] = -1;
             __syncthreads();
         }
-        if (ctask >= g.ntasks_c) return;
+        if (ctask >= g.ntasks_c) {
+#ifdef PDG_LAT_TIMING
+            if (blockIdx.x == 0 && lane == 0)
+                printf("lat-timing ACT=%d warp %d: begin-wait %lld load %lld traces %lld mma1 %lld scan %lld mma2 %lld store %lld sync %lld\n",
+                       ACT, warp, tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], tph[6], tph[7]);
+#endif
+            return;
+        }
         // ticket order (pipe group, velocity, gx): every velocity's pipeline advances together, and
         // the tasks a task waits on (gx - 1: ticket - 1; previous pipe group: ticket - nvel ngx)
         // come earlier.  A cluster task covers CS consecutive pipe groups (one per CTA).
@@ -442,7 +467,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         };
 
         for (int t = 0; t < g.nc + maxskew; ++t) {
+            PDG_TMARK(7);
             step_begin(t);
+            PDG_TMARK(0);
             const int r = t - skew;
             if (r >= 0 && r < g.nc && wvalid) {
                 ucell[CA] = r;
@@ -465,6 +492,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     prefetch(r + PFA);
                     cp_async_wait<PFA>();  // row r has landed, rows r+1 .. r+PFA may be in flight
                 }
+                PDG_TMARK(1);
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
                 const double *src = wbuf + (r % RING) * NB * 32 + lane;
                 double fprev[NB];  // input of the second sweep (output of the first)
@@ -530,6 +558,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         }
 #pragma unroll
                         for (int sidx = 0; sidx < 5; ++sidx) {
+                            if (sidx >= g.nscan) continue;  // powers below 2^-64: no effect in fp64 (uniform)
                             const int o = 1 << sidx;
                             double pv[MF];
 #pragma unroll
@@ -558,6 +587,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             }
                         }
                     };
+                    PDG_TMARK(2);
                     if constexpr (USE_MMA) {
                         // fp64 tensor cores (DMMA 8x8x4): the warp's 32 units are the N dimension.
                         //   F0 = [M | Q_chain | Q_pipe] [F_old; S_chain; S_pipe]     (NB x K) (K x 32)
@@ -612,12 +642,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             __syncwarp();
                         };
                         spill();
+                        PDG_TMARK(3);
                         if constexpr (XA) {
                             double a[MF], sin_[MF];
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
                                 a[j] = valid ? fsrc[(j * N + N - 1) * 32 + lane] + stg[(j * N + N - 1) * 32 + lane] : 0.0;
                             xscan(a, sin_);
+                            PDG_TMARK(4);
                             __syncwarp();
 #pragma unroll
                             for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sin_[j];
@@ -700,6 +732,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                     for (int q = 0; q < NB; ++q) fprev[q] = fn[q];
                 }
+                PDG_TMARK(5);
                 if (valid) {
 #pragma unroll
                     for (int q = 0; q < NB; ++q) {
@@ -710,6 +743,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     }
                 }
             }
+            PDG_TMARK(6);
             step_sync(t);
             if (publish && threadIdx.x == 0 && t >= maxskew) {
                 int tmin = t;  // rows finished by every warp
