@@ -6,15 +6,17 @@ One "step" is one palindromic step M2(dt) = T2(dt/2) C2(dt) T2(dt/2)
 over the whole workload (all rows of SURVEY §8(a)).  The default workload is
 BASELINE config 5 (3-D isothermal, 256^3 cells, p=2, D3Q6 x 4 components: 10.9 G
 node.velocity updates per step; f = 87 GB in place, far larger than L2, so no L2
-flush is needed between steps).  Multi-GPU (torchrun): velocities are sharded
-evenly and one NCCL sum of the moments per step feeds the local relaxation
-(strong scaling: total work fixed).
+flush is needed between steps).  Multi-GPU (torchrun): the exact z-slab decomposition by
+default (--decomp zslab: slabs of cell planes, NCCL all-gather of carry planes), or
+velocity shards with one NCCL sum of the moments per collision (--decomp velocity;
+the default for --lattice workloads); strong scaling: total work fixed.
 
 The JSON line adds:
   roofline     : the dominant kernel's algorithmic bytes / its CUDA-event time (on the
                  library stream), against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline : the CPU oracle (oracle/, as it stands) timed on this host on a bounded
-                 sample of the same workload (N=64 sub-box of config 5, same p, nu, model).
+                 sample of the same workload (N=64 sub-box of config 5, same p, nu, model),
+                 with the CPU model, RAM and a single-thread timing (N=16 sub-box).
   e2e          : the same metric through the public C-ABI with HOST buffers: per step,
                  pdg_set_equilibrium(host w0, pinned) + pdg_step(1) + pdg_moments(host w), with
                  PDG_ASYNC_HOST so that uploads and downloads of consecutive steps overlap.
@@ -153,6 +155,46 @@ def omp_threads():
         return os.cpu_count()
 
 
+def host_info():
+    """CPU model and RAM of the host the oracle runs on (state them)."""
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 1024 ** 2, 1)
+                    break
+    except OSError:
+        pass
+    return model, ram
+
+
+def single_thread_baseline(cfg, N_sub):
+    """The same oracle step on one thread (OMP_NUM_THREADS=1 in a child process)."""
+    code = ("import sys, time, json; sys.path.insert(0, %r); import bench; from pdg_inputs import CONFIGS, lbm_config; "
+            "cfg = %s; sub, pb, fc, fbc, _ = bench.oracle_prepare(cfg, %d); t0 = time.perf_counter(); "
+            "bench.oracle_step(pb, fc, fbc); dt = time.perf_counter() - t0; "
+            "print(json.dumps({'value': sub.updates_per_step / dt, 'seconds': dt, 'N': sub.N, "
+            "'updates': sub.updates_per_step}))")
+    expr = (f"lbm_config({cfg.lattice!r}, {cfg.N}, p={cfg.p}, nu=2.0)" if cfg.lattice else
+            f"[c for c in CONFIGS.values() if c.name == {cfg.name!r}][0]")
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code % (ROOT, expr, N_sub)], env=env, capture_output=True,
+                             text=True, timeout=120)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"value": r["value"], "unit": UNIT, "cores": 1,
+                "sample": f"1 M2 step of the {r['N']}^{cfg.dim}-cell sub-box ({r['updates']} node.velocity "
+                          f"updates, {r['seconds']:.2f} s)"}
+    except Exception as e:  # reported, never fatal
+        return {"error": repr(e)[:200]}
+
+
 def cpu_baseline(cfg, N_sub=64):
     sub, pb, fc, fbc, _ = oracle_prepare(cfg, N_sub)
     N_sub = sub.N
@@ -160,10 +202,13 @@ def cpu_baseline(cfg, N_sub=64):
     oracle_step(pb, fc, fbc)
     dt = time.perf_counter() - t0
     ups = sub.updates_per_step / dt
+    model, ram = host_info()
     return {"value": ups, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
             "sample": f"1 M2 step of the {N_sub}^{cfg.dim}-cell sub-box of {cfg.name} (same p, lambda, nu, model; "
                       f"{sub.updates_per_step} node.velocity updates, {dt:.2f} s), oracle/pdg_oracle.c -O2 "
-                      f"-ffp-contract=off, OpenMP over velocities/nodes"}
+                      f"-ffp-contract=off, OpenMP over velocities/nodes",
+            "cpu_model": model, "ram_gb": ram,
+            "single_thread": single_thread_baseline(cfg, max(4, N_sub // 4))}
 
 
 def run_reference(args, cfg):
