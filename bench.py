@@ -15,8 +15,9 @@ The JSON line adds:
   roofline     : the dominant kernel's algorithmic bytes / its CUDA-event time (on the
                  library stream), against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline : the CPU oracle (oracle/, as it stands) timed on this host on a bounded
-                 sample of the same workload (N=64 sub-box of config 5, same p, nu, model),
-                 with the CPU model, RAM and a single-thread timing (N=16 sub-box).
+                 sample of the same workload (N=128 sub-box of config 5, same p, nu, model:
+                 ~10 s of CPU work), with the CPU model, RAM and a single-thread timing
+                 (N=32 sub-box).
   e2e          : the same metric through the public C-ABI with HOST buffers: per step,
                  pdg_set_equilibrium(host w0, pinned) + pdg_step(1) + pdg_moments(host w), with
                  PDG_ASYNC_HOST so that uploads and downloads of consecutive steps overlap.
@@ -409,7 +410,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-cells", type=int, default=64)
+    ap.add_argument("--cpu-cells", type=int, default=128, help="cells per axis of the oracle's timed sub-box")
     ap.add_argument("--ref-cells", type=int, default=32)
     ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
                     help="multi-GPU decomposition (default: zslab when launched on several ranks)")
@@ -424,7 +425,7 @@ def main():
     from pdg_inputs import CONFIGS, lbm_config
     cfg = lbm_config(args.lattice, args.cells, p=args.degree, nu=2.0) if args.lattice else CONFIGS[args.config]
     if args.lattice:
-        args.cpu_cells = min(args.cpu_cells, 24 if cfg.dim == 3 else 256)
+        args.cpu_cells = min(args.cpu_cells, 64 if cfg.dim == 3 else 512)
         args.ref_cells = min(args.ref_cells, 16 if cfg.dim == 3 else 128)
     if args.decomp is None:  # the z-slab decomposition is implemented for axis-aligned sets only
         args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not args.lattice else "velocity"
