@@ -88,6 +88,8 @@ struct LatPlan {
     int vel[pdg::kLatMaxVel] = {0};  // local velocity indices
     int Wx = 1, Wy = 1, ngx = 1, ngy = 1, nlane = 1, nw = 1, nc = 1, ntasks = 0;
     int cs = 1, ntasks_c = 0;  // cluster size along the pipe axis, cluster-level tasks
+    int nseg = 1, seglen = 1;  // chain segments (truncated-dependency split) and their rows
+    int rcap = 1;              // chain rows per task the trace buffers hold
     size_t xbuf = 0, ybuf = 0;       // doubles
     size_t ints_off = 0, xbuf_off = 0, ybuf_off = 0;  // this class's slices of the work buffers
 };
@@ -141,12 +143,35 @@ void plan_lattice(const Geometry &g, LatPlan &P)
         }
     }
     const int ngyc = (P.ngy + P.cs - 1) / P.cs;
-    P.ntasks_c = P.nvel * P.ngx * ngyc;
+    // Chain segments.  A class without a pipe axis whose tasks cannot fill the GPU (2-D grids:
+    // one task per velocity and x group) is latency-bound by its serial chain; it is cut into
+    // segments swept concurrently, each starting kHalo rows early from a zero chain trace.  The
+    // halo depth comes from a norm bound of the chain operator per launch (lattice_chain_halo:
+    // the truncated traces agree with the exact ones to 2^-64); a launch whose bound exceeds the
+    // segment length runs unsegmented.  Planned for the 148 SMs of a B200 at 2 CTAs per SM (the
+    // segments only change how much of the chain one task walks, not the result).
+    P.nseg = 1;
+    P.seglen = P.nc;
+    if (XA && !PIPE && P.cs == 1) {
+        const int base = P.nvel * P.ngx * P.ngy, slots = 148 * 2;
+        int Ls = 0;
+        if (const char *e = std::getenv("PDG_LATTICE_SEG")) Ls = std::max(0, std::atoi(e));  // 0: off
+        else if (2 * base <= slots && P.nc >= 128) {
+            const int ns = std::min(slots / base, P.nc / 64);  // segments of >= 64 rows
+            Ls = (P.nc + ns - 1) / ns;
+        }
+        if (Ls > 0 && Ls < P.nc) {
+            P.seglen = Ls;
+            P.nseg = (P.nc + Ls - 1) / Ls;
+        }
+    }
+    P.rcap = (P.nseg > 1) ? std::min(P.nc, 2 * P.seglen) : P.nc;  // segment + a halo of at most one segment
+    P.ntasks_c = P.nvel * P.ngx * ngyc * P.nseg;
     P.ntasks = P.ntasks_c * P.cs;  // CTA-level tasks incl. the padding of the last cluster group
     int mf = 1;
     for (int t = 1; t < P.d; ++t) mf *= g.n;
     // boundary traces of up to two sweeps per launch
-    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wy * mf : 0;
+    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.rcap * P.Wy * mf : 0;
     P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * ((mf + 1) & ~1) : 0;  // even stride
     P.xbuf = (P.xbuf + 1) & ~(size_t)1;  // keep every slice 16-byte aligned
 }
@@ -182,7 +207,7 @@ void lattice_classes(const Geometry &g, const double *vel, std::vector<LatPlan> 
         q.ints_off = io;
         q.xbuf_off = xo;
         q.ybuf_off = yo;
-        io += (((size_t)q.ntasks + 1 + 63) / 64) * 64;
+        io += (((size_t)2 * q.ntasks + 1 + 63) / 64) * 64;  // ticket, progress[ntasks], halo flags[ntasks]
         xo += q.xbuf;
         yo += q.ybuf;
     }
@@ -312,7 +337,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
             std::vector<LatPlan> cls;
             lattice_classes(*g, p->vel, cls);
             for (const auto &q : cls) {
-                g->lat_ints = std::max(g->lat_ints, q.ints_off + (((size_t)q.ntasks + 1 + 63) / 64) * 64);
+                g->lat_ints = std::max(g->lat_ints, q.ints_off + (((size_t)2 * q.ntasks + 1 + 63) / 64) * 64);
                 g->lat_xbuf = std::max(g->lat_xbuf, q.xbuf_off + q.xbuf);
                 g->lat_ybuf = std::max(g->lat_ybuf, q.ybuf_off + q.ybuf);
             }
@@ -448,6 +473,7 @@ struct pdg_ctx {
     cudaEvent_t lat_fork = nullptr;
     std::vector<cudaEvent_t> lat_join;
     std::map<std::pair<int, double>, pdg::LatticeBlockLD> lat_blocks;  // (act, dt') -> block
+    std::map<std::pair<int, double>, int> lat_halo;                    // (act, dt') -> chain halo rows (-1: none)
     std::map<std::tuple<const void *, int, size_t>, int> launch_cache;  // (kernel, threads, smem) -> CTAs/SM
     std::map<std::pair<int, double>, double *> lat_gtab;  // (act, dt') -> device copy of a large block table
     double *lat_gtab_base = nullptr;                      // slots in the work buffer
@@ -596,6 +622,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.fb = c->fb;
     P.ticket = c->lat_ints + pl.ints_off;
     P.progress = c->lat_ints + pl.ints_off + 1;
+    P.hdone = P.progress + pl.ntasks;
     P.xbuf = c->lat_xbuf + pl.xbuf_off;
     P.ybuf = c->lat_ybuf + pl.ybuf_off;
     for (int k = 0; k < 3; ++k) {
@@ -613,6 +640,25 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.g.nc = pl.nc;
     P.g.ntasks = pl.ntasks;
     P.g.ntasks_c = pl.ntasks_c;
+    // chain segments: the halo depth of this (class, dt') from the norm bound, or unsegmented
+    P.g.nseg = 1;
+    P.g.seglen = pl.nc;
+    P.g.halo = 0;
+    P.g.rcap = pl.nc;
+    if (pl.nseg > 1) {
+        const auto hk = std::make_pair(pl.act, dtp);
+        auto hi = c->lat_halo.find(hk);
+        int h = -1;
+        if (hi != c->lat_halo.end()) h = hi->second;
+        else h = c->lat_halo[hk] = pdg::lattice_chain_halo(B, 1, pl.seglen);
+        if (h > 0 && NPASS * h <= pl.seglen) {
+            P.g.nseg = pl.nseg;
+            P.g.seglen = pl.seglen;
+            P.g.halo = NPASS * h;  // two sweeps per launch: the second one's input is exact after h rows
+            P.g.rcap = pl.rcap;
+        }
+    }
+    P.g.ntasks_c = pl.ntasks_c / pl.nseg * P.g.nseg;
     P.g.ypf = std::getenv("PDG_LATTICE_NOYPF") ? 0 : 1;
     // scan rounds: round j adds Bx^(2^j) times an earlier lane's out-trace; once the infinity
     // norm of that power is below 2^-64 the term cannot change an fp64 result, nor can any later
@@ -712,9 +758,9 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
         occ = std::max(1, occ);
         c->launch_cache[key] = occ;
     }
-    const int units = std::max(1, std::min(pl.ntasks_c, occ));
+    const int units = std::max(1, std::min(P.g.ntasks_c, occ));
     lc.gridDim = dim3((unsigned)(units * CS));
-    PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)pl.ntasks + 1), st));
+    PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)2 * pl.ntasks + 1), st));
     PDG_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, P));
     return PDG_OK;
 }

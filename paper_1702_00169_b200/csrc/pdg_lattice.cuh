@@ -110,6 +110,10 @@ struct LatGeom {
     int32_t ntasks_c;    // cluster-level tasks (== ntasks without clusters)
     int32_t ypf;         // 1: prefetch the previous CTA's y traces one row ahead
     int32_t nscan;       // x-scan rounds carrying weight: round j is dropped when |Bx^(2^j)| < 2^-64
+    int32_t nseg;        // chain segments (1: the whole chain per task)
+    int32_t seglen;      // chain rows stored by one segment
+    int32_t halo;        // rows a segment sweeps ahead of its first stored row (from a zero chain trace)
+    int32_t rcap;        // chain rows per task in the trace buffers
 };
 
 template <int D, int N, int ACT>
@@ -119,6 +123,7 @@ struct LatParams {
     const double *fb;
     int *ticket;     // [0]; progress counters follow: progress[task] = rows published
     int *progress;
+    int *hdone;      // [task]: 1 once the segment has read its halo rows (their old values)
     double *xbuf;    // [task][row][Wy][MF]       x out-traces at CTA boundaries
     double *ybuf;    // [task][row][pass][Wx][32][MFP] y out-traces at CTA boundaries (MFP = MF rounded up to
                      // an even count: 16-byte cp.async.cg copies)
@@ -374,20 +379,32 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         }
         if (ctask >= g.ntasks_c) {
 #ifdef PDG_LAT_TIMING
-            if (blockIdx.x == 0 && lane == 0)
-                printf("lat-timing ACT=%d warp %d: begin-wait %lld load %lld traces %lld mma1 %lld scan %lld mma2 %lld store %lld sync %lld\n",
-                       ACT, warp, tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], tph[6], tph[7]);
+            if (blockIdx.x < 6 && lane == 0 && (warp == 0 || warp == nwarps - 1))
+                printf("lat-timing ACT=%d cta %d warp %d: begin-wait %lld load %lld traces %lld mma1 %lld scan %lld mma2 %lld store %lld sync %lld\n",
+                       ACT, (int)blockIdx.x, warp, tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], tph[6], tph[7]);
 #endif
             return;
         }
         // ticket order (pipe group, velocity, gx): every velocity's pipeline advances together, and
         // the tasks a task waits on (gx - 1: ticket - 1; previous pipe group: ticket - nvel ngx)
         // come earlier.  A cluster task covers CS consecutive pipe groups (one per CTA).
+        // Chain segments (nseg > 1, CS = 1) are claimed in DESCENDING order: segment s waits for
+        // segment s + 1 to have read its halo rows before overwriting them, so every wait still
+        // targets an earlier ticket.
         const int per_gy = g.nvel * g.ngx;
-        const int gyc = ctask / per_gy, rem = ctask - gyc * per_gy;
+        const int per_seg = g.ntasks_c / g.nseg;
+        const int seg = g.nseg - 1 - ctask / per_seg;
+        const int cts = ctask - (g.nseg - 1 - seg) * per_seg;
+        const int gyc = cts / per_gy, rem = cts - gyc * per_gy;
         const int vi = rem / g.ngx, gx = rem - vi * g.ngx;
         const int gy = gyc * CS + crank;
-        const int task = (gy * g.nvel + vi) * g.ngx + gx;  // CTA-level task: progress and traces
+        const int task = seg * per_seg + (gy * g.nvel + vi) * g.ngx + gx;  // CTA-level task: progress and traces
+        // chain rows: stored [rs, r1), swept from r0 (the halo [r0, rs) starts from a zero trace)
+        const int rs = seg * g.seglen;
+        const int r0 = max(0, rs - g.halo);
+        const int r1 = min(g.nc, rs + g.seglen);
+        const int nrow = r1 - r0;
+        bool hclear = !(seg < g.nseg - 1 && g.halo > 0);  // the next segment has read our last rows
         const LatVel &V = P.v[vi];
         const int ux = (gx * g.Wx + qx) * 32 + lane;  // x cell (XA) or x node
         const int uw = gy * g.Wy + wy;                // pipe cell, batch node or 0
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             double s0c[MF];
 #pragma unroll
             for (int j = 0; j < MF; ++j) s0c[j] = 0.0;
-            if (valid) ghost_face<D, N, ACT, CA>(P, V, ucell, s0c);
+            if (valid && r0 == 0) ghost_face<D, N, ACT, CA>(P, V, ucell, s0c);
 #pragma unroll
             for (int ps = 0; ps < NPASS; ++ps)
 #pragma unroll
@@ -438,8 +455,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         bool ypf = false;  // this lane's y traces for the current row sit in spy
         // issue the copies of row rr into buffer rr & 1 (one commit group per row)
         auto prefetch = [&](int rr) {
-            if (valid && rr < g.nc) {
-                const int64_t ubr = ibase + cbase + (int64_t)rr * cstep;
+            if (valid && rr < nrow) {
+                const int64_t ubr = ibase + cbase + (int64_t)(r0 + rr) * cstep;
                 double *dst = wbuf + (rr % RING) * NB * 32 + lane;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) {
@@ -451,11 +468,11 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             }
             if constexpr (PIPE) {
                 ypf = false;
-                if (ycons && rr < g.nc && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
+                if (ycons && rr < nrow && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
 #pragma unroll
                     for (int ps = 0; ps < NPASS; ++ps) {
                         const double *ysrc =
-                            P.ybuf + (((((int64_t)(task - per_gy) * g.nc + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                            P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
                         double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                         for (int h = 0; h < MFP; h += 2) cp_async16_cg(yd + h, ysrc + h);
@@ -466,14 +483,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             cp_async_commit();
         };
 
-        for (int t = 0; t < g.nc + maxskew; ++t) {
+        for (int t = 0; t < nrow + maxskew; ++t) {
             PDG_TMARK(7);
             step_begin(t);
             PDG_TMARK(0);
-            const int r = t - skew;
-            if (r >= 0 && r < g.nc && wvalid) {
-                ucell[CA] = r;
-                const int64_t ub = ibase + cbase + (int64_t)r * cstep;
+            const int r = t - skew;  // row of the task (chain row r0 + r)
+            if (r >= 0 && r < nrow && wvalid) {
+                ucell[CA] = r0 + r;
+                const int64_t ub = ibase + cbase + (int64_t)(r0 + r) * cstep;
                 if (r == 0)
                     for (int k = 0; k < PFA; ++k) prefetch(k);
                 double sy_pf[(PIPE ? NPASS : 1)][PIPE ? MF : 1];
@@ -520,7 +537,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             } else {
                                 if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
                                 const double *ysrc =
-                                    P.ybuf + (((((int64_t)(task - per_gy) * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                                    P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
                             }
@@ -540,7 +557,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) & 1][warp - 1][j];
                         } else if (gx > 0) {
                             if (ps == 0) wait_progress(P.progress + task - 1, r + 1);
-                            const double *xsrc = P.xbuf + ((((int64_t)(task - 1) * g.nc + r) * NPASS + ps) * g.Wy + wy) * MF;
+                            const double *xsrc = P.xbuf + ((((int64_t)(task - 1) * g.rcap + r) * NPASS + ps) * g.Wy + wy) * MF;
 #pragma unroll
                             for (int j = 0; j < MF; ++j) s0[j] = __ldcg(xsrc + j);
                         } else if (lane == 0 && valid) {
@@ -580,7 +597,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int j = 0; j < MF; ++j) xs[ps][t & 1][warp][j] = a[j];
                             if (qx == g.Wx - 1 && gx < g.ngx - 1) {
-                                double *dst = P.xbuf + ((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wy + wy) * MF;
+                                double *dst = P.xbuf + ((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wy + wy) * MF;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
                                 __threadfence();
@@ -695,11 +712,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                                 for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TY][j * NB + q], sy[j], fn[q]);
                         }
+                        PDG_TMARK(3);
                         if constexpr (XA) {
                             double a[MF], sin_[MF];
 #pragma unroll
                             for (int j = 0; j < MF; ++j) a[j] = valid ? fold(j * N + N - 1) + fn[j * N + N - 1] : 0.0;
                             xscan(a, sin_);
+                            PDG_TMARK(4);
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
 #pragma unroll
@@ -723,7 +742,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
                         if (wy == g.Wy - 1 && crank == CS - 1 && gy < g.ngy - 1) {
                             double *dst =
-                                P.ybuf + (((((int64_t)task * g.nc + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                                P.ybuf + (((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                             for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
                             __threadfence();
@@ -733,7 +752,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     for (int q = 0; q < NB; ++q) fprev[q] = fn[q];
                 }
                 PDG_TMARK(5);
-                if (valid) {
+                // the last halo rows of the next segment: wait until it has read their old values
+                if (!hclear && r0 + r >= r1 - g.halo) {
+                    if (lane == 0) wait_progress(P.hdone + task + per_seg, 1);
+                    __syncwarp();
+                    hclear = true;
+                }
+                if (valid && r0 + r >= rs) {
 #pragma unroll
                     for (int q = 0; q < NB; ++q) {
                         int64_t off = 0;
@@ -749,12 +774,17 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 int tmin = t;  // rows finished by every warp
                 if (p2p)
                     for (int w = 0; w < nwarps; ++w) tmin = min(tmin, vdone[w]);
-                if (tmin >= maxskew) st_release(P.progress + task, min(g.nc, tmin - maxskew + 1));
+                if (tmin >= maxskew) st_release(P.progress + task, min(nrow, tmin - maxskew + 1));
+            }
+            // every warp has read the halo rows (cp.async waited): release them to the previous segment
+            if (rs > r0 && t == rs - r0 - 1 + maxskew) {
+                __syncthreads();
+                if (threadIdx.x == 0) st_release(P.hdone + task, 1);
             }
         }
         if (p2p) {
             __syncthreads();  // every warp done: publish the whole task
-            if (publish && threadIdx.x == 0) st_release(P.progress + task, g.nc);
+            if (publish && threadIdx.x == 0) st_release(P.progress + task, nrow);
         }
         cp_async_wait<0>();
     }

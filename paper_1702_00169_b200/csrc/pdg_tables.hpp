@@ -17,6 +17,7 @@
 //
 // Computed in long double and rounded once to double.  Independent of oracle/.
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <utility>
@@ -258,6 +259,125 @@ inline bool lattice_block(int p, int d, const long double *kappa, LatticeBlockLD
         Bx = T;
     }
     return true;
+}
+
+// small dense helpers of lattice_chain_halo (row-major mf x mf, long double)
+inline void lat_mm(int mf, const long double *A, const long double *B, long double *C)
+{
+    for (int i = 0; i < mf; ++i)
+        for (int j = 0; j < mf; ++j) {
+            long double a = 0.0L;
+            for (int k = 0; k < mf; ++k) a += A[i * mf + k] * B[k * mf + j];
+            C[i * mf + j] = a;
+        }
+}
+inline long double lat_ninf(int mf, const long double *A)
+{
+    long double m = 0.0L;
+    for (int i = 0; i < mf; ++i) {
+        long double r = 0.0L;
+        for (int j = 0; j < mf; ++j) r += fabsl(A[i * mf + j]);
+        m = std::max(m, r);
+    }
+    return m;
+}
+// sum of the block norms of a block sequence (an upper bound of its Toeplitz operator's inf-norm)
+inline long double lat_norm_seq(int mf, const std::vector<long double> &A)
+{
+    const size_t s = (size_t)mf * mf;
+    long double r = 0.0L;
+    for (size_t m = 0; m < A.size() / s; ++m) r += lat_ninf(mf, A.data() + m * s);
+    return r;
+}
+// block sequence convolution (product of block lower-triangular Toeplitz operators)
+inline std::vector<long double> lat_conv(int mf, const std::vector<long double> &A, const std::vector<long double> &B)
+{
+    const size_t s = (size_t)mf * mf, la = A.size() / s, lb = B.size() / s;
+    std::vector<long double> C((la + lb - 1) * s, 0.0L), c(s);
+    for (size_t a = 0; a < la; ++a)
+        for (size_t b = 0; b < lb; ++b) {
+            lat_mm(mf, A.data() + a * s, B.data() + b * s, c.data());
+            for (size_t i = 0; i < s; ++i) C[(a + b) * s + i] += c[i];
+        }
+    return C;
+}
+
+// Chain truncation depth of a lattice sweep whose x axis (active index 0) and chain axis
+// (active index tc) are the block's only coupled directions (classes without a pipe axis).
+//
+// Sweeping rows r0, r0+1, ... of the chain with a ZERO chain in-trace at r0 instead of the
+// true one leaves an error e in the chain in-traces of row r0 that the sweep carries as
+// e_{r+1} = T e_r, where T maps the chain in-traces of a whole row (x = 0, 1, ...; exact x
+// inflow at x = 0) to its chain out-traces: a block lower-triangular Toeplitz operator with
+// blocks T_0 = Y (chain in -> chain out of the same cell) and T_m = X_i B_x^{m-1} X_o (chain in
+// -> x out, m-1 cells of x hand-over, x in -> chain out), all rows of the block's inflow
+// responses Q.  ||T^k||_inf <= sum_m ||(T^k)_m||_inf; the sequence is truncated once
+// ||B_x^j X_o|| < 2^-100 ||X_o|| and the tail is bounded with S = sum_i ||B_x^i|| (from a
+// power of B_x with norm < 1/2) and ||(A+E)^k - A^k|| <= k ||E|| (||A|| + ||E||)^(k-1).
+// Returns the smallest H (a multiple of k in {1, 4}) with ||T^H|| <= 2^-64, i.e. after H rows
+// the computed traces differ from the exact sweep's by at most 2^-64 of the true in-traces
+// (below the fp64 rounding of every later row), or -1 when no such H <= hmax exists.
+inline int lattice_chain_halo(const LatticeBlockLD &B, int tc, int hmax)
+{
+    typedef long double LD;
+    const int n = B.n, nb = B.nb, mf = B.mf, s = mf * mf;
+    if (B.d < 2 || tc < 1 || tc >= B.d) return -1;
+    auto outq = [&](int t, int j) {  // node of reduced index j on the out-face of active axis t
+        int pw = 1;
+        for (int i = 0; i < t; ++i) pw *= n;
+        return (j % pw) + (j / pw) * pw * n + (n - 1) * pw;
+    };
+    std::vector<LD> Y(s), Xo(s), Xi(s), Bx(s), t1(s), t2(s);
+    for (int i = 0; i < mf; ++i)
+        for (int j = 0; j < mf; ++j) {
+            Y[i * mf + j] = B.Q[((size_t)tc * nb + outq(tc, i)) * mf + j];
+            Xo[i * mf + j] = B.Q[((size_t)tc * nb + outq(0, i)) * mf + j];
+            Xi[i * mf + j] = B.Q[((size_t)0 * nb + outq(tc, i)) * mf + j];
+            Bx[i * mf + j] = B.Q[((size_t)0 * nb + outq(0, i)) * mf + j];
+        }
+    // S >= sum_i ||Bx^i||: partial sum up to a power j0 with ||Bx^j0|| = q < 1/2, divided by 1 - q
+    LD S = 0.0L, q = 1.0L;
+    {
+        std::vector<LD> P(s, 0.0L);
+        for (int i = 0; i < mf; ++i) P[i * mf + i] = 1.0L;
+        int j = 0;
+        for (; j < 4096; ++j) {
+            q = lat_ninf(mf, P.data());
+            if (q < 0.5L && j > 0) break;
+            S += q;
+            lat_mm(mf, Bx.data(), P.data(), t1.data());
+            P = t1;
+        }
+        if (j == 4096) return -1;
+        S /= (1.0L - q);
+    }
+    // T_m for m < M, and the tail bound E >= sum_{m >= M} ||T_m||
+    std::vector<LD> T(Y);
+    std::vector<LD> P(Xo);
+    const LD xo = lat_ninf(mf, Xo.data()), xi = lat_ninf(mf, Xi.data());
+    LD tail = 0.0L;
+    for (int m = 1;; ++m) {
+        if (lat_ninf(mf, P.data()) <= 0x1p-100L * xo) {
+            tail = xi * S * lat_ninf(mf, P.data());
+            break;
+        }
+        if (m > 512) return -1;  // slow decay along x: the halo would not pay anyway
+        lat_mm(mf, Xi.data(), P.data(), t1.data());
+        T.insert(T.end(), t1.begin(), t1.end());
+        lat_mm(mf, Bx.data(), P.data(), t2.data());
+        P = t2;
+    }
+    const LD r1 = lat_norm_seq(mf, T) + tail;  // ||T||
+    const std::vector<LD> T2 = lat_conv(mf, T, T);
+    const std::vector<LD> T4 = lat_conv(mf, T2, T2);
+    const LD r4 = lat_norm_seq(mf, T4) + 4.0L * tail * powl(r1, 3.0L);  // ||T^4||
+    int best = -1;
+    if (r1 < 1.0L) best = (int)ceill(64.0L / -log2l(r1));
+    if (r4 < 1.0L) {
+        const int h4 = 4 * (int)ceill(64.0L / -log2l(r4));
+        if (best < 0 || h4 < best) best = h4;
+    }
+    return (best > 0 && best <= hmax) ? best : -1;
 }
 
 }  // namespace pdg

@@ -401,3 +401,109 @@ def test_lattice_host_pointer_paths():
     assert rel_maxnorm(f.numpy().reshape(f0.shape), f0) <= TOL_OP
     assert rel_maxnorm(fb, lattice_planes(cfg, fbf, S.sizes.plane_stride)) <= TOL_OP
     assert rel_maxnorm(w.numpy().reshape((cfg.m,) + cfg.grid_shape), O.moments(pb, f0)) <= TOL_OP
+
+
+# --------------------------------------------------------------------------
+# Chain segments: a class without a pipe axis is cut along its chain into
+# segments swept concurrently, each starting `halo` rows early from a zero chain trace, the
+# halo taken from the norm bound of the chain operator (pdg_tables.hpp lattice_chain_halo).
+# PDG_LATTICE_SEG forces the segment length so that small grids run several segments.
+# --------------------------------------------------------------------------
+@pytest.fixture
+def seglen(request):
+    old = os.environ.get("PDG_LATTICE_SEG")
+    os.environ["PDG_LATTICE_SEG"] = str(request.param)
+    yield request.param
+    if old is None:
+        os.environ.pop("PDG_LATTICE_SEG", None)
+    else:
+        os.environ["PDG_LATTICE_SEG"] = old
+
+
+def _d2q9_box(ncell, p, dt, lam=1.0, hi=(1.0, 1.0, 1.0)):
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import lattice
+    import math
+    vel, wts = lattice("D2Q9", lam)
+    fparams = [lam / math.sqrt(3.0)] + list(wts)
+    pb = pdg.make_problem(2, list(ncell), p, 3, vel, [0] * len(vel), lam, pdg.PDG_FLUX_LBM, fparams, dt, hi=tuple(hi))
+    ob = O.Problem(2, list(ncell), p, vel, [0] * len(vel), 3, lam, 3, fparams, dt, hi=list(hi))
+    return pb, ob
+
+
+def _planes_view(ob):
+    class _C:
+        pass
+    cv = _C()
+    cv.dim, cv.grid_shape = ob.dim, ob.grid_shape()
+    cv.velocities = lambda: (ob.vel.tolist(), None)
+    return cv
+
+
+# (cells x, y), p, kappa = lambda dt'/h, forced segment length, CTA shape.  kappa 0.25 / 0.5 / 1
+# give halos of 12-16 / 16 / 28 rows (<= the segment: segmented); kappa 4 needs > 100 rows and
+# dt' < 0 has no bound (both run unsegmented: the fallback path).
+SEG_CASES = [
+    ((40, 150), 2, 0.25, 24, None),
+    ((70, 200), 2, 1.0, 40, "1,1"),
+    ((33, 130), 1, 0.5, 32, None),
+    ((37, 97), 3, 1.0, 30, "2,2"),
+    ((65, 90), 2, 0.5, 17, "1,1"),
+    ((40, 150), 2, 4.0, 24, None),
+    ((40, 120), 2, -0.05, 24, "1,1"),
+]
+
+
+@pytest.mark.parametrize("ncell,p,kappa,seglen,warps", SEG_CASES, indirect=["seglen", "warps"],
+                         ids=[f"{c[0][0]}x{c[0][1]}-p{c[1]}-k{c[2]}-L{c[3]}-w{c[4]}" for c in SEG_CASES])
+def test_lattice_chain_segments_parity(ncell, p, kappa, seglen, warps):
+    """One T2(dt') and two M2 steps of D2Q9 with the chain cut into segments == the oracle."""
+    h = 1.0 / ncell[0]
+    dtp = kappa * h
+    hi = (1.0, ncell[1] / ncell[0], 1.0)  # square cells: kappa on both axes
+    pb, ob = _d2q9_box(ncell, p, dt=2.0 * dtp if dtp > 0 else 0.5 * h, hi=hi)
+    from paper_1702_00169_b200 import pdg
+    S = pdg.Solver(pb)
+    shape = ob.grid_shape()
+    rng = np.random.default_rng(sum(ncell) + p)
+    f = (1.0 + 0.5 * (rng.random((ob.nv,) + shape) - 0.5)) / ob.nv
+    fb_full = rng.random((ob.nv,) + shape) / ob.nv
+    S.set_state(to_dev(f), to_dev(lattice_planes(_planes_view(ob), fb_full, S.sizes.plane_stride)))
+    S.transport(dtp)
+    got = to_np(S.get_state(), f.shape)
+    fc = ob.grid_to_cells(f)
+    fbc = ob.grid_to_cells(fb_full)
+    O.t2_all(ob, dtp, fc, fbc)
+    assert rel_maxnorm(got, ob.cells_to_grid(fc)) <= TOL_OP
+    S.step(2)
+    got2 = to_np(S.get_state(), f.shape)
+    ref2 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 2)
+    S.destroy()
+    assert rel_maxnorm(got2, ref2) <= TOL_STEP
+
+
+@pytest.mark.parametrize("N", [512, 1024])
+def test_lattice_chain_segments_match_unsegmented(N):
+    """At bench-like sizes the default segmentation (halo from the bound) and the whole-chain sweep
+    agree to the last bits: the truncated trace differs by <= 2^-64 of the true one."""
+    cfg = lbm_config("D2Q9", N, nu=2.0)
+    outs = []
+    for seg in ("0", None):
+        old = os.environ.get("PDG_LATTICE_SEG")
+        if seg is None:
+            os.environ.pop("PDG_LATTICE_SEG", None)
+        else:
+            os.environ["PDG_LATTICE_SEG"] = seg
+        try:
+            S = make_solver(cfg)
+        finally:
+            if old is None:
+                os.environ.pop("PDG_LATTICE_SEG", None)
+            else:
+                os.environ["PDG_LATTICE_SEG"] = old
+        S.set_equilibrium(w0_grid(cfg, device="cuda").reshape(-1))
+        S.step(2)
+        outs.append(S.get_state().clone())
+        S.destroy()
+    err = float((outs[0] - outs[1]).abs().max() / outs[0].abs().max())
+    assert err <= 1e-15, err
