@@ -171,7 +171,8 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     int mf = 1;
     for (int t = 1; t < P.d; ++t) mf *= g.n;
     // boundary traces of up to two sweeps per launch
-    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.rcap * P.Wy * mf : 0;
+    // x traces cross CTAs as tagged 64-bit words (two per double, pdg_lattice.cuh ll_put / ll_take)
+    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.rcap * P.Wy * 2 * mf : 0;
     P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * ((mf + 1) & ~1) : 0;  // even stride
     P.xbuf = (P.xbuf + 1) & ~(size_t)1;  // keep every slice 16-byte aligned
 }
@@ -1537,6 +1538,11 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         c->lat_xbuf = reinterpret_cast<double *>(base + lat_ints_bytes(c->g));
         c->lat_ybuf = c->lat_xbuf + c->g.lat_xbuf;
         c->lat_gtab_base = c->lat_ybuf + c->g.lat_ybuf;
+        // the tagged x-trace words start out empty; every launch's consumers empty them again
+        if (c->g.lat_xbuf && cudaMemsetAsync(c->lat_xbuf, 0, sizeof(double) * c->g.lat_xbuf, c->stream) != cudaSuccess) {
+            pdg_destroy(c);
+            return fail(PDG_E_CUDA, "cannot clear the lattice trace buffers");
+        }
     }
     if (c->g.zslab) {
         c->zcarry = reinterpret_cast<double *>(static_cast<char *>(work_dev) + 256);

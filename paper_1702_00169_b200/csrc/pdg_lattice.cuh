@@ -226,28 +226,78 @@ __device__ __forceinline__ int64_t plane_index(const LatGeom &g, int k, const in
     return ph[1] * g.L[0] + ph[0];
 }
 
-// 2 f^b at the in-face nodes (face axis k, active index t) of the unit with cell/coord ucell[].
+// f^b at in-face node j (face axis K, active index t) of the unit with cell/coord ucell[].
+template <int D, int N, int ACT, int K>
+__device__ __forceinline__ const double *ghost_ptr(const LatParams<D, N, ACT> &P, const LatVel &V, const int (&ucell)[3],
+                                                   int j)
+{
+    using S = LatShape<D, ACT>;
+    constexpr int T = S::t_of(K);
+    const double *pl = P.fb + V.fb_off + (int64_t)K * P.g.plane_stride;
+    const int r = (j % ipow(N, T)) + (j / ipow(N, T)) * ipow(N, T + 1);  // digit T = 0
+    int64_t ph[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if (a == K) continue;
+        const int ta = S::t_of(a);
+        int64_t u = (ta >= 0) ? (int64_t)ucell[a] * N + (r / ipow(N, ta)) % N : (int64_t)ucell[a];
+        if (ta >= 0 && V.sign[a] < 0) u = P.g.L[a] - 1 - u;
+        ph[a] = u;
+    }
+    return pl + plane_index<D>(P.g, K, ph);
+}
+
+// 2 f^b at the in-face nodes of axis K (the ghost trace, reading C4).
 template <int D, int N, int ACT, int K>
 __device__ __forceinline__ void ghost_face(const LatParams<D, N, ACT> &P, const LatVel &V, const int (&ucell)[3],
                                            double (&s)[LatTab<N, LatShape<D, ACT>::DA>::MF])
 {
-    using S = LatShape<D, ACT>;
-    constexpr int MF = LatTab<N, S::DA>::MF;
-    constexpr int T = S::t_of(K);
-    const double *pl = P.fb + V.fb_off + (int64_t)K * P.g.plane_stride;
+    constexpr int MF = LatTab<N, LatShape<D, ACT>::DA>::MF;
+#pragma unroll
+    for (int j = 0; j < MF; ++j) s[j] = 2.0 * *ghost_ptr<D, N, ACT, K>(P, V, ucell, j);
+}
+
+// Tagged trace words (the "LL" idea of NCCL's low-latency protocol): a double crosses CTAs as two
+// 64-bit words, each holding 32 of its bits and a 32-bit tag.  Aligned 64-bit accesses are
+// single-copy atomic, so a consumer that reads the tag in both words holds the value: no fence on
+// the producer, no acquire and no second round trip on the consumer.  The consumer zeroes the
+// words after reading (the buffer is zeroed at pdg_create), so every slot is empty again when the
+// next launch writes it.
+__device__ __forceinline__ void ll_store2(uint64_t *p, uint64_t a, uint64_t b)
+{
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ll_load2(const uint64_t *p, uint64_t &a, uint64_t &b)
+{
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+template <int MF>
+__device__ __forceinline__ void ll_put(uint64_t *slot, const double (&v)[MF], uint32_t tag)
+{
+    const uint64_t t = (uint64_t)tag << 32;
 #pragma unroll
     for (int j = 0; j < MF; ++j) {
-        const int r = (j % ipow(N, T)) + (j / ipow(N, T)) * ipow(N, T + 1);  // digit T = 0
-        int64_t ph[3] = {0, 0, 0};
+        const uint64_t u = (uint64_t)__double_as_longlong(v[j]);
+        ll_store2(slot + 2 * j, (u & 0xffffffffull) | t, (u >> 32) | t);
+    }
+}
+template <int MF>
+__device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_t tag)
+{
+    uint64_t w[2 * MF];
+    for (;;) {
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-            if (a == K) continue;
-            const int ta = S::t_of(a);
-            int64_t u = (ta >= 0) ? (int64_t)ucell[a] * N + (r / ipow(N, ta)) % N : (int64_t)ucell[a];
-            if (ta >= 0 && V.sign[a] < 0) u = P.g.L[a] - 1 - u;
-            ph[a] = u;
-        }
-        s[j] = 2.0 * pl[plane_index<D>(P.g, K, ph)];
+        for (int j = 0; j < MF; ++j) ll_load2(slot + 2 * j, w[2 * j], w[2 * j + 1]);
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 2 * MF; ++k) ok = ok && (uint32_t)(w[k] >> 32) == tag;
+        if (ok) break;
+        __nanosleep(20);
+    }
+#pragma unroll
+    for (int j = 0; j < MF; ++j) {
+        v[j] = __longlong_as_double((long long)((w[2 * j + 1] << 32) | (w[2 * j] & 0xffffffffull)));
+        ll_store2(slot + 2 * j, 0ull, 0ull);
     }
 }
 
@@ -286,6 +336,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #endif
 
     __shared__ double xs[NPASS][2][8][XA ? MF : 1];
+    __shared__ double gxs[8][RING][XA ? MF : 1];  // x inflow ghosts of the first x warp, prefetched per row
     __shared__ int s_task;
     __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
@@ -331,7 +382,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // different batch indices (wy) are independent: each group of Wx skewed x-warps syncs on its
     // own named barrier, and no other CTA reads this task's progress.
     const bool group_sync = !PIPE && g.ngx == 1;
-    const bool publish = (XA && g.ngx > 1) || (PIPE && g.ngy > 1);
+    const bool publish = PIPE && g.ngy > 1;  // y progress (x traces travel as tagged words)
+    uint64_t *const xll = reinterpret_cast<uint64_t *>(P.xbuf);
     // Otherwise (pipe classes, CS = 1) warps sync point to point through shared-memory step
     // counters instead of a CTA-wide barrier: before step t a warp needs its producers (x-1, y-1)
     // and its consumers (x+1, y+1) to have finished step t-1 (the consumers have then read the
@@ -465,6 +517,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
                     cp_async8(dst + q * 32, P.f + ubr + off);
                 }
+                if constexpr (XA) {  // the row's x inflow ghost (first x warp of the first x group)
+                    if (gx == 0 && qx == 0 && lane == 0) {
+                        int uc[3] = {ucell[0], ucell[1], ucell[2]};
+                        uc[CA] = r0 + rr;
+#pragma unroll
+                        for (int j = 0; j < MF; ++j) cp_async8(&gxs[wy][rr % RING][j], ghost_ptr<D, N, ACT, 0>(P, V, uc, j));
+                    }
+                }
             }
             if constexpr (PIPE) {
                 ypf = false;
@@ -556,12 +616,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) & 1][warp - 1][j];
                         } else if (gx > 0) {
-                            if (ps == 0) wait_progress(P.progress + task - 1, r + 1);
-                            const double *xsrc = P.xbuf + ((((int64_t)(task - 1) * g.rcap + r) * NPASS + ps) * g.Wy + wy) * MF;
-#pragma unroll
-                            for (int j = 0; j < MF; ++j) s0[j] = __ldcg(xsrc + j);
+                            // only lane 0 enters the x in-trace into the scan
+                            if (lane == 0)
+                                ll_take<MF>(xll + ((((int64_t)(task - 1) * g.rcap + r) * NPASS + ps) * g.Wy + wy) * 2 * MF, s0,
+                                            (uint32_t)r + 1u);
                         } else if (lane == 0 && valid) {
-                            ghost_face<D, N, ACT, 0>(P, V, ucell, s0);
+#pragma unroll
+                            for (int j = 0; j < MF; ++j) s0[j] = 2.0 * gxs[wy][r % RING][j];
                         }
                     }
                     // x scan: in a[] the zero-inflow x out-traces of the lanes' cells; returns the
@@ -596,12 +657,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         if (lane == 31) {
 #pragma unroll
                             for (int j = 0; j < MF; ++j) xs[ps][t & 1][warp][j] = a[j];
-                            if (qx == g.Wx - 1 && gx < g.ngx - 1) {
-                                double *dst = P.xbuf + ((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wy + wy) * MF;
-#pragma unroll
-                                for (int j = 0; j < MF; ++j) __stcg(dst + j, a[j]);
-                                __threadfence();
-                            }
+                            if (qx == g.Wx - 1 && gx < g.ngx - 1)
+                                ll_put<MF>(xll + ((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wy + wy) * 2 * MF, a,
+                                           (uint32_t)r + 1u);
                         }
                     };
                     PDG_TMARK(2);
