@@ -148,12 +148,13 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     // segments swept concurrently, each starting kHalo rows early from a zero chain trace.  The
     // halo depth comes from a norm bound of the chain operator per launch (lattice_chain_halo:
     // the truncated traces agree with the exact ones to 2^-64); a launch whose bound exceeds the
-    // segment length runs unsegmented.  Planned for the 148 SMs of a B200 at 2 CTAs per SM (the
+    // segment length runs unsegmented.  Planned for the 148 SMs of a B200 at 16 warps per SM (the
     // segments only change how much of the chain one task walks, not the result).
     P.nseg = 1;
     P.seglen = P.nc;
     if (XA && !PIPE && P.cs == 1) {
-        const int base = P.nvel * P.ngx * P.ngy, slots = 148 * 2;
+        // resident CTAs: 16 warps per SM on the FMA path (registers capped for 2 CTAs of 8 warps)
+        const int base = P.nvel * P.ngx * P.ngy, slots = 148 * std::max(1, 16 / (P.Wx * P.Wy));
         int Ls = 0;
         if (const char *e = std::getenv("PDG_LATTICE_SEG")) Ls = std::max(0, std::atoi(e));  // 0: off
         else if (2 * base <= slots && P.nc >= 128) {
