@@ -174,7 +174,7 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     // boundary traces of up to two sweeps per launch
     // x traces cross CTAs as tagged 64-bit words (two per double, pdg_lattice.cuh ll_put / ll_take)
     P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.rcap * P.Wy * 2 * mf : 0;
-    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * ((mf + 1) & ~1) : 0;  // even stride
+    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * 2 * mf : 0;  // tagged words
     P.xbuf = (P.xbuf + 1) & ~(size_t)1;  // keep every slice 16-byte aligned
 }
 
@@ -724,9 +724,10 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
     const size_t smem =
-        sizeof(double) * ((size_t)(threads / 32) * (pdg::LatRing<D>::RING * TB::NB * 32 + (PIPE ? NPASS * 2 * 32 * TB::MF : 0)) +
+        sizeof(double) * ((size_t)(threads / 32) * pdg::LatRing<D>::RING * TB::NB * 32 +
+                          (PIPE ? (size_t)NPASS * 2 * 32 * TB::MF * (CS > 1 ? threads / 32 : threads / 32 - pl.Wx) : 0) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32) +
-                          (PIPE ? (size_t)NPASS * pl.Wx * 32 * ((TB::MF + 1) & ~1) : 0));
+                          (PIPE ? (size_t)NPASS * pl.Wx * 32 * 2 * TB::MF : 0));
     // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy
     auto kern = pdg::lattice_sweep_kernel<D, N, ACT, NPASS, CS>;
     const void *kfn = reinterpret_cast<const void *>(kern);
@@ -1539,8 +1540,9 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
         c->lat_xbuf = reinterpret_cast<double *>(base + lat_ints_bytes(c->g));
         c->lat_ybuf = c->lat_xbuf + c->g.lat_xbuf;
         c->lat_gtab_base = c->lat_ybuf + c->g.lat_ybuf;
-        // the tagged x-trace words start out empty; every launch's consumers empty them again
-        if (c->g.lat_xbuf && cudaMemsetAsync(c->lat_xbuf, 0, sizeof(double) * c->g.lat_xbuf, c->stream) != cudaSuccess) {
+        // the tagged x/y-trace words start out empty; every launch's consumers empty them again
+        if ((c->g.lat_xbuf + c->g.lat_ybuf) &&
+            cudaMemsetAsync(c->lat_xbuf, 0, sizeof(double) * (c->g.lat_xbuf + c->g.lat_ybuf), c->stream) != cudaSuccess) {
             pdg_destroy(c);
             return fail(PDG_E_CUDA, "cannot clear the lattice trace buffers");
         }

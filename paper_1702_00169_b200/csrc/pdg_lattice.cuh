@@ -121,12 +121,12 @@ struct LatParams {
     using S = LatShape<D, ACT>;
     double *f;
     const double *fb;
-    int *ticket;     // [0]; progress counters follow: progress[task] = rows published
+    int *ticket;     // [0]; progress counters follow: progress[task] = rows published (tensor-path y traces)
     int *progress;
     int *hdone;      // [task]: 1 once the segment has read its halo rows (their old values)
-    double *xbuf;    // [task][row][Wy][MF]       x out-traces at CTA boundaries
-    double *ybuf;    // [task][row][pass][Wx][32][MFP] y out-traces at CTA boundaries (MFP = MF rounded up to
-                     // an even count: 16-byte cp.async.cg copies)
+    double *xbuf;    // [task][row][pass][Wy][2 MF] tagged x out-trace words at CTA boundaries
+    double *ybuf;    // [task][row][pass][Wx][32][2 MF] tagged y out-trace words at CTA boundaries (FMA
+                     // path; the tensor path stores plain doubles with an MF rounded up to even stride)
     LatGeom g;
     LatVel v[kLatMaxVel];
     typename LatTabSel<N, S::DA>::type tab;
@@ -189,9 +189,12 @@ struct LatMma {
     static constexpr int KE = NB + (S::PIPE ? 2 : 1) * MF;      // [f_old; chain in-trace; pipe in-trace]
     static constexpr int KS = (KE + 3) / 4;                     // k-steps of the first product
     static constexpr int KSX = (MF + 3) / 4;                    // k-steps of Q_x s_x
+    // row stride of the A operand [M | Q_chain | Q_pipe] in shared memory: a multiple of 16
+    // doubles would put the 8 rows of a fragment (lane / 4) on one bank pair, so pad by 4
+    static constexpr int SA = KS * 4 + (((KS * 4) % 16 == 0) ? 4 : 0);
     static constexpr size_t smem_doubles(int nwarps)
     {
-        return USE ? (size_t)nwarps * NB * 32 + (size_t)MT * 8 * (KS + KSX) * 4 : 0;
+        return USE ? (size_t)nwarps * NB * 32 + (size_t)MT * 8 * (SA + KSX * 4) : 0;
     }
 };
 
@@ -282,6 +285,25 @@ __device__ __forceinline__ void ll_put(uint64_t *slot, const double (&v)[MF], ui
     }
 }
 template <int MF>
+__device__ __forceinline__ void ll_clear(uint64_t *slot)
+{
+#pragma unroll
+    for (int j = 0; j < MF; ++j) ll_store2(slot + 2 * j, 0ull, 0ull);
+}
+// decode tagged words already copied (e.g. into shared memory); false if any tag is not `tag`
+template <int MF>
+__device__ __forceinline__ bool ll_decode(const uint64_t *w, double (&v)[MF], uint32_t tag)
+{
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < MF; ++j) {
+        const uint64_t a = w[2 * j], b = w[2 * j + 1];
+        ok = ok && (uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag;
+        v[j] = __longlong_as_double((long long)((b << 32) | (a & 0xffffffffull)));
+    }
+    return ok;
+}
+template <int MF>
 __device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_t tag)
 {
     uint64_t w[2 * MF];
@@ -324,11 +346,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     using MMA = LatMma<D, N, ACT>;
     constexpr bool USE_MMA = MMA::USE;
     constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
-    constexpr int MFP = (MF + 1) & ~1;  // per-lane stride of the global y traces (16-byte multiple)
     // rows prefetched ahead with cp.async: 2-D diagonals are latency-bound (short rows, one warp
     // per SM sub-partition), so they look three rows ahead; 3-D classes one row
     constexpr int PFA = LatRing<D>::PFA, RING = LatRing<D>::RING;
     static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
+    // [row][32 units] shared buffers (row buffers, staging): the tensor path XOR-swizzles the unit
+    // index with 4 (row mod 4), so the four rows of a DMMA B fragment (lane % 4) and the eight
+    // accumulator rows of a spill fall on different bank pairs
+    auto ro = [](int row, int u) -> int { return row * 32 + (USE_MMA ? (u ^ ((row & 3) << 2)) : u); };
     const unsigned FULL = 0xffffffffu;
 #ifdef PDG_LAT_TIMING
     long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -341,29 +366,33 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
     // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
-    // math), then the y hand-over buffers [pass][2][warps][32][MF] (PIPE)
+    // math), then the y hand-over buffers [pass][2][nys warps][32][MF] (PIPE)
     extern __shared__ double sfo[];  // [warp][RING][NB][32]
     const int nwarps = blockDim.x >> 5;
     double *ysb = sfo + (size_t)nwarps * RING * NB * 32;
+    // y hand-over slots only for warps with a reader in this CTA (all warps with clusters: the next
+    // CTA of the cluster reads the last pipe warps through DSMEM)
+    const int nys = (CS > 1) ? nwarps : nwarps - P.g.Wx;
     auto YS = [&](int ps, int buf, int w, int l) -> double * {
-        return ysb + ((((size_t)ps * 2 + buf) * nwarps + w) * 32 + l) * MF;
+        return ysb + ((((size_t)ps * 2 + buf) * nys + w) * 32 + l) * MF;
     };
     // (tensor path) per-warp staging rows [NB][32], then the A operands [M|Qc|Qp] and Qx
-    double *stg_base = ysb + (PIPE ? (size_t)NPASS * 2 * nwarps * 32 * MF : 0);
+    double *stg_base = ysb + (PIPE ? (size_t)NPASS * 2 * nys * 32 * MF : 0);
     double *sA = stg_base + (USE_MMA ? (size_t)nwarps * NB * 32 : 0);
-    double *sAx = sA + (size_t)MT * 8 * KS * 4;
-    // (pipe classes) y traces of the previous CTA prefetched for the next row: [pass][Wx][32][MFP]
+    double *sAx = sA + (size_t)MT * 8 * MMA::SA;
+    // (pipe classes) tagged y-trace words of the previous CTA prefetched for the next row: [pass][Wx][32][2 MF]
     double *spy = USE_MMA ? sAx + (size_t)MT * 8 * KSX * 4 : stg_base;
     if constexpr (USE_MMA) {
         for (int i = threadIdx.x; i < MT * 8 * KS * 4; i += blockDim.x) {
             const int q = i / (KS * 4), k = i % (KS * 4);
+            double &dstA = sA[q * MMA::SA + k];
             double v = 0.0;
             if (q < NB) {
                 if (k < NB) v = P.tab.M[k * NB + q];
                 else if (k < NB + MF) v = P.tab.Q[TC][(k - NB) * NB + q];
                 else if (PIPE && k < KE) v = P.tab.Q[TY][(k - NB - MF) * NB + q];
             }
-            sA[i] = v;
+            dstA = v;
         }
         for (int i = threadIdx.x; i < MT * 8 * KSX * 4; i += blockDim.x) {
             const int q = i / (KSX * 4), k = i % (KSX * 4);
@@ -382,8 +411,18 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // different batch indices (wy) are independent: each group of Wx skewed x-warps syncs on its
     // own named barrier, and no other CTA reads this task's progress.
     const bool group_sync = !PIPE && g.ngx == 1;
-    const bool publish = PIPE && g.ngy > 1;  // y progress (x traces travel as tagged words)
+    // y traces across CTAs: tagged words on the FMA path; the tensor path (body diagonals) keeps
+    // plain doubles published with a fence and a per-task row-progress counter — measured faster
+    // there (its heavier rows hide the fence; the tagged words cost 1.8x the hand-over traffic)
+    constexpr bool YLL = !USE_MMA;
+    constexpr int MFP = (MF + 1) & ~1;  // per-lane stride of the plain y traces (16-byte multiple)
+    const bool publish = !YLL && PIPE && g.ngy > 1;  // row progress (x traces travel as tagged words)
     uint64_t *const xll = reinterpret_cast<uint64_t *>(P.xbuf);
+    uint64_t *const yll = reinterpret_cast<uint64_t *>(P.ybuf);
+    // tagged y-trace words of (task, row, pass) for this lane: [task][row][pass][Wx][32][2 MF]
+    auto ylslot = [&](int tk, int row, int ps) -> int64_t {
+        return (((((int64_t)tk * g.rcap + row) * NPASS + ps) * g.Wx + qx) * 32 + lane) * 2 * MF;
+    };
     // Otherwise (pipe classes, CS = 1) warps sync point to point through shared-memory step
     // counters instead of a CTA-wide barrier: before step t a warp needs its producers (x-1, y-1)
     // and its consumers (x+1, y+1) to have finished step t-1 (the consumers have then read the
@@ -509,13 +548,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         auto prefetch = [&](int rr) {
             if (valid && rr < nrow) {
                 const int64_t ubr = ibase + cbase + (int64_t)(r0 + rr) * cstep;
-                double *dst = wbuf + (rr % RING) * NB * 32 + lane;
+                double *dst = wbuf + (rr % RING) * NB * 32;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) {
                     int64_t off = 0;
 #pragma unroll
                     for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
-                    cp_async8(dst + q * 32, P.f + ubr + off);
+                    cp_async8(dst + ro(q, lane), P.f + ubr + off);
                 }
                 if constexpr (XA) {  // the row's x inflow ghost (first x warp of the first x group)
                     if (gx == 0 && qx == 0 && lane == 0) {
@@ -527,12 +566,24 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 }
             }
             if constexpr (PIPE) {
+                // the previous pipe group's tagged y-trace words of row rr, copied whether or not they
+                // have arrived: the tags tell at the use (normally they have: the producer runs ahead)
                 ypf = false;
-                if (ycons && rr < nrow && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
+                if (YLL && ycons && rr < nrow) {
 #pragma unroll
                     for (int ps = 0; ps < NPASS; ++ps) {
-                        const double *ysrc =
-                            P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                        const uint64_t *ysrc = yll + ylslot(task - per_gy, rr, ps);
+                        double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * 2 * MF;
+#pragma unroll
+                        for (int h = 0; h < 2 * MF; h += 2)
+                            cp_async16_cg(yd + h, reinterpret_cast<const double *>(ysrc + h));
+                    }
+                    ypf = true;
+                } else if (!YLL && ycons && rr < nrow && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
+                    // plain traces: copied only once published (the producer normally runs ahead)
+#pragma unroll
+                    for (int ps = 0; ps < NPASS; ++ps) {
+                        const double *ysrc = P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
                         double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                         for (int h = 0; h < MFP; h += 2) cp_async16_cg(yd + h, ysrc + h);
@@ -553,31 +604,23 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 const int64_t ub = ibase + cbase + (int64_t)(r0 + r) * cstep;
                 if (r == 0)
                     for (int k = 0; k < PFA; ++k) prefetch(k);
-                double sy_pf[(PIPE ? NPASS : 1)][PIPE ? MF : 1];
-                bool have_sy = false;
-                if constexpr (PIPE) {  // PFA == 1: the y-trace slot is read before the next prefetch
-                    cp_async_wait<0>();  // row r (and its prefetched y traces) have landed
-                    have_sy = ypf;
-                    if (have_sy) {
-#pragma unroll
-                        for (int ps = 0; ps < NPASS; ++ps)
-#pragma unroll
-                            for (int j = 0; j < MF; ++j) sy_pf[ps][j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
-                    }
-                    prefetch(r + 1);  // overlaps the rest of the row
+                if constexpr (PIPE) {
+                    // PFA == 1: row r (and its prefetched y-trace words) have landed; the next row's
+                    // prefetch is issued once the y-trace words have been read (below)
+                    cp_async_wait<0>();
                 } else {
                     prefetch(r + PFA);
                     cp_async_wait<PFA>();  // row r has landed, rows r+1 .. r+PFA may be in flight
                 }
                 PDG_TMARK(1);
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
-                const double *src = wbuf + (r % RING) * NB * 32 + lane;
+                const double *src = wbuf + (r % RING) * NB * 32;
                 double fprev[NB];  // input of the second sweep (output of the first)
                 double fn[NB];
 #pragma unroll
                 for (int ps = 0; ps < NPASS; ++ps) {
                     // f_old of this sweep: the row buffer (first) or the first sweep's result
-                    auto fold = [&](int c) -> double { return (ps == 0) ? src[c * 32] : fprev[c]; };
+                    auto fold = [&](int c) -> double { return (ps == 0) ? src[ro(c, lane)] : fprev[c]; };
                     // pipe (y) in-trace
                     double sy[PIPE ? MF : 1];
                     if constexpr (PIPE) {
@@ -591,13 +634,19 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int j = 0; j < MF; ++j) sy[j] = rsy[j];
                         } else if (gy > 0) {
-                            if (have_sy) {
+                            if constexpr (YLL) {
+                                uint64_t *ysl = yll + ylslot(task - per_gy, r, ps);
+                                const uint64_t *w = reinterpret_cast<const uint64_t *>(spy) + (((size_t)ps * g.Wx + qx) * 32 + lane) * 2 * MF;
+                                if (ypf && ll_decode<MF>(w, sy, (uint32_t)r + 1u))
+                                    ll_clear<MF>(ysl);  // empty the slot for the next launch
+                                else
+                                    ll_take<MF>(ysl, sy, (uint32_t)r + 1u);
+                            } else if (ypf) {
 #pragma unroll
-                                for (int j = 0; j < MF; ++j) sy[j] = sy_pf[ps][j];
+                                for (int j = 0; j < MF; ++j) sy[j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
                             } else {
                                 if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
-                                const double *ysrc =
-                                    P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                                const double *ysrc = P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
                             }
@@ -606,6 +655,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             for (int j = 0; j < MF; ++j) sy[j] = 0.0;
                             if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
                         }
+                        if (ps == NPASS - 1) prefetch(r + 1);  // overlaps the rest of the row
                     }
                     // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
                     double s0[XA ? MF : 1];
@@ -672,10 +722,10 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         const double *fsrc = wbuf + (r % RING) * NB * 32;
                         double *stg = stg_base + (size_t)warp * NB * 32;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sc[ps][j];
+                        for (int j = 0; j < MF; ++j) stg[ro(j, lane)] = sc[ps][j];
                         if constexpr (PIPE) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) stg[(MF + j) * 32 + lane] = sy[j];
+                            for (int j = 0; j < MF; ++j) stg[ro(MF + j, lane)] = sy[j];
                         }
                         __syncwarp();
                         double acc[MT][4][2];
@@ -691,13 +741,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int nt = 0; nt < 4; ++nt) {
                                 const int u = nt * 8 + gq;
-                                if (ks * 4 + 3 < NB) b[nt] = fsrc[k * 32 + u];
-                                else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[(k - NB) * 32 + u];
-                                else b[nt] = (k < NB) ? fsrc[k * 32 + u] : ((k < KE) ? stg[(k - NB) * 32 + u] : 0.0);
+                                if (ks * 4 + 3 < NB) b[nt] = fsrc[ro(k, u)];
+                                else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[ro(k - NB, u)];
+                                else b[nt] = (k < NB) ? fsrc[ro(k, u)] : ((k < KE) ? stg[ro(k - NB, u)] : 0.0);
                             }
 #pragma unroll
                             for (int mt = 0; mt < MT; ++mt) {
-                                const double av = sA[(mt * 8 + gq) * (KS * 4) + k];
+                                const double av = sA[(mt * 8 + gq) * MMA::SA + k];
 #pragma unroll
                                 for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av, b[nt]);
                             }
@@ -710,8 +760,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                                 for (int nt = 0; nt < 4; ++nt) {
                                     const int q = mt * 8 + gq;
                                     if (q < NB) {
-                                        stg[q * 32 + nt * 8 + 2 * tq] = acc[mt][nt][0];
-                                        stg[q * 32 + nt * 8 + 2 * tq + 1] = acc[mt][nt][1];
+                                        stg[ro(q, nt * 8 + 2 * tq)] = acc[mt][nt][0];
+                                        stg[ro(q, nt * 8 + 2 * tq + 1)] = acc[mt][nt][1];
                                     }
                                 }
                             __syncwarp();
@@ -722,19 +772,19 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             double a[MF], sin_[MF];
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
-                                a[j] = valid ? fsrc[(j * N + N - 1) * 32 + lane] + stg[(j * N + N - 1) * 32 + lane] : 0.0;
+                                a[j] = valid ? fsrc[ro(j * N + N - 1, lane)] + stg[ro(j * N + N - 1, lane)] : 0.0;
                             xscan(a, sin_);
                             PDG_TMARK(4);
                             __syncwarp();
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) stg[j * 32 + lane] = sin_[j];
+                            for (int j = 0; j < MF; ++j) stg[ro(j, lane)] = sin_[j];
                             __syncwarp();
 #pragma unroll
                             for (int ks = 0; ks < KSX; ++ks) {
                                 const int k = ks * 4 + tq;
                                 double b[4];
 #pragma unroll
-                                for (int nt = 0; nt < 4; ++nt) b[nt] = (k < MF) ? stg[k * 32 + nt * 8 + gq] : 0.0;
+                                for (int nt = 0; nt < 4; ++nt) b[nt] = (k < MF) ? stg[ro(k, nt * 8 + gq)] : 0.0;
 #pragma unroll
                                 for (int mt = 0; mt < MT; ++mt) {
                                     const double av = sAx[(mt * 8 + gq) * (KSX * 4) + k];
@@ -745,7 +795,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             spill();
                         }
 #pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = stg[q * 32 + lane];
+                        for (int q = 0; q < NB; ++q) fn[q] = stg[ro(q, lane)];
                     } else {
                         // FMA pipe: f_new (without the x inflow) = M f_old + Q_chain s_chain + Q_pipe s_pipe,
                         // streamed column by column: NB independent accumulators
@@ -796,14 +846,19 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             const int q = (j % ipow(N, TY)) + (j / ipow(N, TY)) * ipow(N, TY + 1) + (N - 1) * ipow(N, TY);
                             ty[j] = fold(q) + fn[q];
                         }
+                        if (warp < nys) {
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
+                            for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
+                        }
                         if (wy == g.Wy - 1 && crank == CS - 1 && gy < g.ngy - 1) {
-                            double *dst =
-                                P.ybuf + (((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                            if constexpr (YLL) {
+                                ll_put<MF>(yll + ylslot(task, r, ps), ty, (uint32_t)r + 1u);
+                            } else {
+                                double *dst = P.ybuf + (((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
-                            __threadfence();
+                                for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
+                                __threadfence();
+                            }
                         }
                     }
 #pragma unroll
