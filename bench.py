@@ -330,8 +330,10 @@ def run_product(args, cfg):
         step_roof = None
         if cfg.lattice:
             # whole-step HBM roofline of a lattice workload: per node and velocity, 16 B for the
-            # relaxation plus 16 B per transport launch (axis velocities and 3-D two-axis classes:
-            # both half-steps in one launch; body diagonals and 2-D diagonals: one launch each)
+            # relaxation plus 16 B per pass over f that the path needs at least (axis velocities and
+            # 3-D two-axis classes: both half-steps can share one pass; body diagonals and 2-D
+            # diagonals: one pass each).  Algorithmic bytes: the 3-D two-axis classes now run one
+            # launch per half-step (measured faster), which moves more than this.
             vel, _ = cfg.velocities()
             b = 0.0
             for v in vel:

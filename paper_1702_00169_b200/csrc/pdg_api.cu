@@ -788,7 +788,13 @@ pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_
     if (!B) return fail(PDG_E_INVALID_ARGUMENT, "singular lattice block for this dt");
     const int D = c->g.dim, n = c->g.n, a = pl.act;
     // (2-D grids are latency-bound: one sweep per launch keeps the per-row chain short)
-    const bool fused = (npass == 2 && popcount3(a) < 3 && D == 3);
+    // PDG_LATTICE_FUSE: bit mask over the active-axis masks whose two sweeps share one launch.
+    // Default none: with the tagged hand-over the single-sweep launches are fast enough that the
+    // fused variant (twice the per-row chain, register spills) loses (D3Q19 128^3: 8.93 ms per
+    // step fused, 8.24 ms unfused; tools/gpu/fuse.sh)
+    int fuse_mask = 0;
+    if (const char *e = std::getenv("PDG_LATTICE_FUSE")) fuse_mask = std::atoi(e);
+    const bool fused = (npass == 2 && popcount3(a) < 3 && D == 3 && ((fuse_mask >> a) & 1));
     for (int q = 0; q < (fused ? 1 : npass); ++q) {
         const int e = prof_begin(c, st);
         pdg_status s = PDG_E_UNSUPPORTED;

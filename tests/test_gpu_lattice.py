@@ -507,3 +507,30 @@ def test_lattice_chain_segments_match_unsegmented(N):
         S.destroy()
     err = float((outs[0] - outs[1]).abs().max() / outs[0].abs().max())
     assert err <= 1e-15, err
+
+
+@pytest.mark.parametrize("lat,N,p", [("D3Q19", 6, 2), ("D3Q27", 5, 1), ("D3Q19", 4, 3), ("D3Q27", 33, 2)])
+def test_lattice_fused_two_sweeps_parity(lat, N, p):
+    """PDG_LATTICE_FUSE=104 (axis masks 3, 5, 6): the 3-D two-axis classes apply the trailing and the
+    leading T2(dt/2) of consecutive steps in one launch (NPASS = 2, off by default) == the oracle."""
+    old = os.environ.get("PDG_LATTICE_FUSE")
+    os.environ["PDG_LATTICE_FUSE"] = "104"
+    try:
+        from paper_1702_00169_b200 import pdg
+        cfg = lbm_config(lat, N, p=p, steps=3)
+        w0 = w0_grid(cfg)
+        wb = wb_grid(cfg, w0)
+        S = make_solver(cfg)
+        S.set_equilibrium(w0.reshape(-1).cuda(), wb.reshape(-1).cuda())
+        S.step(cfg.steps)
+        got = to_np(S.get_state(), (cfg.nv,) + cfg.grid_shape)
+        S.destroy()
+    finally:
+        if old is None:
+            os.environ.pop("PDG_LATTICE_FUSE", None)
+        else:
+            os.environ["PDG_LATTICE_FUSE"] = old
+    pb = oracle_problem(cfg)
+    f0, fb = O.initial_data(pb, w0.numpy(), wb.numpy())
+    ref = O.scheme_run(pb, f0, fb, cfg.steps, "m2")
+    assert rel_maxnorm(got, ref) <= TOL_STEP
