@@ -691,8 +691,10 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     // into a device slot of the work buffer, uploaded once per (class, dt')
     std::vector<double> host(sizeof(TB) / sizeof(double), 0.0);
     TB &T = *reinterpret_cast<TB *>(host.data());
+    // the sweeps multiply A^{-1} by the rhs 2 f_old + (kappa_t/omega_0) E_in^(t) s_t (pdg_lattice.cuh)
     for (int q = 0; q < NB; ++q)
-        for (int cc = 0; cc < NB; ++cc) T.M[cc * NB + q] = (double)B.M[(size_t)q * NB + cc];
+        for (int cc = 0; cc < NB; ++cc) T.M[cc * NB + q] = (double)B.Ainv[(size_t)q * NB + cc];
+    for (int t = 0; t < 3; ++t) P.g.kw[t] = (t < DA) ? (double)(B.kappa[t] / B.w0) : 0.0;
     for (int t = 0; t < DA; ++t)
         for (int q = 0; q < NB; ++q)
             for (int j = 0; j < MF; ++j) T.Q[t][j * NB + q] = (double)B.Q[((size_t)t * NB + q) * MF + j];

@@ -68,7 +68,7 @@ struct LatTab {
     static constexpr int MF = NB / N;
     // stored column-major ([column][row]): the kernels stream one column at a time into NB
     // independent accumulators, so consecutive rows are adjacent (LDCU.128 loads two at once)
-    double M[NB * NB];      // A^{-1} (I + sum_t kappa_t G^(t)),                  M[c * NB + q]
+    double M[NB * NB];      // A^{-1} (applied to the rhs 2 f_old + in-trace injections), M[c * NB + q]
     double Q[DA][NB * MF];  // A^{-1} E_in^(t) kappa_t / omega_0 (in-traces of axis t), Q[t][j * NB + q]
     double Bp[5][MF * MF];  // Bx^(2^j), Bx = rows of Q[0] on the x-out face,     Bp[s][j * MF + i]
 };
@@ -114,6 +114,7 @@ struct LatGeom {
     int32_t seglen;      // chain rows stored by one segment
     int32_t halo;        // rows a segment sweeps ahead of its first stored row (from a zero chain trace)
     int32_t rcap;        // chain rows per task in the trace buffers
+    double kw[3];        // kappa_t / omega_0 per active axis (tensor path: in-trace injection into the rhs)
 };
 
 template <int D, int N, int ACT>
@@ -186,7 +187,9 @@ struct LatMma {
     static constexpr bool USE = (S::DA == 3);
 #endif
     static constexpr int MT = (NB + 7) / 8;                     // 8-row tiles of the block
-    static constexpr int KE = NB + (S::PIPE ? 2 : 1) * MF;      // [f_old; chain in-trace; pipe in-trace]
+    // the first product is A^{-1} r with the rhs r = 2 f_old + sum_t (kappa_t/omega_0) E_in^(t) s_t of
+    // the chain and pipe in-traces (M = A^{-1}(2I - A) = 2 A^{-1} - I, Q_t = A^{-1} E_in^(t) kappa_t/omega_0)
+    static constexpr int KE = NB;
     static constexpr int KS = (KE + 3) / 4;                     // k-steps of the first product
     static constexpr int KSX = (MF + 3) / 4;                    // k-steps of Q_x s_x
     // row stride of the A operand [M | Q_chain | Q_pipe] in shared memory: a multiple of 16
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     constexpr int TY = S::T1;
     using MMA = LatMma<D, N, ACT>;
     constexpr bool USE_MMA = MMA::USE;
-    constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX, KE = MMA::KE;
+    constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX;
     // rows prefetched ahead with cp.async: 2-D diagonals are latency-bound (short rows, one warp
     // per SM sub-partition), so they look three rows ahead; 3-D classes one row
     constexpr int PFA = LatRing<D>::PFA, RING = LatRing<D>::RING;
@@ -387,11 +390,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             const int q = i / (KS * 4), k = i % (KS * 4);
             double &dstA = sA[q * MMA::SA + k];
             double v = 0.0;
-            if (q < NB) {
-                if (k < NB) v = P.tab.M[k * NB + q];
-                else if (k < NB + MF) v = P.tab.Q[TC][(k - NB) * NB + q];
-                else if (PIPE && k < KE) v = P.tab.Q[TY][(k - NB - MF) * NB + q];
-            }
+            if (q < NB && k < NB) v = P.tab.M[k * NB + q];  // the tensor path's M slot holds A^{-1}
             dstA = v;
         }
         for (int i = threadIdx.x; i < MT * 8 * KSX * 4; i += blockDim.x) {
@@ -715,17 +714,23 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     PDG_TMARK(2);
                     if constexpr (USE_MMA) {
                         // fp64 tensor cores (DMMA 8x8x4): the warp's 32 units are the N dimension.
-                        //   F0 = [M | Q_chain | Q_pipe] [F_old; S_chain; S_pipe]     (NB x K) (K x 32)
-                        //   F  = F0 + Q_x S_x_in                                     after the x scan
-                        // B operands come from shared memory: F_old from the cp.async row buffer, the
-                        // in-traces from the warp's staging rows; A operands from the CTA's tables.
+                        //   R  = 2 F_old + (kappa_c/omega_0) E_c S_chain + (kappa_p/omega_0) E_p S_pipe
+                        //   F0 = A^{-1} R          (NB x NB) (NB x 32)  = F_old + f_new without x inflow
+                        //   F  = F0 + Q_x S_x_in   after the x scan     = F_old + f_new
+                        // F0 and F are the old + new traces on the out-faces; f_new = F - F_old.  B
+                        // operands from the warp's staging rows (R, then S_x_in), A from the CTA's tables.
                         const double *fsrc = wbuf + (r % RING) * NB * 32;
                         double *stg = stg_base + (size_t)warp * NB * 32;
 #pragma unroll
-                        for (int j = 0; j < MF; ++j) stg[ro(j, lane)] = sc[ps][j];
-                        if constexpr (PIPE) {
-#pragma unroll
-                            for (int j = 0; j < MF; ++j) stg[ro(MF + j, lane)] = sy[j];
+                        for (int q = 0; q < NB; ++q) {
+                            double v = 2.0 * fsrc[ro(q, lane)];
+                            if ((q / ipow(N, TC)) % N == 0)  // chain in-face node
+                                v = fma(g.kw[TC], sc[ps][(q % ipow(N, TC)) + (q / ipow(N, TC + 1)) * ipow(N, TC)], v);
+                            if constexpr (PIPE) {
+                                if ((q / ipow(N, TY)) % N == 0)  // pipe in-face node
+                                    v = fma(g.kw[TY], sy[(q % ipow(N, TY)) + (q / ipow(N, TY + 1)) * ipow(N, TY)], v);
+                            }
+                            stg[ro(q, lane)] = v;
                         }
                         __syncwarp();
                         double acc[MT][4][2];
@@ -741,9 +746,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                             for (int nt = 0; nt < 4; ++nt) {
                                 const int u = nt * 8 + gq;
-                                if (ks * 4 + 3 < NB) b[nt] = fsrc[ro(k, u)];
-                                else if (ks * 4 >= NB && ks * 4 + 3 < KE) b[nt] = stg[ro(k - NB, u)];
-                                else b[nt] = (k < NB) ? fsrc[ro(k, u)] : ((k < KE) ? stg[ro(k - NB, u)] : 0.0);
+                                b[nt] = (ks * 4 + 3 < NB || k < NB) ? stg[ro(k, u)] : 0.0;
                             }
 #pragma unroll
                             for (int mt = 0; mt < MT; ++mt) {
@@ -772,7 +775,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             double a[MF], sin_[MF];
 #pragma unroll
                             for (int j = 0; j < MF; ++j)
-                                a[j] = valid ? fsrc[ro(j * N + N - 1, lane)] + stg[ro(j * N + N - 1, lane)] : 0.0;
+                                a[j] = valid ? stg[ro(j * N + N - 1, lane)] : 0.0;  // old + new, zero x inflow
                             xscan(a, sin_);
                             PDG_TMARK(4);
                             __syncwarp();
@@ -795,36 +798,37 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             spill();
                         }
 #pragma unroll
-                        for (int q = 0; q < NB; ++q) fn[q] = stg[ro(q, lane)];
+                        for (int q = 0; q < NB; ++q) fn[q] = stg[ro(q, lane)] - fsrc[ro(q, lane)];
                     } else {
-                        // FMA pipe: f_new (without the x inflow) = M f_old + Q_chain s_chain + Q_pipe s_pipe,
-                        // streamed column by column: NB independent accumulators
+                        // FMA pipe, same algebra as the tensor path: F0 = A^{-1} R with the rhs
+                        // R = 2 f_old + (kappa_c/omega_0) E_c s_chain (+ pipe), streamed column by column
+                        // into NB independent accumulators; F = F0 + Q_x s_x_in; f_new = F - f_old
+                        auto rhs = [&](int c) -> double {
+                            double v = 2.0 * fold(c);
+                            if ((c / ipow(N, TC)) % N == 0)  // chain in-face node
+                                v = fma(g.kw[TC], sc[ps][(c % ipow(N, TC)) + (c / ipow(N, TC + 1)) * ipow(N, TC)], v);
+                            if constexpr (PIPE) {
+                                if ((c / ipow(N, TY)) % N == 0)  // pipe in-face node
+                                    v = fma(g.kw[TY], sy[(c % ipow(N, TY)) + (c / ipow(N, TY + 1)) * ipow(N, TY)], v);
+                            }
+                            return v;
+                        };
                         {
-                            const double f0v = fold(0);
+                            const double r0v = rhs(0);
 #pragma unroll
-                            for (int q = 0; q < NB; ++q) fn[q] = P.tab.M[q] * f0v;
+                            for (int q = 0; q < NB; ++q) fn[q] = P.tab.M[q] * r0v;
                         }
 #pragma unroll
                         for (int c = 1; c < NB; ++c) {
-                            const double fc = fold(c);
+                            const double rc = rhs(c);
 #pragma unroll
-                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.M[c * NB + q], fc, fn[q]);
-                        }
-#pragma unroll
-                        for (int j = 0; j < MF; ++j)
-#pragma unroll
-                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TC][j * NB + q], sc[ps][j], fn[q]);
-                        if constexpr (PIPE) {
-#pragma unroll
-                            for (int j = 0; j < MF; ++j)
-#pragma unroll
-                                for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[TY][j * NB + q], sy[j], fn[q]);
+                            for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.M[c * NB + q], rc, fn[q]);
                         }
                         PDG_TMARK(3);
                         if constexpr (XA) {
                             double a[MF], sin_[MF];
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) a[j] = valid ? fold(j * N + N - 1) + fn[j * N + N - 1] : 0.0;
+                            for (int j = 0; j < MF; ++j) a[j] = valid ? fn[j * N + N - 1] : 0.0;  // old + new, zero x inflow
                             xscan(a, sin_);
                             PDG_TMARK(4);
 #pragma unroll
@@ -832,6 +836,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                                 for (int q = 0; q < NB; ++q) fn[q] = fma(P.tab.Q[0][j * NB + q], sin_[j], fn[q]);
                         }
+#pragma unroll
+                        for (int q = 0; q < NB; ++q) fn[q] -= fold(q);
                     }
                     // chain out-trace -> next row (registers)
 #pragma unroll
