@@ -534,3 +534,38 @@ def test_lattice_fused_two_sweeps_parity(lat, N, p):
     f0, fb = O.initial_data(pb, w0.numpy(), wb.numpy())
     ref = O.scheme_run(pb, f0, fb, cfg.steps, "m2")
     assert rel_maxnorm(got, ref) <= TOL_STEP
+
+
+@pytest.mark.parametrize("lat,N,warps", [("D2Q9", 1024, None), ("D2Q9", 300, "1,1"), ("D3Q27", 48, None),
+                                         ("D3Q15", 40, "2,2")], indirect=["warps"])
+def test_lattice_sweeps_bitwise_deterministic(lat, N, warps):
+    """The cross-CTA hand-overs (tagged x/y words, fenced y traces, segment halo flags) are races if
+    wrong: a stale or torn trace changes the result.  Tasks are claimed dynamically, so repeated
+    launches exercise different CTA interleavings; every repeat must be bit-identical, including
+    replays of a captured CUDA graph (the consumers empty the tagged slots for the next launch)."""
+    cfg = lbm_config(lat, N, nu=2.0)
+    S = make_solver(cfg)
+    w0 = w0_grid(cfg, device="cuda").reshape(-1)
+    outs = []
+    for _ in range(3):
+        S.set_equilibrium(w0)
+        S.step(2)
+        outs.append(S.get_state().clone())
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        S2 = make_solver(cfg, stream=st.cuda_stream)
+        S2.set_equilibrium(w0)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            S2.step(2)
+        for _ in range(2):
+            S2.set_equilibrium(w0)
+            g.replay()
+            st.synchronize()
+            outs.append(S2.get_state().clone())
+        st.synchronize()
+    S.destroy()
+    S2.destroy()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
