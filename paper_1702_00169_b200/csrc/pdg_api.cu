@@ -111,8 +111,9 @@ void plan_lattice(const Geometry &g, LatPlan &P)
         // x carries a dependency: the CTA's x-warps are skewed, keep them few enough that the
         // grid still has tasks for every SM (2-D grids: one warp per CTA along x)
         // (body diagonals, x and pipe both active: 2 x-warps by 4 pipe warps measured best, D3Q15
-        // 128^3 12.32 -> 11.82 ms per step against 4 x 2; tools/gpu/bdshape.sh)
-        P.Wx = std::min(PIPE ? 2 : 8, (P.nlane + 31) / 32);
+        // 128^3 12.32 -> 11.82 ms per step against 4 x 2; tools/gpu/bdshape.sh.  2-D diagonals:
+        // 4 x-warps, 2-3 % faster than 8 with the chain segments; tools/gpu/wsweep.sh)
+        P.Wx = std::min(PIPE ? 2 : (D == 2 ? 4 : 8), (P.nlane + 31) / 32);
         P.Wy = std::max(1, std::min(8 / P.Wx, P.nw));
     } else {
         // lanes over independent x nodes: spend the warps on the pipe axis (y hand-over in smem)
