@@ -906,7 +906,11 @@ void launch_relax_x_k(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
         c->launch_cache[key] = 1;
     }
     const unsigned nlines = (unsigned)(c->g.nnodes / (c->g.ncell[0] * N));
-    kern<<<nlines, 256, smem, c->stream>>>(P);
+    // one thread per node of the line up to 256 (a 192-node line of config 3 left a quarter of a
+    // 256-thread CTA idle in the collision and store phases)
+    const int lx = (int)(c->g.ncell[0] * N);
+    const unsigned threads = (unsigned)std::min(256, ((lx + 31) / 32) * 32);
+    kern<<<nlines, threads, smem, c->stream>>>(P);
 }
 
 template <int DIM, int MODEL, int N, int NPASS>
