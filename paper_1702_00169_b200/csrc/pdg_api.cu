@@ -999,7 +999,12 @@ void launch_relax_lbm_t(pdg_ctx *c, pdg::LocalOps op)
 {
     const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
-    pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
+    // two-phase kernel (moments, then an L1 re-read per update): 0.90-0.99 -> 1.01-1.03 of the
+    // measured copy bandwidth on the 3-D sets (tools/gpu/relax2.sh); PDG_LBM_RELAX2=0 selects the
+    // one-read kernel
+    static const int two = std::getenv("PDG_LBM_RELAX2") ? std::atoi(std::getenv("PDG_LBM_RELAX2")) : 1;
+    if (two) pdg::relax_lbm2_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
+    else pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
 }
 

@@ -1050,6 +1050,49 @@ __global__ void __launch_bounds__(256, (D == 3 && NV <= 15) ? 3 : 2) relax_lbm_k
     }
 }
 
+__device__ __forceinline__ double ld_l1(const double *p)
+{
+    double v;
+    asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Two-phase variant for the 3-D sets: the moments from a first read of the node's NV values
+// (short live ranges), then each value read again -- an L1 hit: the CTA's values were just loaded
+// -- for its update.  ~60 registers instead of 92-128, so more threads per SM keep loads in flight
+// without the spills of a register cap.  Same arithmetic, same results as relax_lbm_kernel.
+template <int D, int NV>
+__global__ void __launch_bounds__(256, 4) relax_lbm2_kernel(double *__restrict__ f, int64_t nnodes,
+                                                           const __grid_constant__ LbmParams L, const LocalOps op)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nnodes) return;
+    double w[D + 1];
+    {
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) fv[i] = f[(int64_t)i * nnodes + x];
+        lbm_moments<D, NV>(fv, L, w);
+    }
+    double gs[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        gs[d] = w[0] * L.G[d] * L.inv_c2;
+        w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
+    }
+    const double hg = fma(op.ca, op.hs1, op.hs2);
+    const LbmNode<D> nd(w, L);
+    const double cb = op.cb;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double vg = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
+        const double fs = fma(hg * L.wgt[i], vg, op.ca * ld_l1(f + (int64_t)i * nnodes + x));
+        __stcs(f + (int64_t)i * nnodes + x, (cb != 0.0) ? fma(cb, nd.feq(i, L), fs) : fs);
+    }
+}
+
 // Partial moments of the local velocities [v0, v0 + nvl) (sharded path, pdg_moments).
 template <int D, int NV>
 __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *__restrict__ f, double *__restrict__ w,
