@@ -190,8 +190,9 @@ typedef struct {
     size_t fb_elems;       /* doubles in fb_dev = nv_local * plane_stride (x dim for PDG_FLUX_LBM) */
     size_t w_elems;        /* doubles in w_dev  = m * nnodes_local (moments / exchange / equilibrium init) */
     size_t work_bytes;     /* bytes of work_dev (device scratch: counters, z-slab carry planes and tables,
-                              lattice ticket/progress counters and boundary traces, large lattice block
-                              tables, the PDG_ASYNC_HOST upload staging) */
+                              lattice ticket/progress/halo counters and tagged boundary-trace words, large
+                              lattice block tables, the PDG_ASYNC_HOST upload staging); the plan-time
+                              lattice knobs (PDG_LATTICE_WARPS / _SEG / _CLUSTER) change it */
     int64_t nnodes;        /* nodes of the full grid */
     int64_t plane_stride;  /* doubles per velocity in fb */
     int32_t nv_local;      /* velocities owned by this rank */
@@ -213,7 +214,9 @@ pdg_status pdg_query_sizes(const pdg_problem *p, pdg_sizes *out);
  * becomes a tiny precomputed inverse: dt and v are constant) and, for lattice sets, the
  * dense blocks of the scheme's steps; creates the library's own streams (one per lattice
  * velocity class, the PDG_ASYNC_HOST copy streams).  With nccl_id it also creates an NCCL
- * communicator (collective over all ranks).
+ * communicator (collective over all ranks).  work_dev's previous content is ignored: the
+ * lattice trace-word region is zeroed on the context stream (every launch leaves it zeroed
+ * again), the counters are reset before each launch that uses them.
  * Errors: as pdg_query_sizes, plus PDG_E_BUFFER, PDG_E_CUDA, PDG_E_NCCL. */
 pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, double *w_dev, void *work_dev,
                       pdg_ctx **out);
