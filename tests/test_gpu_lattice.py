@@ -569,3 +569,53 @@ def test_lattice_sweeps_bitwise_deterministic(lat, N, warps):
     S2.destroy()
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("seglen,fuse", [(16, None), (40, "104")])
+def test_lattice_chain_segments_3d_two_axis_classes(seglen, fuse):
+    """Chain segments on the 3-D classes without a pipe axis (x,y and x,z active: D3Q19's face
+    diagonals), one sweep per launch (halo H) and two sweeps per launch (PDG_LATTICE_FUSE, halo 2H),
+    against the oracle: one T2 and two M2 steps on a box whose chains span several segments."""
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import lattice
+    import math
+    ncell = (10, 48, 48)
+    h = 1.0 / ncell[0]
+    hi = (1.0, ncell[1] * h, ncell[2] * h)
+    kappa = 0.5
+    dtp = kappa * h
+    vel, wts = lattice("D3Q19", 1.0)
+    fparams = [1.0 / math.sqrt(3.0)] + list(wts)
+    env = {"PDG_LATTICE_SEG": str(seglen), "PDG_LATTICE_FUSE": fuse}
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        pb = pdg.make_problem(3, list(ncell), 2, 4, vel, [0] * len(vel), 1.0, pdg.PDG_FLUX_LBM, fparams, 2.0 * dtp, hi=hi)
+        S = pdg.Solver(pb)
+        ob = O.Problem(3, list(ncell), 2, vel, [0] * len(vel), 4, 1.0, 3, fparams, 2.0 * dtp, hi=list(hi))
+        shape = ob.grid_shape()
+        rng = np.random.default_rng(123 + seglen)
+        f = (1.0 + 0.5 * (rng.random((ob.nv,) + shape) - 0.5)) / ob.nv
+        fb_full = rng.random((ob.nv,) + shape) / ob.nv
+        S.set_state(to_dev(f), to_dev(lattice_planes(_planes_view(ob), fb_full, S.sizes.plane_stride)))
+        S.transport(dtp)
+        got = to_np(S.get_state(), f.shape)
+        fc = ob.grid_to_cells(f)
+        fbc = ob.grid_to_cells(fb_full)
+        O.t2_all(ob, dtp, fc, fbc)
+        assert rel_maxnorm(got, ob.cells_to_grid(fc)) <= TOL_OP
+        S.step(2)
+        got2 = to_np(S.get_state(), f.shape)
+        S.destroy()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    ref2 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 2)
+    assert rel_maxnorm(got2, ref2) <= TOL_STEP
