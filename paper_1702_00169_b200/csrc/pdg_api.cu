@@ -128,9 +128,9 @@ void plan_lattice(const Geometry &g, LatPlan &P)
             P.Wy = std::min(wy, P.nw);
         }
     }
-    if (P.d == 3 && g.n == 4) {  // p = 3 body diagonals: ~90 KB of shared memory per warp
+    if (P.d == 3 && g.n == 4) {  // p = 3 body diagonals: ~50 KB of shared memory per warp (no row prefetch)
         P.Wx = std::min(P.Wx, 2);
-        P.Wy = std::max(1, std::min(P.Wy, 2 / P.Wx));
+        P.Wy = std::max(1, std::min(P.Wy, 4 / P.Wx));
     }
     P.ngx = (P.nlane + 32 * P.Wx - 1) / (32 * P.Wx);
     P.ngy = (P.nw + P.Wy - 1) / P.Wy;
@@ -729,7 +729,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     constexpr int PIPE = pdg::LatShape<D, ACT>::PIPE;
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
     const size_t smem =
-        sizeof(double) * ((size_t)(threads / 32) * pdg::LatRing<D>::RING * TB::NB * 32 +
+        sizeof(double) * ((size_t)(threads / 32) * pdg::LatRing<D, N, DA>::RING * TB::NB * 32 +
                           (PIPE ? (size_t)NPASS * 2 * 32 * TB::MF * (CS > 1 ? threads / 32 : threads / 32 - pl.Wx) : 0) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32) +
                           (PIPE ? (size_t)NPASS * pl.Wx * 32 * 2 * TB::MF : 0));

@@ -169,10 +169,12 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b)
         : "d"(a), "d"(b));
 }
 
-template <int D>
+// Rows prefetched ahead: 3 for the 2-D diagonals (latency-bound, short rows), 1 in 3-D, none for
+// the p = 3 body diagonals, whose 64-node rows would leave room for only two warps per SM.
+template <int D, int N = 0, int DA = 0>
 struct LatRing {
-    static constexpr int PFA = (D == 2) ? 3 : 1;  // rows prefetched ahead
-    static constexpr int RING = PFA + 1;          // row buffers per warp
+    static constexpr int PFA = (D == 2) ? 3 : ((N == 4 && DA == 3) ? 0 : 1);
+    static constexpr int RING = PFA + 1;  // row buffers per warp
 };
 
 // Tensor-core path of the lattice sweep: used for the body diagonals (3 active axes), whose
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     constexpr int MT = MMA::MT, KS = MMA::KS, KSX = MMA::KSX;
     // rows prefetched ahead with cp.async: 2-D diagonals are latency-bound (short rows, one warp
     // per SM sub-partition), so they look three rows ahead; 3-D classes one row
-    constexpr int PFA = LatRing<D>::PFA, RING = LatRing<D>::RING;
+    constexpr int PFA = LatRing<D, N, S::DA>::PFA, RING = LatRing<D, N, S::DA>::RING;
     static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     // [row][32 units] shared buffers (row buffers, staging): the tensor path XOR-swizzles the unit
     // index with 4 (row mod 4), so the four rows of a DMMA B fragment (lane % 4) and the eight
@@ -605,7 +607,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     for (int k = 0; k < PFA; ++k) prefetch(k);
                 if constexpr (PIPE) {
                     // PFA == 1: row r (and its prefetched y-trace words) have landed; the next row's
-                    // prefetch is issued once the y-trace words have been read (below)
+                    // prefetch is issued once the y-trace words have been read (below).  PFA == 0:
+                    // the row is loaded now.
+                    if constexpr (PFA == 0) prefetch(r);
                     cp_async_wait<0>();
                 } else {
                     prefetch(r + PFA);
@@ -654,7 +658,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             for (int j = 0; j < MF; ++j) sy[j] = 0.0;
                             if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
                         }
-                        if (ps == NPASS - 1) prefetch(r + 1);  // overlaps the rest of the row
+                        if (PFA > 0 && ps == NPASS - 1) prefetch(r + 1);  // overlaps the rest of the row
                     }
                     // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
                     double s0[XA ? MF : 1];
