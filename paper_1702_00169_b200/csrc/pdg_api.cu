@@ -212,7 +212,7 @@ void lattice_classes(const Geometry &g, const double *vel, std::vector<LatPlan> 
         q.ints_off = io;
         q.xbuf_off = xo;
         q.ybuf_off = yo;
-        io += (((size_t)2 * q.ntasks + 1 + 63) / 64) * 64;  // ticket, progress[ntasks], halo flags[ntasks]
+        io += (((size_t)9 * q.ntasks + 1 + 63) / 64) * 64;  // ticket, progress[ntasks][8 x-warps], halo flags[ntasks]
         xo += q.xbuf;
         yo += q.ybuf;
     }
@@ -342,7 +342,7 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
             std::vector<LatPlan> cls;
             lattice_classes(*g, p->vel, cls);
             for (const auto &q : cls) {
-                g->lat_ints = std::max(g->lat_ints, q.ints_off + (((size_t)2 * q.ntasks + 1 + 63) / 64) * 64);
+                g->lat_ints = std::max(g->lat_ints, q.ints_off + (((size_t)9 * q.ntasks + 1 + 63) / 64) * 64);
                 g->lat_xbuf = std::max(g->lat_xbuf, q.xbuf_off + q.xbuf);
                 g->lat_ybuf = std::max(g->lat_ybuf, q.ybuf_off + q.ybuf);
             }
@@ -627,7 +627,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.fb = c->fb;
     P.ticket = c->lat_ints + pl.ints_off;
     P.progress = c->lat_ints + pl.ints_off + 1;
-    P.hdone = P.progress + pl.ntasks;
+    P.hdone = P.progress + (size_t)8 * pl.ntasks;
     P.xbuf = c->lat_xbuf + pl.xbuf_off;
     P.ybuf = c->lat_ybuf + pl.ybuf_off;
     for (int k = 0; k < 3; ++k) {
@@ -768,7 +768,7 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     }
     const int units = std::max(1, std::min(P.g.ntasks_c, occ));
     lc.gridDim = dim3((unsigned)(units * CS));
-    PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)2 * pl.ntasks + 1), st));
+    PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)9 * pl.ntasks + 1), st));
     PDG_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, P));
     return PDG_OK;
 }

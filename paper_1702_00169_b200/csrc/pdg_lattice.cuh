@@ -122,7 +122,7 @@ struct LatParams {
     using S = LatShape<D, ACT>;
     double *f;
     const double *fb;
-    int *ticket;     // [0]; progress counters follow: progress[task] = rows published (tensor-path y traces)
+    int *ticket;     // [0]; progress counters follow: progress[task * 8 + x-warp] = rows published (tensor-path y traces)
     int *progress;
     int *hdone;      // [task]: 1 once the segment has read its halo rows (their old values)
     double *xbuf;    // [task][row][pass][Wy][2 MF] tagged x out-trace words at CTA boundaries
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // there (its heavier rows hide the fence; the tagged words cost 1.8x the hand-over traffic)
     constexpr bool YLL = !USE_MMA;
     constexpr int MFP = (MF + 1) & ~1;  // per-lane stride of the plain y traces (16-byte multiple)
-    const bool publish = !YLL && PIPE && g.ngy > 1;  // row progress (x traces travel as tagged words)
+    // (tensor-path y traces: each producing warp publishes its own row progress, per (task, x-warp))
     uint64_t *const xll = reinterpret_cast<uint64_t *>(P.xbuf);
     uint64_t *const yll = reinterpret_cast<uint64_t *>(P.ybuf);
     // tagged y-trace words of (task, row, pass) for this lane: [task][row][pass][Wx][32][2 MF]
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             cp_async16_cg(yd + h, reinterpret_cast<const double *>(ysrc + h));
                     }
                     ypf = true;
-                } else if (!YLL && ycons && rr < nrow && ld_acquire(P.progress + task - per_gy) >= rr + 1) {
+                } else if (!YLL && ycons && rr < nrow && ld_acquire(P.progress + (int64_t)(task - per_gy) * 8 + qx) >= rr + 1) {
                     // plain traces: copied only once published (the producer normally runs ahead)
 #pragma unroll
                     for (int ps = 0; ps < NPASS; ++ps) {
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) sy[j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
                             } else {
-                                if (ps == 0) wait_progress(P.progress + task - per_gy, r + 1);
+                                if (ps == 0) wait_progress(P.progress + (int64_t)(task - per_gy) * 8 + qx, r + 1);
                                 const double *ysrc = P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
@@ -867,7 +867,10 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                                 double *dst = P.ybuf + (((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
-                                __threadfence();
+                                // the producing warp publishes its own row progress: __syncwarp orders
+                                // the lanes' stores before lane 0's release (cumulative at gpu scope)
+                                __syncwarp();
+                                if (lane == 0) st_release(P.progress + (int64_t)task * 8 + qx, r + 1);
                             }
                         }
                     }
@@ -893,22 +896,13 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             }
             PDG_TMARK(6);
             step_sync(t);
-            if (publish && threadIdx.x == 0 && t >= maxskew) {
-                int tmin = t;  // rows finished by every warp
-                if (p2p)
-                    for (int w = 0; w < nwarps; ++w) tmin = min(tmin, vdone[w]);
-                if (tmin >= maxskew) st_release(P.progress + task, min(nrow, tmin - maxskew + 1));
-            }
             // every warp has read the halo rows (cp.async waited): release them to the previous segment
             if (rs > r0 && t == rs - r0 - 1 + maxskew) {
                 __syncthreads();
                 if (threadIdx.x == 0) st_release(P.hdone + task, 1);
             }
         }
-        if (p2p) {
-            __syncthreads();  // every warp done: publish the whole task
-            if (publish && threadIdx.x == 0) st_release(P.progress + task, nrow);
-        }
+        if (p2p) __syncthreads();  // every warp done with the task before the next ticket
         cp_async_wait<0>();
     }
 }
