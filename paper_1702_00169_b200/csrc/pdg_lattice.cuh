@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     long long tlast = clock64();
 #endif
 
-    __shared__ double xs[NPASS][2][8][XA ? MF : 1];
+    // x hand-over slots between the x-warps of a CTA: a ring of XR rows; with the point-to-point
+    // sync of the pipe classes a producer may run XR - 1 rows ahead of its x consumer
+    constexpr int XR = PIPE ? 4 : 2;
+    __shared__ double xs[NPASS][XR][8][XA ? MF : 1];
     __shared__ double gxs[8][RING][XA ? MF : 1];  // x inflow ghosts of the first x warp, prefetched per row
     __shared__ int s_task;
     __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         if (!p2p || t == 0) return;
         if (lane == 0) {
             if (XA && qx > 0) wait_done(warp - 1, t - 1);
-            if (XA && qx < g.Wx - 1) wait_done(warp + 1, t - 1);
+            if (XA && qx < g.Wx - 1) wait_done(warp + 1, t - (XR - 1));
             if (PIPE && wy > 0) wait_done(warp - g.Wx, t - 1);
             if (PIPE && wy < g.Wy - 1) wait_done(warp + g.Wx, t - 1);
         }
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     if constexpr (XA) {
                         if (qx > 0) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) & 1][warp - 1][j];
+                            for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) % XR][warp - 1][j];
                         } else if (gx > 0) {
                             // only lane 0 enters the x in-trace into the scan
                             if (lane == 0)
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
                         if (lane == 31) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) xs[ps][t & 1][warp][j] = a[j];
+                            for (int j = 0; j < MF; ++j) xs[ps][t % XR][warp][j] = a[j];
                             if (qx == g.Wx - 1 && gx < g.ngx - 1)
                                 ll_put<MF>(xll + ((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wy + wy) * 2 * MF, a,
                                            (uint32_t)r + 1u);
