@@ -158,3 +158,17 @@ def test_lattice_validation_errors():
         pdg.query_sizes(pdg.make_problem(3, 4, 2, 4, v3, c3comp, c3.lam, c3.flux, list(c3.fparams), c3.dt,
                                          gravity=(0.0, 0.0, -1.0)))
     assert e.value.status == pdg.PDG_E_UNSUPPORTED
+
+
+def test_product_never_uses_the_oracle():
+    """The product path (package + CUDA sources) neither imports nor links anything under oracle/;
+    only tests, __graft_entry__.smoke() and bench.py's baseline legs may."""
+    pkg = os.path.join(ROOT, "paper_1702_00169_b200")
+    offenders = []
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".hpp", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, fn), errors="ignore").read()
+                if re.search(r"(import\s+oracle|from\s+oracle|liboracle|oracle/|pdg_oracle)", txt):
+                    offenders.append(fn)
+    assert offenders == []
