@@ -17,16 +17,25 @@
 //     s_out = a + Bx s_in (Bx uniform): a 5-step warp-shuffle Kogge-Stone scan with the
 //     precomputed powers Bx^(2^j); warps along x and along the PIPE axis (y, when y and z
 //     are both active) are skewed by one row per warp inside the CTA and hand traces over
-//     through shared memory (one __syncthreads per row).
-//   * across CTAs the same hand-over goes through global memory with per-task row
-//     progress counters (release/acquire); tasks are claimed in dependency order with an
-//     atomic ticket, so every wait targets a task already owned by a running CTA.
-//   * dense block constants live in the kernel parameter space (constant bank): every
-//     DFMA of the n^d x n^d mat-vec takes its coefficient as a c[0x0][...] operand.
+//     through shared memory (a barrier per row, or point-to-point step counters).
+//   * across CTAs the x traces (and the FMA path's y traces) travel as tagged 64-bit words
+//     (ll_put / ll_take: no fences, the consumer empties the slot); the tensor path's y
+//     traces are plain doubles with a per-(task, x-warp) row-progress counter published by
+//     the producing warp.  Tasks are claimed in dependency order with an atomic ticket, so
+//     every wait targets a task already owned by a running CTA.
+//   * classes without a pipe axis that cannot fill the GPU walk their chain in segments
+//     that start a norm-bounded halo early from a zero trace (pdg_tables.hpp
+//     lattice_chain_halo); segments are claimed in descending order and release their halo
+//     rows to the previous segment with a flag.
+//   * the block is applied in the rhs form F = A^{-1} (2 f_old + in-trace injections), then
+//     + Q_x s_x after the scan, f_new = F - f_old; on the FMA path the constants come from
+//     the kernel parameter space, on the tensor path (body diagonals, DMMA.8x8x4) from
+//     shared memory.
 //
-//  relax_lbm_kernel<D, NV>: collision fused with the moments w = (rho, rho u) = P f,
-//  P = [1; v^T], f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2))
-//  (P:1138-1145), f <- ca f + cb f^eq (eq collision_cn).
+//  relax_lbm2_kernel<D, NV> (default) / relax_lbm_kernel<D, NV>: collision fused with the
+//  moments w = (rho, rho u) = P f, P = [1; v^T],
+//  f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2)),
+//  f <- ca f + cb f^eq (eq collision_cn).
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
