@@ -85,3 +85,63 @@ def test_fuzz_parity(seed):
         twin = rel_maxnorm(O.scheme_run(ob, f2, fb, steps, scheme), ref)
         tol = max(tol, 4.0 * twin)
     assert err_f <= tol and err_w <= tol, (desc, err_f, err_w, tol)
+
+
+# --------------------------------------------------------------------------
+# Protocol fuzz: lattice sets with the cross-CTA hand-overs, chain segments and the fused
+# two-sweep variant forced on through the plan knobs, on boxes large enough for
+# several CTAs and segments.  PDG_FUZZ_SEEDS widens the sweep (default 24 seeds).
+# --------------------------------------------------------------------------
+N_PROTO = int(__import__("os").environ.get("PDG_FUZZ_SEEDS", "24"))
+
+
+@pytest.mark.parametrize("seed", range(N_PROTO))
+def test_fuzz_lattice_protocols(seed):
+    import os
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import lattice
+    rng = np.random.default_rng(5000 + seed)
+    dim = int(rng.integers(2, 4))
+    p = int(rng.integers(1, 4)) if dim == 2 else int(rng.integers(1, 3))
+    name = LATTICES[dim][int(rng.integers(0, len(LATTICES[dim])))]
+    ncell = ([int(rng.integers(20, 81)) for _ in range(2)] if dim == 2
+             else [int(rng.integers(4, 13)), int(rng.integers(4, 13)), int(rng.integers(12, 33))])
+    kappa = float(rng.choice([0.1, 0.25, 0.5, 1.0]))
+    h = 1.0 / ncell[0]
+    hi = [ncell[d] * h for d in range(dim)] + [1.0] * (3 - dim)  # square cells: equal kappas
+    dt = 2.0 * kappa * h
+    env = {"PDG_LATTICE_WARPS": str(rng.choice(["1,1", "2,2", "1,2", "2,1", "4,2"])),
+           "PDG_LATTICE_SEG": str(int(rng.choice([0, 12, 16, 20, 30]))),
+           "PDG_LATTICE_FUSE": str(int(rng.choice([0, 104])))}
+    vel, wts = lattice(name, 1.0)
+    fparams = [1.0 / math.sqrt(3.0)] + list(wts)
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        os.environ.update(env)
+        pb = pdg.make_problem(dim, ncell, p, dim + 1, vel, [0] * len(vel), 1.0, pdg.PDG_FLUX_LBM, fparams, dt,
+                              hi=tuple(hi))
+        S = pdg.Solver(pb)
+        ob = O.Problem(dim, ncell, p, vel, [0] * len(vel), dim + 1, 1.0, 3, fparams, dt, hi=hi)
+        shape = ob.grid_shape()
+        base = 1.0 / ob.nv
+        f = base * (1.0 + 0.2 * (rng.random((ob.nv,) + shape) - 0.5))
+        fb = base * (1.0 + 0.2 * rng.random((ob.nv,) + shape))
+
+        class _C:
+            pass
+        cv = _C()
+        cv.dim, cv.grid_shape = ob.dim, shape
+        cv.velocities = lambda: (ob.vel.tolist(), None)
+        S.set_state(to_dev(f), to_dev(lattice_planes(cv, fb, S.sizes.plane_stride)))
+        S.step(2)
+        got = to_np(S.get_state(), f.shape)
+        S.destroy()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    ref = O.scheme_run(ob, f, fb, 2, "m2")
+    err = rel_maxnorm(got, ref)
+    assert err <= 1e-12, (seed, name, dim, ncell, p, kappa, env, err)
