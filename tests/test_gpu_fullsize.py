@@ -135,7 +135,7 @@ def _smooth_field(X, Y, Z, i, nv, amp):
     return (1.0 + amp * sin(0.37 * X + 0.71 * Y + 1.13 * Z + 0.5 * i + 0.3 * X * Y / 97.0)) / nv
 
 
-@pytest.mark.parametrize("lat,N", [("D3Q27", 128), ("D2Q9", 1024)])
+@pytest.mark.parametrize("lat,N", [("D3Q27", 128), ("D2Q9", 1024), ("D2Q9", 2048), ("D3Q15", 128)])
 def test_lattice_fullsize_sampled_transport(lat, N):
     from pdg_inputs import lbm_config
     cfg = lbm_config(lat, N, nu=2.0)
