@@ -26,7 +26,9 @@
  *  - All device work is enqueued on the stream given in pdg_problem.cuda_stream
  *    (a cudaStream_t, NULL = legacy default stream); pdg_step/pdg_transport/
  *    pdg_collide are asynchronous and CUDA-graph capturable when nranks == 1.
- *  - One context per device; calls on one context are serialised by the caller.
+ *  - One context per device; calls on one context are serialised by the caller.  The context
+ *    is bound to the device that was current at pdg_create: every call taking a context makes
+ *    that device current for its duration and restores the caller's device on return.
  *
  * Canonical layouts (row-major, last index fastest):
  *  - node grid: for an N_0 x N_1 (x N_2) cell box of degree p, n = p+1 nodes per
@@ -64,7 +66,9 @@ typedef struct pdg_ctx pdg_ctx; /* opaque, owned by the library */
 
 typedef enum {
     PDG_OK = 0,
-    PDG_E_INVALID_ARGUMENT = 1, /* NULL pointer, bad size, dt == 0, lambda <= 0, tau < 0, nranks > nv */
+    PDG_E_INVALID_ARGUMENT = 1, /* NULL pointer, bad size, dt == 0, lambda <= 0, tau < 0, nranks > nv,
+                                   tau > 0 with a collision substep h of the scheme (or a pdg_collide /
+                                   pdg_relax_from_w dt) where 2 tau + h <= 0 (eq collision_cn) */
     PDG_E_DIMENSION = 2,        /* dim not in {2, 3}                                   (SPEC DimensionOutOfRange) */
     PDG_E_DEGREE = 3,           /* degree not in the compiled set {1, 2, 3}            (SPEC DegreeOutOfRange) */
     PDG_E_VELOCITY_SET = 4,     /* velocities not the canonical +-lambda e_k per component set, or comp[] wrong */
@@ -96,7 +100,7 @@ typedef enum {
     PDG_SCHEME_M2KIN = 1, /* T2(dt/4) C2(dt/2) T2(dt/2) C2(dt/2) T2(dt/4) */
     PDG_SCHEME_M4 = 2,    /* M2kin(g1 dt) M2kin(g2 dt) M2kin(g1 dt), g1 = 1/(2 - 2^(1/3)), g2 = 1 - 2 g1:
                              palindromic composition raising the order to 4; needs
-                             2 tau + g2 dt/2 > 0 when tau > 0 */
+                             2 tau + g2 dt/2 > 0 when tau > 0 (checked at pdg_query_sizes/pdg_create) */
     PDG_SCHEME_M2S = 3    /* T2(dt/2) S2(dt/2) C2(dt) S2(dt/2) T2(dt/2): the Strang scheme with the source
                              step (NEXT-3); needs a source (pdg_problem.source) */
 } pdg_scheme;
@@ -248,7 +252,8 @@ pdg_status pdg_transport(pdg_ctx *c, double dtp);
 
 /* One collision operator C2(dt) on every node (row a2): w = P f, f^eq(w),
  * f <- ((2 tau - dt) f + 2 dt f^eq)/(2 tau + dt)   (= 2 f^eq - f at tau = 0).
- * With nranks > 1: partial moments, NCCL sum, then relaxation of local velocities. */
+ * With nranks > 1: partial moments, NCCL sum, then relaxation of local velocities.
+ * PDG_E_INVALID_ARGUMENT if tau > 0 and 2 tau + dt <= 0, or dt is not finite. */
 pdg_status pdg_collide(pdg_ctx *c, double dt);
 
 /* One source operator S2(h) on every node (NEXT-3): f <- f + h g(f) for the gravity

@@ -222,6 +222,17 @@ constexpr int kMaxTables = 16;
 constexpr int kMaxLatTables = 16;  // distinct (class, dt') of the large (p = 3 body-diagonal) block tables
 constexpr size_t kLatBigTableDoubles = sizeof(pdg::LatTab<4, 3>) / sizeof(double);
 
+// tau > 0: eq collision_cn divides by 2 tau + h; a substep with 2 tau + h <= 0 (the negative
+// middle step of M4, or dt < 0) has no meaningful collision factor (SPEC's tau > |dt| gamma guard)
+bool collision_step_ok(double tau, double h) { return tau == 0.0 || 2.0 * tau + h > 0.0; }
+
+// An operator of a scheme: T(h) = T2(h) on every velocity, C(h) = C2(h), S(h) = S2(h).
+struct Op {
+    int kind;  // 0: T, 1: C, 2: S (source)
+    double h;
+};
+void append_scheme(std::vector<Op> &ops, int scheme, double dt);
+
 pdg_status validate(const pdg_problem *p, Geometry *g)
 {
     if (!p) return fail(PDG_E_INVALID_ARGUMENT, "problem is NULL");
@@ -243,6 +254,14 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     }
     if (p->scheme == PDG_SCHEME_M2S && p->source == PDG_SOURCE_NONE)
         return fail(PDG_E_INVALID_ARGUMENT, "PDG_SCHEME_M2S needs a source");
+    if (p->tau > 0.0) {
+        std::vector<Op> ops;
+        append_scheme(ops, p->scheme, p->dt);
+        for (const Op &o : ops)
+            if (o.kind == 1 && !collision_step_ok(p->tau, o.h))
+                return fail(PDG_E_INVALID_ARGUMENT, "tau > 0 needs 2 tau + h > 0 for every collision substep h of the "
+                                                    "scheme (eq collision_cn, P:453)");
+    }
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
     g->async_host = (p->flags & PDG_ASYNC_HOST) ? 1 : 0;
     g->dim = p->dim;
@@ -488,6 +507,24 @@ struct pdg_ctx {
 namespace {
 
 pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass);
+
+// Every entry point taking a context runs on the context's device (the caller's current
+// device may differ) and restores the caller's device on exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const pdg_ctx *c)
+    {
+        if (!c) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
 
 pdg_status post_launch(pdg_ctx *c, const char *what)
 {
@@ -1178,10 +1215,6 @@ bool use_relax_x(const pdg_ctx *c)
 // T(h) = T2(h) on every velocity, C(h) = C2(h).  Execution fuses, without changing any
 // operator: two consecutive T(h) with the same h into one pass over f (two sweeps), and a
 // C followed by T's into the collision + x-sweep kernel plus one y/z sweep pass.
-struct Op {
-    int kind;  // 0: T, 1: C, 2: S (source)
-    double h;
-};
 
 void append_m2kin(std::vector<Op> &ops, double dt)
 {
@@ -1619,7 +1652,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
                     const pdg_ctx::ZTable *zt = nullptr;
                     pdg_status zs = ztable(c, o.h, np, &zt);
                     if (zs != PDG_OK) {
-                        delete c;
+                        pdg_destroy(c);
                         return zs;
                     }
                 }
@@ -1648,16 +1681,14 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
             }
         }
         if (!c->prof.on) {
-            for (auto &e : c->prof.ev)
-                if (e) cudaEventDestroy(e);
-            delete c;
+            pdg_destroy(c);  // destroys the events that were created
             return fail(PDG_E_CUDA, "cudaEventCreate failed");
         }
     }
     if (p->nccl_id) {
         std::string err;
         if (!c->comm.init(p->nccl_id, p->nranks, p->rank, &err)) {
-            delete c;
+            pdg_destroy(c);
             return fail(PDG_E_NCCL, err);
         }
     }
@@ -1667,6 +1698,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
 
 pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_device)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     if (f) PDG_CUDA_TRY(cudaMemcpyAsync(c->f, f, sizeof(double) * c->g.nvl * c->g.nnodes, kind, c->stream));
@@ -1681,6 +1713,7 @@ pdg_status pdg_set_state(pdg_ctx *c, const double *f, const double *fb, int on_d
 
 pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, int on_device)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!w) return fail(PDG_E_INVALID_ARGUMENT, "w is NULL");
     const size_t wbytes = sizeof(double) * c->g.m * c->g.nnodes;
@@ -1753,6 +1786,7 @@ pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, in
 
 pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device)
 {
+    DeviceGuard dg(c);
     if (!c || !f) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     PDG_CUDA_TRY(cudaMemcpyAsync(f, c->f, sizeof(double) * c->g.nvl * c->g.nnodes,
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
@@ -1762,6 +1796,7 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device)
 
 pdg_status pdg_transport(pdg_ctx *c, double dtp)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
     if (!std::isfinite(dtp)) return fail(PDG_E_INVALID_ARGUMENT, "dtp must be finite");
@@ -1770,13 +1805,17 @@ pdg_status pdg_transport(pdg_ctx *c, double dtp)
 
 pdg_status pdg_collide(pdg_ctx *c, double dt)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
+    if (!std::isfinite(dt) || !collision_step_ok(c->prob.tau, dt))
+        return fail(PDG_E_INVALID_ARGUMENT, "collision needs a finite dt with 2 tau + dt > 0 (tau > 0)");
     return collide(c, dt);
 }
 
 pdg_status pdg_source(pdg_ctx *c, double h)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
     if (c->prob.source == PDG_SOURCE_NONE) return fail(PDG_E_INVALID_ARGUMENT, "the problem has no source");
@@ -1786,7 +1825,9 @@ pdg_status pdg_source(pdg_ctx *c, double h)
 
 pdg_status pdg_partial_moments(pdg_ctx *c)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    wait_w_download(c);  // PDG_ASYNC_HOST: a pending pdg_moments download may still read w_dev
     if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
     else PDG_DISPATCH(launch_partial_t, c);
     return post_launch(c, "partial_moments");
@@ -1794,7 +1835,10 @@ pdg_status pdg_partial_moments(pdg_ctx *c)
 
 pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!std::isfinite(dt) || !collision_step_ok(c->prob.tau, dt))
+        return fail(PDG_E_INVALID_ARGUMENT, "collision needs a finite dt with 2 tau + dt > 0 (tau > 0)");
     double ca, cb;
     collision_coeffs(c, dt, &ca, &cb);
     if (c->g.lattice) {
@@ -1808,6 +1852,7 @@ pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
 
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
 {
+    DeviceGuard dg(c);
     NvtxRange nv("pdg_step");
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
@@ -1828,6 +1873,7 @@ pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
 
 pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device)
 {
+    DeviceGuard dg(c);
     if (!c || !w) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     pdg_status s = partial_and_reduce(c);
     if (s != PDG_OK) return s;
@@ -1849,6 +1895,7 @@ pdg_status pdg_moments(pdg_ctx *c, double *w, int on_device)
 
 pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad)
 {
+    DeviceGuard dg(c);
     if (!c || !n_bad) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     PDG_CUDA_TRY(cudaMemsetAsync(c->counter, 0, sizeof(unsigned long long), c->stream));
     const int grid = grid_for(c->g.nnodes, 256);
@@ -1880,6 +1927,7 @@ pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, dou
 
 pdg_status pdg_synchronize(pdg_ctx *c)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     PDG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->copy_stream) PDG_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
@@ -1889,6 +1937,7 @@ pdg_status pdg_synchronize(pdg_ctx *c)
 
 void pdg_destroy(pdg_ctx *c)
 {
+    DeviceGuard dg(c);
     if (!c) return;
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
@@ -1921,6 +1970,7 @@ pdg_status pdg_nccl_unique_id(void *out)
 
 pdg_status pdg_profile_read(pdg_ctx *c, double *ms, int64_t *launches, double *alg_bytes)
 {
+    DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     double t[PDG_NUM_KERNEL_KINDS] = {0}, b[PDG_NUM_KERNEL_KINDS] = {0};
     int64_t n[PDG_NUM_KERNEL_KINDS] = {0};

@@ -44,6 +44,17 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float, device=None, group=None) -> float:
+    """Sum of a per-rank scalar (e.g. counts of non-physical nodes)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    backend = dist.get_backend(group)
+    dev = device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
+
+
 def sharded_solver(cfg, device, flags=0, stream=None, tau=0.0, scheme=pdg.PDG_SCHEME_M2,
                    decomposition=pdg.PDG_DECOMP_VELOCITY, slabs_per_rank=1):
     """A libpdg context for this rank's share (velocity block or z-slab), with its NCCL communicator."""

@@ -224,22 +224,36 @@ class Solver:
         self.w = torch.empty(s.w_elems, **kw)
         self.work = torch.zeros(max(64, s.work_bytes // 8), **kw)
         self.ctx = ctypes.c_void_p()
-        _check(self.lib.pdg_create(ctypes.byref(pb), _ptr(self.f), _ptr(self.fb), _ptr(self.w), _ptr(self.work),
-                                   ctypes.byref(self.ctx)), "pdg_create")
+        self._keep = []
+        with torch.cuda.device(self.device):  # the context records the current device
+            _check(self.lib.pdg_create(ctypes.byref(pb), _ptr(self.f), _ptr(self.fb), _ptr(self.w),
+                                       _ptr(self.work), ctypes.byref(self.ctx)), "pdg_create")
 
     # --- state ---------------------------------------------------------------
     def set_state(self, f=None, fb=None):
-        """f, fb: torch tensors (device or host) in the canonical layout."""
+        """f, fb: torch tensors (both on the device or both on the host) in the canonical layout."""
+        if f is None and fb is None:
+            return
+        if f is not None and fb is not None and f.is_cuda != fb.is_cuda:
+            raise ValueError("f and fb must both be device or both be host tensors")
         on_dev = int((f if f is not None else fb).is_cuda)
-        fp = _ptr(f.contiguous()) if f is not None else None
-        fbp = _ptr(fb.contiguous()) if fb is not None else None
+        # contiguous copies bound to locals: they must outlive the (possibly asynchronous) copy
         if f is not None:
             assert f.numel() == self.sizes.f_elems and f.dtype == self.torch.float64
+            f = f.contiguous()
         if fb is not None:
             assert fb.numel() == self.sizes.fb_elems and fb.dtype == self.torch.float64
-        keep = (f, fb)
+            fb = fb.contiguous()
+        fp = _ptr(f) if f is not None else None
+        fbp = _ptr(fb) if fb is not None else None
         _check(self.lib.pdg_set_state(self.ctx, fp, fbp, on_dev), "pdg_set_state")
-        del keep
+        self._keep_until_sync(on_dev, f, fb)
+
+    def _keep_until_sync(self, on_dev, *tensors):
+        # PDG_ASYNC_HOST: a host-input call returns before its copy ran; keep the (pinned) sources
+        # alive until the next pdg_synchronize.  Device inputs are ordered on the context stream.
+        if not on_dev and (self.pb.flags & PDG_ASYNC_HOST):
+            self._keep.append(tensors)
 
     def set_equilibrium(self, w, wb=None):
         assert w.numel() == self.sizes.w_elems and w.dtype == self.torch.float64
@@ -250,6 +264,7 @@ class Solver:
             assert wb.numel() == self.sizes.w_elems and wb.is_cuda == w.is_cuda
             wbp = _ptr(wb)
         _check(self.lib.pdg_set_equilibrium(self.ctx, _ptr(w), wbp, int(w.is_cuda)), "pdg_set_equilibrium")
+        self._keep_until_sync(int(w.is_cuda), w, wb)
 
     def get_state(self, out=None):
         if out is None:
@@ -306,6 +321,7 @@ class Solver:
 
     def synchronize(self):
         _check(self.lib.pdg_synchronize(self.ctx), "pdg_synchronize")
+        self._keep.clear()
 
     def destroy(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:

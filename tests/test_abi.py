@@ -62,6 +62,14 @@ def _bad(cfg, **over):
     return e.value.status
 
 
+def _good(cfg, **over) -> bool:
+    vel, comp = cfg.velocities()
+    kw = dict(dim=cfg.dim, ncell=cfg.N, degree=cfg.p, m=cfg.m, vel=vel, comp=comp, lam=cfg.lam, flux=cfg.flux,
+              flux_params=list(cfg.fparams), dt=cfg.dt)
+    kw.update(over)
+    return pdg.query_sizes(pdg.make_problem(**kw)).f_elems > 0
+
+
 def test_validation_errors():
     cfg = CONFIGS[3]
     assert _bad(cfg, dim=4) == pdg.PDG_E_DIMENSION
@@ -78,6 +86,13 @@ def test_validation_errors():
     comp2[0] = 1
     assert _bad(cfg, comp=comp2) == pdg.PDG_E_VELOCITY_SET
     assert _bad(cfg, ncell=0) == pdg.PDG_E_INVALID_ARGUMENT
+    # tau > 0: every collision substep h of the scheme needs 2 tau + h > 0 (eq collision_cn)
+    dt = cfg.dt
+    assert _bad(cfg, tau=0.2 * dt, dt=-dt) == pdg.PDG_E_INVALID_ARGUMENT            # M2, C2(-dt)
+    assert _bad(cfg, tau=0.1 * dt, scheme=pdg.PDG_SCHEME_M4) == pdg.PDG_E_INVALID_ARGUMENT  # g2 dt/2 < 0
+    ok = dict(tau=0.6 * dt, scheme=pdg.PDG_SCHEME_M4)  # 2 tau + g2 dt/2 = (1.2 - 0.85) dt > 0
+    assert _good(cfg, **ok) and _good(cfg, tau=0.0, dt=-dt) and _good(cfg, tau=0.3 * dt, dt=-dt,
+                                                                       scheme=pdg.PDG_SCHEME_M2KIN)
 
 
 def test_solver_refuses_without_gpu():

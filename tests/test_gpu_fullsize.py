@@ -212,3 +212,30 @@ def test_lattice_fullsize_sampled_transport(lat, N):
     del S
     torch.cuda.empty_cache()
     assert max(errs) <= 1e-13, errs
+
+
+# --------------------------------------------------------------------------
+# The parity protocol on whole arrays at full size (tests/parity_harness.py; the long runs of every
+# config are in test_gpu_long.py, gated): the fast cases that run in every `pytest -m gpu`.
+# --------------------------------------------------------------------------
+def test_fullsize_cfg2_stabilised_free_running_whole_arrays():
+    """Config 2's stabilised twin (lambda = 3.5, same nu) at full 256^2 over its 100 steps: the GPU
+    (pdg_step(1) per step, and one pdg_step(100) call) against the oracle on the whole f and w at
+    every step, plus re-synced steps 1, 50, 100: all <= 1e-12."""
+    from parity_harness import run_protocol
+    rec = run_protocol(CONFIGS[2].stabilised(), {1, 50, 100}, lockstep=True, gpu_twin=False)
+    for e in rec["per_step"]:
+        assert e["free_f"] <= TOL and e["free_w"] <= TOL and e["free_nonfinite_gpu"] == 0, e
+        if "resync_f" in e:
+            assert e["resync_f"] <= TOL and e["resync_w"] <= TOL, e
+    assert rec["fused_free_f"] <= TOL and rec["fused_free_w"] <= TOL, rec
+
+
+def test_fullsize_cfg3_as_written_resynced_whole_arrays():
+    """Config 3 as written at full 64^3: steps 1-3 re-synced and free-running on the whole arrays."""
+    from parity_harness import run_protocol
+    rec = run_protocol(CONFIGS[3], {1, 2, 3}, lockstep=True, gpu_twin=False, steps=3)
+    for e in rec["per_step"]:
+        assert e["resync_f"] <= TOL and e["resync_w"] <= TOL, e
+        assert e["free_f"] <= TOL and e["free_w"] <= TOL, e
+    assert rec["fused_free_f"] <= TOL, rec

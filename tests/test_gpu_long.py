@@ -1,0 +1,75 @@
+"""The SURVEY §8(c) parity protocol at BASELINE.json's FULL sizes (long: minutes to an hour per config).
+
+Gated: runs only with PDG_PARITY_LONG=1 on a GPU box (tools/gpu/parity_long.sh), and writes its
+records to $PDG_PARITY_OUT (default gpurun_out/); the committed logs live in profiles/r02_parity/.
+The fast full-size cases that run in every `pytest -m gpu` are in test_gpu_fullsize.py.
+
+Protocol (reading C7):
+  1. re-synced one-step parity, whole arrays of f and w, <= 1e-12: every step for configs 2-3,
+     steps {1, 2, ceil(steps/2), last} for configs 4-5;
+  2. free-running parity over the full run: required <= 1e-12 for config 5 (and config 1, in the
+     fast suite); reported for configs 2-4 with the twin amplification of the map, measured in the
+     same harness (GPU twin, plus the oracle's own twin for configs 2 and 3); config 3: the last step
+     at which both runs are finite and agree to 1e-12;
+  3. stabilised twins 2s-5s (lambda = 3.5, same nu): free-running <= 1e-12 at every step;
+  4. non-physical states (rho <= 0 or non-finite) reported per step.
+"""
+import math
+import os
+
+import pytest
+
+from pdg_inputs import CONFIGS
+
+pytestmark = [pytest.mark.gpu_long,
+              pytest.mark.skipif(not os.environ.get("PDG_PARITY_LONG"), reason="full-size protocol: set PDG_PARITY_LONG=1")]
+
+TOL = 1e-12
+
+
+def _out(name):
+    d = os.environ.get("PDG_PARITY_OUT", "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    return os.path.join(d, f"parity_long_{name}.json")
+
+
+def _resync_set(cfg, every):
+    s = cfg.steps
+    return set(range(1, s + 1)) if every else {1, 2, math.ceil(s / 2), s}
+
+
+# (key, stabilised, re-sync every step, lockstep free-running solvers, oracle twin)
+CASES = {
+    "cfg2": (2, False, True, True, True),
+    "cfg3": (3, False, True, True, True),
+    "cfg4": (4, False, False, True, False),
+    "cfg5": (5, False, False, False, False),
+    "cfg2s": (2, True, True, True, False),
+    "cfg3s": (3, True, True, True, False),
+    "cfg4s": (4, True, False, True, False),
+    "cfg5s": (5, True, False, False, False),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_parity_protocol_full_size(name):
+    from parity_harness import run_protocol
+    sel = os.environ.get("PDG_PARITY_CASES")
+    if sel and name not in sel.split(","):
+        pytest.skip("not selected")
+    key, stab, every, lockstep, otwin = CASES[name]
+    cfg = CONFIGS[key].stabilised() if stab else CONFIGS[key]
+    rec = run_protocol(cfg, _resync_set(cfg, every), lockstep=lockstep, oracle_twin=otwin, gpu_twin=True,
+                       out_path=_out(name), stop_on_nonfinite=True)
+    # 1. re-synced one-step parity (every config, as long as the oracle's state is finite)
+    for e in rec["per_step"]:
+        if "resync_f" in e and e.get("nonfinite_oracle", 0) == 0:
+            assert e["resync_f"] <= TOL and e["resync_w"] <= TOL, e
+            assert e["resync_nonfinite_gpu"] == 0, e
+    # 2./3. free-running: required for config 5 and every stabilised twin
+    if stab or key == 5:
+        assert rec.get("stopped_at_step") is None
+        assert rec["fused_free_f"] <= TOL and rec["fused_free_w"] <= TOL, rec
+        for e in rec["per_step"]:
+            if "free_f" in e:
+                assert e["free_f"] <= TOL and e["free_w"] <= TOL, e

@@ -464,6 +464,65 @@ def test_m2_second_order_in_time():
     assert all(1.9 <= s <= 2.1 for s in slopes[-2:]), (errs, slopes)
 
 
+def _advection_exact_errors(dim, Ns, p=2, nu=0.5, T=0.25, lam=2.0, a=(1.0, 0.5), c=(0.35, 0.4), k=200.0,
+                            half_step=True):
+    """max |w - w_exact| at t = T for the config-1 model (vectorial D1Q2 / D2Q4, q = a w,
+    lambda = 2), Gaussian bump w0 = exp(-k |x - c|^2), mesh and dt refined together at fixed
+    nu = lambda dt / h.  The exact solution of the limit system (eq macro_limit_system) is
+    w0(x - a t) (P M2 converges to the macroscopic identity); with the bump at
+    <= 2e-11 on the inflow faces for t <= T, the inflow data f^b = f^eq(0) is exact to that
+    level.  half_step=False composes T2(dt) C2(dt) T2(dt) -- the plausible mistake of a full
+    transport step on each side -- as a negative control."""
+    errs = []
+    for N in Ns:
+        vel, comp = [], []
+        for kk in range(dim):
+            for s in (1.0, -1.0):
+                v = [0.0, 0.0, 0.0]
+                v[kk] = s * lam
+                vel.append(v)
+                comp.append(0)
+        h = 1.0 / N
+        nsteps = int(round(T / (nu * h / lam)))
+        dt = T / nsteps
+        pb = O.Problem(dim, N, p, vel, comp, 1, lam, 0, list(a[:dim]), dt)
+        xg = {1: [-1.0, 1.0], 2: [-1.0, 0.0, 1.0], 3: [-1.0, -1 / math.sqrt(5), 1 / math.sqrt(5), 1.0]}[p]
+        xs = [((np.arange(N)[:, None] + (np.asarray(xg)[None, :] + 1) / 2) * h).reshape(-1) for _ in range(dim)]
+
+        def wfield(t):
+            r2 = (xs[0] - c[0] - a[0] * t) ** 2
+            if dim == 2:
+                r2 = r2[None, :] + ((xs[1] - c[1] - a[1] * t) ** 2)[:, None]
+            return np.exp(-k * r2)[None]
+        w0 = wfield(0.0)
+        f0, fb = O.initial_data(pb, w0, np.zeros_like(w0))
+        if half_step:
+            f = O.m2_run(pb, f0, fb, nsteps)
+        else:
+            fc, fbc = pb.grid_to_cells(f0), pb.grid_to_cells(fb)
+            for _ in range(nsteps):
+                O.t2_all(pb, dt, fc, fbc)
+                O.collide(pb, fc, dt)
+                O.t2_all(pb, dt, fc, fbc)
+            f = pb.cells_to_grid(fc)
+        errs.append(float(np.max(np.abs(O.moments(pb, f) - wfield(T)))))
+    return errs
+
+
+@pytest.mark.parametrize("dim,Ns", [(1, (32, 64, 128, 256)), (2, (16, 32, 64, 128))])
+def test_m2_converges_to_exact_advection(dim, Ns):
+    """M2 at tau = 0 against an exact solution, not itself: w -> w0(x - a t) at second order
+    when h and dt are refined together; measured slopes 2.08/2.04/2.01
+    (1-D) and 2.03/2.09/2.07 (2-D).  A wrong transport step (T2(dt) instead of T2(dt/2))
+    moves the bump twice as far and does not converge at all."""
+    errs = _advection_exact_errors(dim, Ns)
+    slopes = [math.log2(errs[j] / errs[j + 1]) for j in range(len(errs) - 1)]
+    assert all(1.85 <= s <= 2.25 for s in slopes[-2:]), (errs, slopes)
+    assert errs[-1] < 3.5e-3, errs
+    bad = _advection_exact_errors(dim, Ns[-2:], half_step=False)
+    assert min(bad) > 0.3, bad
+
+
 def test_cone_evaluation_matches_full_mesh():
     """Evaluating one M2 step on dependency cones of sampled cells equals the
     full-mesh step there (used for sampled parity at full config sizes)."""
@@ -636,3 +695,29 @@ def test_gravity_m2s_second_order_in_time():
     assert all(1.75 <= s <= 2.25 for s in slopes), (e, slopes)
     e_nosrc = _gravity_error(16, dts[-1], "m2")
     assert e_nosrc > 30 * e[-1], (e_nosrc, e[-1])
+
+
+# --------------------------------------------------------------------------
+# The full-size parity harness (tests/parity_harness.py) builds the oracle's state in z-chunks
+# with inflow data only on the inflow cell layers; on small boxes it must equal oracle.m2_run
+# exactly (same oracle calls, different plumbing).
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("key,N,chunk", [(1, 8, 1 << 25), (2, 12, 1 << 25), (3, 5, 300), (4, 3, 1 << 25),
+                                         (5, 6, 2000)])
+def test_parity_harness_oracle_state_equals_m2_run(key, N, chunk):
+    import torch
+    from parity_harness import OracleRun, cells_to_grid_t, fill_w0
+    from pdg_inputs import w0_grid, wb_grid
+    cfg = CONFIGS[key].resized(N)
+    w0 = torch.empty(cfg.m * cfg.nnodes, dtype=torch.float64)
+    fill_w0(cfg, w0)
+    orun = OracleRun(cfg, w0, chunk_elems=chunk)
+    for _ in range(2):
+        orun.step()
+    pb = O.Problem.from_config(cfg)
+    wg = w0_grid(cfg)
+    f0, fb = O.initial_data(pb, wg.numpy(), wb_grid(cfg, wg).numpy())
+    ref = O.m2_run(pb, f0, fb, 2)
+    got = np.stack([cells_to_grid_t(torch.from_numpy(orun.fc[i]), orun.N, cfg.n, cfg.dim).numpy()
+                    for i in range(cfg.nv)])
+    assert np.array_equal(got, ref)
