@@ -187,6 +187,13 @@ typedef struct {
     int32_t source;              /* pdg_source_kind (PDG_SOURCE_NONE: no source) */
     const double *source_params; /* host, n_source_params values (see pdg_source_kind); copied */
     int32_t n_source_params;
+    /* Launch plan of the lattice sweeps (PDG_FLUX_LBM); zeros select the tuned
+       defaults.  The results do not depend on them (tests force small CTAs and short chain segments
+       so that the cross-CTA hand-overs and the segment halos run on small grids). */
+    int32_t lattice_cta[2];      /* warps per CTA along x and along the pipe / batch axis (both >= 1,
+                                    product <= 8); {0, 0}: default */
+    int32_t lattice_segment;     /* chain-segment rows: 0 default, < 0 never segment, > 0 this length
+                                    (used only where a halo bound exists) */
 } pdg_problem;
 
 typedef struct {
@@ -195,8 +202,8 @@ typedef struct {
     size_t w_elems;        /* doubles in w_dev  = m * nnodes_local (moments / exchange / equilibrium init) */
     size_t work_bytes;     /* bytes of work_dev (device scratch: counters, z-slab carry planes and tables,
                               lattice ticket/progress/halo counters and tagged boundary-trace words, large
-                              lattice block tables, the PDG_ASYNC_HOST upload staging); the plan-time
-                              lattice knobs (PDG_LATTICE_WARPS / _SEG / _CLUSTER) change it */
+                              lattice block tables, the PDG_ASYNC_HOST upload staging); the lattice launch
+                              plan (pdg_problem.lattice_cta / lattice_segment) changes it */
     int64_t nnodes;        /* nodes of the full grid */
     int64_t plane_stride;  /* doubles per velocity in fb */
     int32_t nv_local;      /* velocities owned by this rank */

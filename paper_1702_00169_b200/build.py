@@ -8,6 +8,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdg.so")
+# the checked build (-DPDG_CHECKED: bounds-checked global accesses, bounded cross-CTA waits,
+# csrc/pdg_check.cuh); the binding loads it when PDG_CHECKED=1
+LIB_CHECKED = os.path.join(HERE, "libpdg_checked.so")
 SOURCES = [os.path.join(SRC, "pdg_api.cu")]
 # every file under csrc/ (kernels, tables, NCCL plumbing) and the public header
 DEPS = sorted(set(SOURCES + [os.path.join(SRC, f) for f in os.listdir(SRC)
@@ -22,21 +25,22 @@ def nvcc_cmd(out=LIB, extra=()):
             "--expt-relaxed-constexpr", *extra, "-o", out, *SOURCES, "-ldl"]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = nvcc_cmd(tmp, ("-Xptxas", "-v") if verbose else ())
-        subprocess.check_call(cmd, stdout=sys.stderr if verbose else subprocess.DEVNULL)
-        os.replace(tmp, LIB)
-    return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    if force or needs_build(lib):
+        tmp = lib + f".tmp{os.getpid()}"
+        extra = (("-Xptxas", "-v") if verbose else ()) + (("-DPDG_CHECKED",) if checked else ())
+        subprocess.check_call(nvcc_cmd(tmp, extra), stdout=sys.stderr if verbose else subprocess.DEVNULL)
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

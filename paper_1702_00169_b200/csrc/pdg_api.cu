@@ -80,6 +80,8 @@ struct Geometry {
     size_t lat_ints = 0;                      // ticket + progress counters (sum over classes)
     size_t lat_xbuf = 0, lat_ybuf = 0;        // boundary trace buffers (doubles, sum over classes: the
                                               // classes run concurrently on their own streams)
+    int lat_cta[2] = {0, 0};                  // pdg_problem.lattice_cta (0: default plan)
+    int lat_seg = 0;                          // pdg_problem.lattice_segment
 };
 
 // Work decomposition of one active-axis class of lattice velocities (pdg_lattice.cuh).
@@ -87,7 +89,6 @@ struct LatPlan {
     int act = 0, d = 0, nvel = 0;
     int vel[pdg::kLatMaxVel] = {0};  // local velocity indices
     int Wx = 1, Wy = 1, ngx = 1, ngy = 1, nlane = 1, nw = 1, nc = 1, ntasks = 0;
-    int cs = 1, ntasks_c = 0;  // cluster size along the pipe axis, cluster-level tasks
     int nseg = 1, seglen = 1;  // chain segments (truncated-dependency split) and their rows
     int rcap = 1;              // chain rows per task the trace buffers hold
     size_t xbuf = 0, ybuf = 0;       // doubles
@@ -120,13 +121,11 @@ void plan_lattice(const Geometry &g, LatPlan &P)
         P.Wy = std::max(1, std::min(8, P.nw));
         P.Wx = std::max(1, std::min(8 / P.Wy, (P.nlane + 31) / 32));
     }
-    // test knob: force small CTAs so that the cross-CTA hand-over paths run on small grids
-    if (const char *e = std::getenv("PDG_LATTICE_WARPS")) {
-        int wx = 0, wy = 0;
-        if (std::sscanf(e, "%d,%d", &wx, &wy) == 2 && wx >= 1 && wy >= 1 && wx * wy <= 8) {
-            P.Wx = std::min(wx, std::max(1, (P.nlane + 31) / 32));
-            P.Wy = std::min(wy, P.nw);
-        }
+    // pdg_problem.lattice_cta: a forced CTA shape (tests run the cross-CTA hand-over paths on
+    // small grids with it)
+    if (g.lat_cta[0] >= 1 && g.lat_cta[1] >= 1) {
+        P.Wx = std::min(g.lat_cta[0], std::max(1, (P.nlane + 31) / 32));
+        P.Wy = std::min(g.lat_cta[1], P.nw);
     }
     if (P.d == 3 && g.n == 4) {  // p = 3 body diagonals: ~50 KB of shared memory per warp (no row prefetch)
         P.Wx = std::min(P.Wx, 2);
@@ -134,18 +133,6 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     }
     P.ngx = (P.nlane + 32 * P.Wx - 1) / (32 * P.Wx);
     P.ngy = (P.nw + P.Wy - 1) / P.Wy;
-    // pipe classes may use clusters of CTAs along the pipe axis (y traces through DSMEM, one
-    // cluster barrier per row); measured slower than independent CTAs on B200,
-    // so the default is 1 and PDG_LATTICE_CLUSTER=2|4|8 selects them
-    P.cs = 1;
-    if (PIPE) {
-        if (const char *e = std::getenv("PDG_LATTICE_CLUSTER")) {
-            const int v = std::atoi(e);
-            if (v == 1 || v == 2 || v == 4 || v == 8) P.cs = std::min(v, std::max(1, P.ngy));
-            if (P.cs == 3) P.cs = 2;
-        }
-    }
-    const int ngyc = (P.ngy + P.cs - 1) / P.cs;
     // Chain segments.  A class without a pipe axis whose tasks cannot fill the GPU (2-D grids:
     // one task per velocity and x group) is latency-bound by its serial chain; it is cut into
     // segments swept concurrently, each starting kHalo rows early from a zero chain trace.  The
@@ -155,11 +142,11 @@ void plan_lattice(const Geometry &g, LatPlan &P)
     // segments only change how much of the chain one task walks, not the result).
     P.nseg = 1;
     P.seglen = P.nc;
-    if (XA && !PIPE && P.cs == 1) {
+    if (XA && !PIPE) {
         // resident CTAs: 16 warps per SM on the FMA path (registers capped for 2 CTAs of 8 warps)
         const int base = P.nvel * P.ngx * P.ngy, slots = 148 * std::max(1, 16 / (P.Wx * P.Wy));
         int Ls = 0;
-        if (const char *e = std::getenv("PDG_LATTICE_SEG")) Ls = std::max(0, std::atoi(e));  // 0: off
+        if (g.lat_seg != 0) Ls = std::max(0, g.lat_seg);  // pdg_problem.lattice_segment (< 0: never)
         else if (2 * base <= slots && P.nc >= 128) {
             const int ns = std::min(slots / base, P.nc / 64);  // segments of >= 64 rows
             Ls = (P.nc + ns - 1) / ns;
@@ -170,14 +157,13 @@ void plan_lattice(const Geometry &g, LatPlan &P)
         }
     }
     P.rcap = (P.nseg > 1) ? std::min(P.nc, 2 * P.seglen) : P.nc;  // segment + a halo of at most one segment
-    P.ntasks_c = P.nvel * P.ngx * ngyc * P.nseg;
-    P.ntasks = P.ntasks_c * P.cs;  // CTA-level tasks incl. the padding of the last cluster group
+    P.ntasks = P.nvel * P.ngx * P.ngy * P.nseg;
     int mf = 1;
     for (int t = 1; t < P.d; ++t) mf *= g.n;
-    // boundary traces of up to two sweeps per launch
-    // x traces cross CTAs as tagged 64-bit words (two per double, pdg_lattice.cuh ll_put / ll_take)
-    P.xbuf = (XA && P.ngx > 1) ? (size_t)2 * P.ntasks * P.rcap * P.Wy * 2 * mf : 0;
-    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)2 * P.ntasks * P.nc * P.Wx * 32 * 2 * mf : 0;  // tagged words
+    // boundary traces: x traces cross CTAs as tagged 64-bit words (two per double, pdg_lattice.cuh
+    // ll_put / ll_take); y traces as tagged words (FMA path) or plain doubles (tensor path)
+    P.xbuf = (XA && P.ngx > 1) ? (size_t)P.ntasks * P.rcap * P.Wy * 2 * mf : 0;
+    P.ybuf = (PIPE && P.ngy > 1) ? (size_t)P.ntasks * P.nc * P.Wx * 32 * 2 * mf : 0;
     P.xbuf = (P.xbuf + 1) & ~(size_t)1;  // keep every slice 16-byte aligned
 }
 
@@ -264,6 +250,12 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     }
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return fail(PDG_E_INVALID_ARGUMENT, "bad rank/nranks");
     g->async_host = (p->flags & PDG_ASYNC_HOST) ? 1 : 0;
+    if (p->lattice_cta[0] < 0 || p->lattice_cta[1] < 0 || p->lattice_cta[0] * p->lattice_cta[1] > 8 ||
+        ((p->lattice_cta[0] == 0) != (p->lattice_cta[1] == 0)))
+        return fail(PDG_E_INVALID_ARGUMENT, "lattice_cta: both 0 (default) or both >= 1 with a product <= 8");
+    g->lat_cta[0] = p->lattice_cta[0];
+    g->lat_cta[1] = p->lattice_cta[1];
+    g->lat_seg = p->lattice_segment;
     g->dim = p->dim;
     g->p = p->degree;
     g->n = p->degree + 1;
@@ -651,7 +643,7 @@ const pdg::LatticeBlockLD *lattice_block_for(pdg_ctx *c, int act, double dtp)
     return &(c->lat_blocks[key] = std::move(B));
 }
 
-template <int D, int N, int ACT, int NPASS, int CS>
+template <int D, int N, int ACT>
 pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, double dtp, cudaStream_t st)
 {
     using PP = pdg::LatParams<D, N, ACT>;
@@ -667,6 +659,10 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.hdone = P.progress + (size_t)8 * pl.ntasks;
     P.xbuf = c->lat_xbuf + pl.xbuf_off;
     P.ybuf = c->lat_ybuf + pl.ybuf_off;
+    P.f_elems = (int64_t)g.nvl * g.nnodes;
+    P.fb_elems = (int64_t)g.nvl * g.nplanes * g.plane_stride;
+    P.xbuf_elems = (int64_t)pl.xbuf;
+    P.ybuf_elems = (int64_t)pl.ybuf;
     for (int k = 0; k < 3; ++k) {
         P.g.L[k] = g.L[k];
         P.g.stride[k] = g.stride[k];
@@ -681,7 +677,6 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     P.g.nw = pl.nw;
     P.g.nc = pl.nc;
     P.g.ntasks = pl.ntasks;
-    P.g.ntasks_c = pl.ntasks_c;
     // chain segments: the halo depth of this (class, dt') from the norm bound, or unsegmented
     P.g.nseg = 1;
     P.g.seglen = pl.nc;
@@ -693,15 +688,14 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
         int h = -1;
         if (hi != c->lat_halo.end()) h = hi->second;
         else h = c->lat_halo[hk] = pdg::lattice_chain_halo(B, 1, pl.seglen);
-        if (h > 0 && NPASS * h <= pl.seglen) {
+        if (h > 0 && h <= pl.seglen) {
             P.g.nseg = pl.nseg;
             P.g.seglen = pl.seglen;
-            P.g.halo = NPASS * h;  // two sweeps per launch: the second one's input is exact after h rows
+            P.g.halo = h;
             P.g.rcap = pl.rcap;
         }
     }
-    P.g.ntasks_c = pl.ntasks_c / pl.nseg * P.g.nseg;
-    P.g.ypf = std::getenv("PDG_LATTICE_NOYPF") ? 0 : 1;
+    P.g.ntasks = pl.ntasks / pl.nseg * P.g.nseg;
     // scan rounds: round j adds Bx^(2^j) times an earlier lane's out-trace; once the infinity
     // norm of that power is below 2^-64 the term cannot change an fp64 result, nor can any later
     // (smaller) power
@@ -767,90 +761,49 @@ pdg_status launch_lattice_t(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlo
     // cp.async row buffers + the y hand-over buffers (pdg_lattice.cuh)
     const size_t smem =
         sizeof(double) * ((size_t)(threads / 32) * pdg::LatRing<D, N, DA>::RING * TB::NB * 32 +
-                          (PIPE ? (size_t)NPASS * 2 * 32 * TB::MF * (CS > 1 ? threads / 32 : threads / 32 - pl.Wx) : 0) +
+                          (PIPE ? (size_t)2 * 32 * TB::MF * (threads / 32 - pl.Wx) : 0) +
                           pdg::LatMma<D, N, ACT>::smem_doubles(threads / 32) +
-                          (PIPE ? (size_t)NPASS * pl.Wx * 32 * 2 * TB::MF : 0));
+                          (PIPE ? (size_t)pl.Wx * 32 * 2 * TB::MF : 0));
     // per-context (hence per-device, per-thread) cache of the shared-memory opt-in and occupancy
-    auto kern = pdg::lattice_sweep_kernel<D, N, ACT, NPASS, CS>;
+    auto kern = pdg::lattice_sweep_kernel<D, N, ACT>;
     const void *kfn = reinterpret_cast<const void *>(kern);
-    cudaLaunchConfig_t lc = {};
-    cudaLaunchAttribute la[1];
-    lc.blockDim = dim3((unsigned)threads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = st;
-    la[0].id = cudaLaunchAttributeClusterDimension;
-    la[0].val.clusterDim.x = CS;
-    la[0].val.clusterDim.y = 1;
-    la[0].val.clusterDim.z = 1;
-    lc.attrs = la;
-    lc.numAttrs = (CS > 1) ? 1 : 0;
     const auto key = std::make_tuple(kfn, threads, smem);
     auto oc = c->launch_cache.find(key);
-    int occ = 0;  // resident CTAs (CS = 1) or clusters (CS > 1) on the whole GPU
+    int occ = 0;  // resident CTAs on the whole GPU (persistent kernel: one grid of resident CTAs)
     if (oc != c->launch_cache.end()) occ = oc->second;
     else {
         const cudaError_t ea = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess)
             return fail(PDG_E_CUDA, std::string("lattice sweep shared memory opt-in: ") + cudaGetErrorString(ea));
-        if (CS > 1) {
-            lc.gridDim = dim3((unsigned)(CS * c->sms));
-            if (cudaOccupancyMaxActiveClusters(&occ, kern, &lc) != cudaSuccess) occ = 1;
-        } else {
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
-            occ *= c->sms;
-        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
+        occ *= c->sms;
         cudaGetLastError();
         occ = std::max(1, occ);
         c->launch_cache[key] = occ;
     }
-    const int units = std::max(1, std::min(P.g.ntasks_c, occ));
-    lc.gridDim = dim3((unsigned)(units * CS));
+    const int units = std::max(1, std::min(P.g.ntasks, occ));
     PDG_CUDA_TRY(cudaMemsetAsync(P.ticket, 0, sizeof(int) * ((size_t)9 * pl.ntasks + 1), st));
-    PDG_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, P));
+    kern<<<units, threads, smem, st>>>(P);
     return PDG_OK;
 }
 
-// cluster size dispatch (pipe classes only: 3-D with y and z active)
-template <int D, int N, int ACT, int NPASS>
-pdg_status launch_lattice_cs(pdg_ctx *c, const LatPlan &pl, const pdg::LatticeBlockLD &B, double dtp, cudaStream_t st)
-{
-    if constexpr (pdg::LatShape<D, ACT>::PIPE) {
-        if (pl.cs == 2) return launch_lattice_t<D, N, ACT, NPASS, 2>(c, pl, B, dtp, st);
-        if (pl.cs == 4) return launch_lattice_t<D, N, ACT, NPASS, 4>(c, pl, B, dtp, st);
-        if (pl.cs == 8) return launch_lattice_t<D, N, ACT, NPASS, 8>(c, pl, B, dtp, st);
-    }
-    return launch_lattice_t<D, N, ACT, NPASS, 1>(c, pl, B, dtp, st);
-}
-
-// One pass over the velocities of class `pl` applying T2(dtp) npass times: the FMA-path classes
-// (two active axes in 3-D) take both sweeps in one launch, the others one each.
+// One pass over the velocities of class `pl` applying T2(dtp) npass times, one sweep per launch
+// (two sweeps per launch measured slower once the hand-overs were tagged).
 pdg_status launch_lattice(pdg_ctx *c, const LatPlan &pl, double dtp, cudaStream_t st, int npass)
 {
     const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, dtp);
     if (!B) return fail(PDG_E_INVALID_ARGUMENT, "singular lattice block for this dt");
     const int D = c->g.dim, n = c->g.n, a = pl.act;
-    // (2-D grids are latency-bound: one sweep per launch keeps the per-row chain short)
-    // PDG_LATTICE_FUSE: bit mask over the active-axis masks whose two sweeps share one launch.
-    // Default none: with the tagged hand-over the single-sweep launches are fast enough that the
-    // fused variant (twice the per-row chain, register spills) loses (D3Q19 128^3: 8.93 ms per
-    // step fused, 8.24 ms unfused; tools/gpu/fuse.sh)
-    int fuse_mask = 0;
-    if (const char *e = std::getenv("PDG_LATTICE_FUSE")) fuse_mask = std::atoi(e);
-    const bool fused = (npass == 2 && popcount3(a) < 3 && D == 3 && ((fuse_mask >> a) & 1));
-    for (int q = 0; q < (fused ? 1 : npass); ++q) {
+    for (int q = 0; q < npass; ++q) {
         const int e = prof_begin(c, st);
         pdg_status s = PDG_E_UNSUPPORTED;
-#define PDG_LAT(DD, NN, AA, NP) \
-    else if (D == DD && n == NN && a == AA && (fused ? 2 : 1) == NP) s = launch_lattice_cs<DD, NN, AA, NP>(c, pl, *B, dtp, st)
+#define PDG_LAT(DD, NN, AA) else if (D == DD && n == NN && a == AA) s = launch_lattice_t<DD, NN, AA>(c, pl, *B, dtp, st)
         if (false) {}
-        PDG_LAT(2, 2, 3, 1); PDG_LAT(2, 3, 3, 1); PDG_LAT(2, 4, 3, 1);
-        PDG_LAT(3, 2, 3, 1); PDG_LAT(3, 3, 3, 1); PDG_LAT(3, 4, 3, 1);
-        PDG_LAT(3, 2, 5, 1); PDG_LAT(3, 3, 5, 1); PDG_LAT(3, 4, 5, 1);
-        PDG_LAT(3, 2, 6, 1); PDG_LAT(3, 3, 6, 1); PDG_LAT(3, 4, 6, 1);
-        PDG_LAT(3, 2, 7, 1); PDG_LAT(3, 3, 7, 1); PDG_LAT(3, 4, 7, 1);
-        PDG_LAT(3, 2, 3, 2); PDG_LAT(3, 3, 3, 2); PDG_LAT(3, 4, 3, 2);
-        PDG_LAT(3, 2, 5, 2); PDG_LAT(3, 3, 5, 2); PDG_LAT(3, 4, 5, 2);
-        PDG_LAT(3, 2, 6, 2); PDG_LAT(3, 3, 6, 2); PDG_LAT(3, 4, 6, 2);
+        PDG_LAT(2, 2, 3); PDG_LAT(2, 3, 3); PDG_LAT(2, 4, 3);
+        PDG_LAT(3, 2, 3); PDG_LAT(3, 3, 3); PDG_LAT(3, 4, 3);
+        PDG_LAT(3, 2, 5); PDG_LAT(3, 3, 5); PDG_LAT(3, 4, 5);
+        PDG_LAT(3, 2, 6); PDG_LAT(3, 3, 6); PDG_LAT(3, 4, 6);
+        PDG_LAT(3, 2, 7); PDG_LAT(3, 3, 7); PDG_LAT(3, 4, 7);
 #undef PDG_LAT
         if (s == PDG_E_UNSUPPORTED) return fail(s, "lattice sweep not compiled for this (dim, degree, axes)");
         if (s != PDG_OK) return s;
@@ -1036,12 +989,9 @@ void launch_relax_lbm_t(pdg_ctx *c, pdg::LocalOps op)
 {
     const unsigned grid = grid_all(c->g.nnodes, 256);
     const int e = prof_begin(c);
-    // two-phase kernel (moments, then an L1 re-read per update): 0.90-0.99 -> 1.01-1.03 of the
-    // measured copy bandwidth on the 3-D sets (tools/gpu/relax2.sh); PDG_LBM_RELAX2=0 selects the
-    // one-read kernel
-    static const int two = std::getenv("PDG_LBM_RELAX2") ? std::atoi(std::getenv("PDG_LBM_RELAX2")) : 1;
-    if (two) pdg::relax_lbm2_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
-    else pdg::relax_lbm_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
+    // two-phase kernel (moments, then an L1 re-read per update): 1.01-1.03 of the measured copy
+    // bandwidth on the 3-D sets against 0.90-0.99 for a one-read kernel (tools/gpu/relax2.sh, round 1)
+    pdg::relax_lbm2_kernel<D, NV><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->lbm, op);
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
 }
 
@@ -1190,6 +1140,8 @@ pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
     std::memset(&P, 0, sizeof(P));
     P.f = c->f;
     P.fb = c->fb;
+    P.f_elems = (int64_t)c->g.nvl * c->g.nnodes;
+    P.fb_elems = (int64_t)c->g.nvl * c->g.nplanes * c->g.plane_stride;
     P.nnodes = c->g.nnodes;
     P.plane_stride = c->g.plane_stride;
     P.ncx = (int32_t)c->g.ncell[0];
@@ -1311,6 +1263,9 @@ void build_sweep_params(pdg_ctx *c)
     for (auto *sp : {&c->x_params, &c->yz_params, &c->all_params}) {
         sp->f = c->f;
         sp->fb = c->fb;
+        sp->f_elems = (int64_t)g.nvl * g.nnodes;
+        sp->fb_elems = (int64_t)g.nvl * g.nplanes * g.plane_stride;
+        sp->cout_elems = (int64_t)g.carry_doubles;
     }
     if (g.lattice) {
         // lattice set: single-axis velocities take the line sweeps, diagonal ones the
@@ -1478,6 +1433,9 @@ pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
     P.carry = c->zcarry;
     P.inflow = c->zinflow;
     P.f = c->f;
+    P.f_elems = (int64_t)g.nvl * g.nnodes;
+    P.carry_elems = (int64_t)g.carry_doubles;
+    P.table_elems = (int64_t)g.table_doubles;
     P.table = c->ztables + (size_t)zt->slot * g.table_doubles;
     P.plane = g.nnodes / g.L[g.outer];
     P.nnodes = g.nnodes;
@@ -1633,7 +1591,7 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
                 for (const Op &o : ops) {
                     if (o.kind != 0) continue;
                     const pdg::LatticeBlockLD *B = lattice_block_for(c, pl.act, o.h);
-                    pdg_status ps = B ? launch_lattice_t<3, 4, 7, 1, 1>(c, pl, *B, o.h, nullptr)
+                    pdg_status ps = B ? launch_lattice_t<3, 4, 7>(c, pl, *B, o.h, nullptr)
                                       : fail(PDG_E_INVALID_ARGUMENT, "singular lattice block");
                     if (ps != PDG_OK) {
                         pdg_destroy(c);

@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pdg_check.cuh"
+
 namespace pdg {
 
 constexpr int kMaxVel = 32;
@@ -48,6 +50,7 @@ struct SweepParams {
     double *f;
     const double *fb;
     double *cout;     // outgoing carries of slab sweeps (z-slab decomposition)
+    int64_t f_elems, fb_elems, cout_elems;  // buffer bounds (checked build)
     DevBlock blk[3];  // per axis (kappa_k = lambda dt' / h_k)
     int32_t nvel;
     SweepVel v[kMaxVel];
@@ -147,7 +150,11 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
     const int64_t Lk = (int64_t)V.ncells * N;
     const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
     const int64_t step = (V.sign > 0) ? V.inner : -V.inner;
-    double *p = P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    const int64_t p_at = V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);  // element index of p
+    double *p = P.f + p_at;
+    // the line's first and last nodes bound every access of the walk
+    PDG_CHECK_IDX(p_at, P.f_elems, "sweep_strided f");
+    PDG_CHECK_IDX(p_at + (Lk - 1) * step, P.f_elems, "sweep_strided f");
 
     double M[N * N], g[N];
 #pragma unroll
@@ -157,6 +164,7 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
 
     double carry[NPASS];
     // ghost cell: f^b old + f^b new (reading C5); a slab interior start has zero inflow
+    if (!V.zero_inflow) PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided fb");
     const double s0 = V.zero_inflow ? 0.0 : 2.0 * P.fb[V.fb_off + line];
 #pragma unroll
     for (int q = 0; q < NPASS; ++q) carry[q] = s0;
@@ -204,7 +212,10 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
     }
     if (V.cout_off >= 0) {
 #pragma unroll
-        for (int q = 0; q < NPASS; ++q) P.cout[V.cout_off + q * V.nlines + line] = carry[q];
+        for (int q = 0; q < NPASS; ++q) {
+            PDG_CHECK_IDX(V.cout_off + q * V.nlines + line, P.cout_elems, "sweep_strided cout");
+            P.cout[V.cout_off + q * V.nlines + line] = carry[q];
+        }
     }
 }
 
@@ -228,7 +239,13 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
     const int64_t ln = active ? line : 0;
     const int64_t base = (ln / V.inner) * (V.inner * Lk) + (ln % V.inner);
     const int64_t step = (V.sign > 0) ? V.inner : -V.inner;
-    double *p0 = P.f + V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    const int64_t p_at = V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    double *p0 = P.f + p_at;
+    if (active) {
+        PDG_CHECK_IDX(p_at, P.f_elems, "sweep_strided_seg f");
+        PDG_CHECK_IDX(p_at + (Lk - 1) * step, P.f_elems, "sweep_strided_seg f");
+        if (!V.zero_inflow) PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided_seg fb");
+    }
     const int ks = (V.ncells + nseg - 1) / nseg;
     const int c0 = min(V.ncells, sg * ks), c1 = min(V.ncells, c0 + ks);
 
@@ -276,7 +293,10 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
 #pragma unroll
                 for (int a = 0; a < N; ++a) p0[((int64_t)c * N + a) * step] = fn[a];
             }
-            if (V.cout_off >= 0 && c1 == V.ncells && c0 < c1) P.cout[V.cout_off + q * V.nlines + line] = s;
+            if (V.cout_off >= 0 && c1 == V.ncells && c0 < c1) {
+                PDG_CHECK_IDX(V.cout_off + q * V.nlines + line, P.cout_elems, "sweep_strided_seg cout");
+                P.cout[V.cout_off + q * V.nlines + line] = s;
+            }
         }
         __syncthreads();
     }
@@ -392,6 +412,7 @@ __device__ __forceinline__ void warp_line_sweep(double *row, int ncells, bool up
 struct RelaxXParams {
     double *f;
     const double *fb;
+    int64_t f_elems, fb_elems;  // buffer bounds (checked build)
     int64_t nnodes;
     int64_t plane_stride;
     int32_t ncx;  // cells along x
@@ -419,6 +440,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
     const int64_t line = blockIdx.x;
     const int64_t base = line * Lx;
     const int64_t nn = P.nnodes;
+    PDG_CHECK_IDX(base + (NV - 1) * nn + Lx - 1, P.f_elems, "relax_xsweep f");  // the line's last node
 
     // phase 1: collision at every node of the line
     for (int X = threadIdx.x; X < Lx; X += blockDim.x) {
@@ -457,6 +479,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
     for (int v = warp; v < 2 * M; v += nwarps) {
         const int c = v >> 1, s = v & 1;
         const int i = c * 2 * DIM + s;
+        PDG_CHECK_IDX(i * P.plane_stride + line, P.fb_elems, "relax_xsweep fb");
         const double s0 = 2.0 * P.fb[i * P.plane_stride + line];  // ghost: f^b old + new
         warp_line_sweep<N, NPASS, K>(sx + v * Lp, P.ncx, s == 0, Mb, gb, s0, lane);
     }
@@ -488,6 +511,8 @@ __global__ void __launch_bounds__(kXsWarps * 32) sweep_x_kernel(const SweepParam
     const int64_t line = (int64_t)blockIdx.x * kXsWarps + warp;
     if (line >= V.nlines) return;  // warp-uniform
     double *row = P.f + V.f_off + line * (int64_t)V.ncells * N;
+    PDG_CHECK_IDX(V.f_off + (line + 1) * (int64_t)V.ncells * N - 1, P.f_elems, "sweep_x f");
+    PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_x fb");
     double *buf = sbuf[warp];
     const unsigned FULL = 0xffffffffu;
 
@@ -723,6 +748,7 @@ struct ZSlabParams {
     const double *carry;   // [slab][vel][2][plane] outgoing carries of the slab sweeps
     double *inflow;        // [slab][vel][2][plane] exact inflows (output of the scan)
     double *f;
+    int64_t f_elems, carry_elems, table_elems;  // buffer bounds (checked build; inflow has carry_elems)
     const double *table;   // P[lmax][n], Q[lmax][n]
     double B[64], C[64];   // per global slab: beta^len, pass-2 carry response
     int64_t plane;         // lines per slab
@@ -744,6 +770,7 @@ __global__ void __launch_bounds__(256) zslab_scan_kernel(const ZSlabParams P)
     const int first = up ? 0 : P.nslab - 1;
     const int64_t vstride = 2 * P.plane;
     const int64_t sstride = (int64_t)P.nvo * vstride;
+    PDG_CHECK_IDX((int64_t)(P.nslab - 1) * sstride + j * vstride + P.plane + line, P.carry_elems, "zslab_scan carry");
     double c1 = P.carry[first * sstride + j * vstride + line];
     double c2 = (P.npass > 1) ? P.carry[first * sstride + j * vstride + P.plane + line] : 0.0;
     for (int k = 1; k < P.nslab; ++k) {
@@ -775,6 +802,8 @@ __global__ void __launch_bounds__(256) zslab_correct_kernel(const ZSlabParams P)
     const int ncell = P.cells[s];
     const int lend = min(ncell, P.leff);
     double *col = P.f + (int64_t)P.vel[j] * P.nnodes + line;  // the outer axis is the slowest: base = line
+    PDG_CHECK_IDX(o + P.plane, P.carry_elems, "zslab_correct inflow");
+    PDG_CHECK_IDX((int64_t)(lend > 0 ? lend : 1) * N - 1 + P.lmax * N, P.table_elems, "zslab_correct table");
     const double *Pt = P.table;
     const double *Qt = P.table + (int64_t)P.lmax * N;
     for (int l = 0; l < lend; ++l) {
@@ -783,6 +812,7 @@ __global__ void __launch_bounds__(256) zslab_correct_kernel(const ZSlabParams P)
         for (int a = 0; a < N; ++a) {
             const int am = up ? a : N - 1 - a;
             double *ptr = col + ((int64_t)cell * N + am) * P.inner;
+            PDG_CHECK_IDX(ptr - P.f, P.f_elems, "zslab_correct f");
             double corr = Qt[l * N + a] * ((P.npass > 1) ? S2 : S1);
             if (P.npass > 1) corr = fma(Pt[l * N + a], S1, corr);
             *ptr += corr;

@@ -32,15 +32,16 @@
 //     the kernel parameter space, on the tensor path (body diagonals, DMMA.8x8x4) from
 //     shared memory.
 //
-//  relax_lbm2_kernel<D, NV> (default) / relax_lbm_kernel<D, NV>: collision fused with the
+//  relax_lbm2_kernel<D, NV>: collision fused with the
 //  moments w = (rho, rho u) = P f, P = [1; v^T],
 //  f^eq_i = w_i rho (1 + u.v_i/c^2 + (u.v_i)^2/(2c^4) - u.u/(2c^2)),
 //  f <- ca f + cb f^eq (eq collision_cn).
 #pragma once
-#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <type_traits>
+
+#include "pdg_check.cuh"
 
 namespace pdg {
 
@@ -114,10 +115,8 @@ struct LatGeom {
     int32_t nlane;       // x cells (x active) or x nodes
     int32_t nw;          // pipe cells, batch nodes or 1
     int32_t nc;          // chain cells
-    int32_t ntasks;      // CTA-level tasks (pipe groups padded to a multiple of the cluster size)
+    int32_t ntasks;      // tasks: (segment, pipe group, velocity, x group)
     int32_t nvel;
-    int32_t ntasks_c;    // cluster-level tasks (== ntasks without clusters)
-    int32_t ypf;         // 1: prefetch the previous CTA's y traces one row ahead
     int32_t nscan;       // x-scan rounds carrying weight: round j is dropped when |Bx^(2^j)| < 2^-64
     int32_t nseg;        // chain segments (1: the whole chain per task)
     int32_t seglen;      // chain rows stored by one segment
@@ -134,9 +133,10 @@ struct LatParams {
     int *ticket;     // [0]; progress counters follow: progress[task * 8 + x-warp] = rows published (tensor-path y traces)
     int *progress;
     int *hdone;      // [task]: 1 once the segment has read its halo rows (their old values)
-    double *xbuf;    // [task][row][pass][Wy][2 MF] tagged x out-trace words at CTA boundaries
-    double *ybuf;    // [task][row][pass][Wx][32][2 MF] tagged y out-trace words at CTA boundaries (FMA
+    double *xbuf;    // [task][row][Wy][2 MF] tagged x out-trace words at CTA boundaries
+    double *ybuf;    // [task][row][Wx][32][2 MF] tagged y out-trace words at CTA boundaries (FMA
                      // path; the tensor path stores plain doubles with an MF rounded up to even stride)
+    int64_t f_elems, fb_elems, xbuf_elems, ybuf_elems, ints_elems;  // buffer bounds (checked build)
     LatGeom g;
     LatVel v[kLatMaxVel];
     typename LatTabSel<N, S::DA>::type tab;
@@ -192,11 +192,8 @@ template <int D, int N, int ACT>
 struct LatMma {
     using S = LatShape<D, ACT>;
     static constexpr int NB = ipow(N, S::DA), MF = NB / N;
-#ifdef PDG_LATTICE_MMA_ALL
-    static constexpr bool USE = true;
-#else
+    // (the two-axis classes on the tensor path measured slower: their 9-row block pads to 16)
     static constexpr bool USE = (S::DA == 3);
-#endif
     static constexpr int MT = (NB + 7) / 8;                     // 8-row tiles of the block
     // the first product is A^{-1} r with the rhs r = 2 f_old + sum_t (kappa_t/omega_0) E_in^(t) s_t of
     // the chain and pipe in-traces (M = A^{-1}(2I - A) = 2 A^{-1} - I, Q_t = A^{-1} E_in^(t) kappa_t/omega_0)
@@ -229,7 +226,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ void wait_progress(const int *p, int need)
 {
     if (ld_acquire(p) >= need) return;
-    while (ld_acquire(p) < need) __nanosleep(64);
+    PDG_SPIN_DECL(spins);
+    while (ld_acquire(p) < need) {
+        __nanosleep(64);
+        PDG_SPIN_TICK(spins, "lattice wait_progress");
+    }
 }
 
 // Index of a node (given by its flow coordinates u[] on every axis) in the inflow plane of
@@ -250,7 +251,8 @@ __device__ __forceinline__ const double *ghost_ptr(const LatParams<D, N, ACT> &P
 {
     using S = LatShape<D, ACT>;
     constexpr int T = S::t_of(K);
-    const double *pl = P.fb + V.fb_off + (int64_t)K * P.g.plane_stride;
+    const int64_t pl_at = V.fb_off + (int64_t)K * P.g.plane_stride;
+    const double *pl = P.fb + pl_at;
     const int r = (j % ipow(N, T)) + (j / ipow(N, T)) * ipow(N, T + 1);  // digit T = 0
     int64_t ph[3] = {0, 0, 0};
 #pragma unroll
@@ -261,6 +263,7 @@ __device__ __forceinline__ const double *ghost_ptr(const LatParams<D, N, ACT> &P
         if (ta >= 0 && V.sign[a] < 0) u = P.g.L[a] - 1 - u;
         ph[a] = u;
     }
+    PDG_CHECK_IDX(pl_at + plane_index<D>(P.g, K, ph), P.fb_elems, "lattice ghost fb");
     return pl + plane_index<D>(P.g, K, ph);
 }
 
@@ -321,6 +324,7 @@ template <int MF>
 __device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_t tag)
 {
     uint64_t w[2 * MF];
+    PDG_SPIN_DECL(spins);
     for (;;) {
 #pragma unroll
         for (int j = 0; j < MF; ++j) ll_load2(slot + 2 * j, w[2 * j], w[2 * j + 1]);
@@ -329,6 +333,7 @@ __device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_
         for (int k = 0; k < 2 * MF; ++k) ok = ok && (uint32_t)(w[k] >> 32) == tag;
         if (ok) break;
         __nanosleep(20);
+        PDG_SPIN_TICK(spins, "lattice ll_take");
     }
 #pragma unroll
     for (int j = 0; j < MF; ++j) {
@@ -337,21 +342,14 @@ __device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_
     }
 }
 
-// NPASS = 2 applies T2 twice in one pass over f (step n's trailing and step n+1's leading
-// T2(dt/2), as the line sweeps do; both sweeps keep their own traces and hand-overs, the
-// second sweep reads the first one's output from registers).  Registers are capped for two
-// CTAs per SM on the FMA path (the two-sweep variant spills a few bytes, measured faster than
-// one CTA per SM without spills); the tensor path (body diagonals, NPASS = 1) needs ~218 KB of
-// shared memory and runs one CTA per SM.
-// CS > 1: thread-block clusters of CS CTAs along the pipe axis (consecutive pipe groups): the
-// y hand-over between the cluster's CTAs goes through distributed shared memory and the
-// cluster advances in lockstep (one cluster barrier per row); global traces and progress
-// flags remain only at cluster boundaries.
-template <int D, int N, int ACT, int NPASS, int CS>
+// One T2(dt') per launch.  Registers are capped for two CTAs per SM on the FMA path; the tensor
+// path (body diagonals) needs ~218 KB of shared memory and runs one CTA per SM.  (Measured and
+// dropped in round 1: two sweeps per launch, thread-block clusters along the pipe
+// axis, the tensor path for the two-axis classes.)
+template <int D, int N, int ACT>
 __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
-    namespace cg = cooperative_groups;
     using S = LatShape<D, ACT>;
     using TB = LatTab<N, S::DA>;
     constexpr int DA = S::DA, NB = TB::NB, MF = TB::MF;
@@ -363,7 +361,6 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // rows prefetched ahead with cp.async: 2-D diagonals are latency-bound (short rows, one warp
     // per SM sub-partition), so they look three rows ahead; 3-D classes one row
     constexpr int PFA = LatRing<D, N, S::DA>::PFA, RING = LatRing<D, N, S::DA>::RING;
-    static_assert(!(USE_MMA && NPASS == 2), "the tensor path runs one sweep per launch");
     // [row][32 units] shared buffers (row buffers, staging): the tensor path XOR-swizzles the unit
     // index with 4 (row mod 4), so the four rows of a DMMA B fragment (lane % 4) and the eight
     // accumulator rows of a spill fall on different bank pairs
@@ -377,27 +374,24 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // x hand-over slots between the x-warps of a CTA: a ring of XR rows; with the point-to-point
     // sync of the pipe classes a producer may run XR - 1 rows ahead of its x consumer
     constexpr int XR = PIPE ? 4 : 2;
-    __shared__ double xs[NPASS][XR][8][XA ? MF : 1];
+    __shared__ double xs[XR][8][XA ? MF : 1];
     __shared__ double gxs[8][RING][XA ? MF : 1];  // x inflow ghosts of the first x warp, prefetched per row
     __shared__ int s_task;
     __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
     // dynamic shared memory: per-warp double buffer of the unit values of the current and the next
     // row (cp.async prefetch: the loads of row r+1 do not depend on the carries and overlap row r's
-    // math), then the y hand-over buffers [pass][2][nys warps][32][MF] (PIPE)
+    // math), then the y hand-over buffers [2][nys warps][32][MF] (PIPE)
     extern __shared__ double sfo[];  // [warp][RING][NB][32]
     const int nwarps = blockDim.x >> 5;
     double *ysb = sfo + (size_t)nwarps * RING * NB * 32;
-    // y hand-over slots only for warps with a reader in this CTA (all warps with clusters: the next
-    // CTA of the cluster reads the last pipe warps through DSMEM)
-    const int nys = (CS > 1) ? nwarps : nwarps - P.g.Wx;
-    auto YS = [&](int ps, int buf, int w, int l) -> double * {
-        return ysb + ((((size_t)ps * 2 + buf) * nys + w) * 32 + l) * MF;
-    };
+    // y hand-over slots only for warps with a reader in this CTA
+    const int nys = nwarps - P.g.Wx;
+    auto YS = [&](int buf, int w, int l) -> double * { return ysb + (((size_t)buf * nys + w) * 32 + l) * MF; };
     // (tensor path) per-warp staging rows [NB][32], then the A operands [M|Qc|Qp] and Qx
-    double *stg_base = ysb + (PIPE ? (size_t)NPASS * 2 * nys * 32 * MF : 0);
+    double *stg_base = ysb + (PIPE ? (size_t)2 * nys * 32 * MF : 0);
     double *sA = stg_base + (USE_MMA ? (size_t)nwarps * NB * 32 : 0);
     double *sAx = sA + (size_t)MT * 8 * MMA::SA;
-    // (pipe classes) tagged y-trace words of the previous CTA prefetched for the next row: [pass][Wx][32][2 MF]
+    // (pipe classes) tagged y-trace words of the previous CTA prefetched for the next row: [Wx][32][2 MF]
     double *spy = USE_MMA ? sAx + (size_t)MT * 8 * KSX * 4 : stg_base;
     if constexpr (USE_MMA) {
         for (int i = threadIdx.x; i < MT * 8 * KS * 4; i += blockDim.x) {
@@ -417,9 +411,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     const LatGeom &g = P.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qx = warp % g.Wx, wy = warp / g.Wx;
-    const int crank = (CS > 1) ? (int)cg::this_cluster().block_rank() : 0;
-    const int skew = (XA ? qx : 0) + (PIPE ? crank * g.Wy + wy : 0);
-    const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? CS * g.Wy - 1 : 0);
+    const int skew = (XA ? qx : 0) + (PIPE ? wy : 0);
+    const int maxskew = (XA ? g.Wx - 1 : 0) + (PIPE ? g.Wy - 1 : 0);
     // Per-row synchronisation.  Without a pipe axis and with one CTA along x, the warp groups of
     // different batch indices (wy) are independent: each group of Wx skewed x-warps syncs on its
     // own named barrier, and no other CTA reads this task's progress.
@@ -432,19 +425,31 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     // (tensor-path y traces: each producing warp publishes its own row progress, per (task, x-warp))
     uint64_t *const xll = reinterpret_cast<uint64_t *>(P.xbuf);
     uint64_t *const yll = reinterpret_cast<uint64_t *>(P.ybuf);
-    // tagged y-trace words of (task, row, pass) for this lane: [task][row][pass][Wx][32][2 MF]
-    auto ylslot = [&](int tk, int row, int ps) -> int64_t {
-        return (((((int64_t)tk * g.rcap + row) * NPASS + ps) * g.Wx + qx) * 32 + lane) * 2 * MF;
+    // tagged y-trace words of (task, row) for this lane: [task][row][Wx][32][2 MF]
+    auto ylslot = [&](int tk, int row) -> int64_t {
+        const int64_t o = ((((int64_t)tk * g.rcap + row) * g.Wx + qx) * 32 + lane) * 2 * MF;
+        PDG_CHECK_IDX(o + 2 * MF - 1, P.ybuf_elems, "lattice y trace slot");
+        return o;
     };
-    // Otherwise (pipe classes, CS = 1) warps sync point to point through shared-memory step
+    // tagged x-trace words of (task, row) for the warp's pipe index: [task][row][Wy][2 MF]
+    auto xlslot = [&](int tk, int row) -> int64_t {
+        const int64_t o = (((int64_t)tk * g.rcap + row) * g.Wy + wy) * 2 * MF;
+        PDG_CHECK_IDX(o + 2 * MF - 1, P.xbuf_elems, "lattice x trace slot");
+        return o;
+    };
+    // Otherwise (pipe classes) warps sync point to point through shared-memory step
     // counters instead of a CTA-wide barrier: before step t a warp needs its producers (x-1, y-1)
     // and its consumers (x+1, y+1) to have finished step t-1 (the consumers have then read the
     // double-buffered slot this step overwrites).  Warps may drift apart within that slack.
-    const bool p2p = (CS == 1) && PIPE;
+    const bool p2p = PIPE;
     volatile int *vdone = s_done;
     auto wait_done = [&](int w, int t_need) {
         if (vdone[w] >= t_need) return;
-        while (vdone[w] < t_need) __nanosleep(16);
+        PDG_SPIN_DECL(spins);
+        while (vdone[w] < t_need) {
+            __nanosleep(16);
+            PDG_SPIN_TICK(spins, "lattice wait_done");
+        }
     };
     auto step_begin = [&](int t) {
         if (!p2p || t == 0) return;
@@ -458,8 +463,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         __threadfence_block();
     };
     auto step_sync = [&](int t) {
-        if constexpr (CS > 1) cg::this_cluster().sync();
-        else if (group_sync) asm volatile("bar.sync %0, %1;" ::"r"(1 + wy), "r"(32 * g.Wx) : "memory");
+        if (group_sync) asm volatile("bar.sync %0, %1;" ::"r"(1 + wy), "r"(32 * g.Wx) : "memory");
         else if (p2p) {
             __syncwarp();
             __threadfence_block();
@@ -468,20 +472,12 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     };
 
     for (;;) {
-        int ctask;
-        if constexpr (CS > 1) {
-            if (crank == 0 && threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
-            cg::this_cluster().sync();
-            ctask = *cg::this_cluster().map_shared_rank(&s_task, 0);
-            cg::this_cluster().sync();
-        } else {
-            if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
-            __syncthreads();
-            ctask = s_task;
-            if ((threadIdx.x & 31) == 0) s_done[threadIdx.x >> 5] = -1;
-            __syncthreads();
-        }
-        if (ctask >= g.ntasks_c) {
+        if (threadIdx.x == 0) s_task = atomicAdd(P.ticket, 1);
+        __syncthreads();
+        const int ctask = s_task;
+        if ((threadIdx.x & 31) == 0) s_done[threadIdx.x >> 5] = -1;
+        __syncthreads();
+        if (ctask >= g.ntasks) {
 #ifdef PDG_LAT_TIMING
             if (blockIdx.x < 6 && lane == 0 && (warp == 0 || warp == nwarps - 1))
                 printf("lat-timing ACT=%d cta %d warp %d: begin-wait %lld load %lld traces %lld mma1 %lld scan %lld mma2 %lld store %lld sync %lld\n",
@@ -491,18 +487,17 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         }
         // ticket order (pipe group, velocity, gx): every velocity's pipeline advances together, and
         // the tasks a task waits on (gx - 1: ticket - 1; previous pipe group: ticket - nvel ngx)
-        // come earlier.  A cluster task covers CS consecutive pipe groups (one per CTA).
-        // Chain segments (nseg > 1, CS = 1) are claimed in DESCENDING order: segment s waits for
+        // come earlier.
+        // Chain segments (nseg > 1) are claimed in DESCENDING order: segment s waits for
         // segment s + 1 to have read its halo rows before overwriting them, so every wait still
         // targets an earlier ticket.
         const int per_gy = g.nvel * g.ngx;
-        const int per_seg = g.ntasks_c / g.nseg;
+        const int per_seg = g.ntasks / g.nseg;
         const int seg = g.nseg - 1 - ctask / per_seg;
         const int cts = ctask - (g.nseg - 1 - seg) * per_seg;
-        const int gyc = cts / per_gy, rem = cts - gyc * per_gy;
+        const int gy = cts / per_gy, rem = cts - gy * per_gy;
         const int vi = rem / g.ngx, gx = rem - vi * g.ngx;
-        const int gy = gyc * CS + crank;
-        const int task = seg * per_seg + (gy * g.nvel + vi) * g.ngx + gx;  // CTA-level task: progress and traces
+        const int task = seg * per_seg + (gy * g.nvel + vi) * g.ngx + gx;  // progress and traces
         // chain rows: stored [rs, r1), swept from r0 (the halo [r0, rs) starts from a zero trace)
         const int rs = seg * g.seglen;
         const int r0 = max(0, rs - g.halo);
@@ -539,23 +534,16 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
         const int64_t cstep = (int64_t)V.sign[CA] * g.stride[CA] * N;                        // one chain cell
         const int64_t cbase = (V.sign[CA] > 0) ? 0 : (g.L[CA] - 1) * g.stride[CA];          // chain cell 0
 
-        // chain in-traces of every sweep (the ghost f^b is constant in time: same for both)
-        double sc[NPASS][MF];
-        {
-            double s0c[MF];
+        // chain in-trace (the ghost f^b at the inflow face, a zero trace at a segment's halo start)
+        double sc[MF];
 #pragma unroll
-            for (int j = 0; j < MF; ++j) s0c[j] = 0.0;
-            if (valid && r0 == 0) ghost_face<D, N, ACT, CA>(P, V, ucell, s0c);
-#pragma unroll
-            for (int ps = 0; ps < NPASS; ++ps)
-#pragma unroll
-                for (int j = 0; j < MF; ++j) sc[ps][j] = s0c[j];
-        }
+        for (int j = 0; j < MF; ++j) sc[j] = 0.0;
+        if (valid && r0 == 0) ghost_face<D, N, ACT, CA>(P, V, ucell, sc);
 
         double *wbuf = sfo + (size_t)warp * RING * NB * 32;
         // y traces of the previous CTA for row rr, if already published (speculative: the
         // producer normally runs ahead, so the global hand-over leaves the critical path)
-        const bool ycons = PIPE && g.ypf && wy == 0 && gy > 0 && (CS == 1 || crank == 0);
+        const bool ycons = PIPE && wy == 0 && gy > 0;
         bool ypf = false;  // this lane's y traces for the current row sit in spy
         // issue the copies of row rr into buffer rr & 1 (one commit group per row)
         auto prefetch = [&](int rr) {
@@ -567,6 +555,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     int64_t off = 0;
 #pragma unroll
                     for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
+                    PDG_CHECK_IDX(ubr + off, P.f_elems, "lattice row load f");
                     cp_async8(dst + ro(q, lane), P.f + ubr + off);
                 }
                 if constexpr (XA) {  // the row's x inflow ghost (first x warp of the first x group)
@@ -583,24 +572,19 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 // have arrived: the tags tell at the use (normally they have: the producer runs ahead)
                 ypf = false;
                 if (YLL && ycons && rr < nrow) {
+                    const uint64_t *ysrc = yll + ylslot(task - per_gy, rr);
+                    double *yd = spy + ((size_t)qx * 32 + lane) * 2 * MF;
 #pragma unroll
-                    for (int ps = 0; ps < NPASS; ++ps) {
-                        const uint64_t *ysrc = yll + ylslot(task - per_gy, rr, ps);
-                        double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * 2 * MF;
-#pragma unroll
-                        for (int h = 0; h < 2 * MF; h += 2)
-                            cp_async16_cg(yd + h, reinterpret_cast<const double *>(ysrc + h));
-                    }
+                    for (int h = 0; h < 2 * MF; h += 2) cp_async16_cg(yd + h, reinterpret_cast<const double *>(ysrc + h));
                     ypf = true;
                 } else if (!YLL && ycons && rr < nrow && ld_acquire(P.progress + (int64_t)(task - per_gy) * 8 + qx) >= rr + 1) {
                     // plain traces: copied only once published (the producer normally runs ahead)
+                    const int64_t yo = ((((int64_t)(task - per_gy) * g.rcap + rr) * g.Wx + qx) * 32 + lane) * MFP;
+                    PDG_CHECK_IDX(yo + MFP - 1, P.ybuf_elems, "lattice y trace (plain)");
+                    const double *ysrc = P.ybuf + yo;
+                    double *yd = spy + ((size_t)qx * 32 + lane) * MFP;
 #pragma unroll
-                    for (int ps = 0; ps < NPASS; ++ps) {
-                        const double *ysrc = P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + rr) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
-                        double *yd = spy + (((size_t)ps * g.Wx + qx) * 32 + lane) * MFP;
-#pragma unroll
-                        for (int h = 0; h < MFP; h += 2) cp_async16_cg(yd + h, ysrc + h);
-                    }
+                    for (int h = 0; h < MFP; h += 2) cp_async16_cg(yd + h, ysrc + h);
                     ypf = true;
                 }
             }
@@ -630,38 +614,32 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                 PDG_TMARK(1);
                 // f_old of the unit stays in shared memory (per-lane column: conflict-free)
                 const double *src = wbuf + (r % RING) * NB * 32;
-                double fprev[NB];  // input of the second sweep (output of the first)
                 double fn[NB];
-#pragma unroll
-                for (int ps = 0; ps < NPASS; ++ps) {
-                    // f_old of this sweep: the row buffer (first) or the first sweep's result
-                    auto fold = [&](int c) -> double { return (ps == 0) ? src[ro(c, lane)] : fprev[c]; };
+                auto fold = [&](int c) -> double { return src[ro(c, lane)]; };
+                {
                     // pipe (y) in-trace
                     double sy[PIPE ? MF : 1];
                     if constexpr (PIPE) {
                         if (wy > 0) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) sy[j] = YS(ps, (t - 1) & 1, warp - g.Wx, lane)[j];
-                        } else if (CS > 1 && crank > 0) {
-                            // the previous CTA of the cluster: its last pipe warp, through DSMEM
-                            const double *rsy = cg::this_cluster().map_shared_rank(
-                                YS(ps, (t - 1) & 1, (g.Wy - 1) * g.Wx + qx, lane), crank - 1);
-#pragma unroll
-                            for (int j = 0; j < MF; ++j) sy[j] = rsy[j];
+                            for (int j = 0; j < MF; ++j) sy[j] = YS((t - 1) & 1, warp - g.Wx, lane)[j];
                         } else if (gy > 0) {
                             if constexpr (YLL) {
-                                uint64_t *ysl = yll + ylslot(task - per_gy, r, ps);
-                                const uint64_t *w = reinterpret_cast<const uint64_t *>(spy) + (((size_t)ps * g.Wx + qx) * 32 + lane) * 2 * MF;
+                                uint64_t *ysl = yll + ylslot(task - per_gy, r);
+                                const uint64_t *w = reinterpret_cast<const uint64_t *>(spy) + ((size_t)qx * 32 + lane) * 2 * MF;
                                 if (ypf && ll_decode<MF>(w, sy, (uint32_t)r + 1u))
                                     ll_clear<MF>(ysl);  // empty the slot for the next launch
                                 else
                                     ll_take<MF>(ysl, sy, (uint32_t)r + 1u);
                             } else if (ypf) {
 #pragma unroll
-                                for (int j = 0; j < MF; ++j) sy[j] = spy[(((size_t)ps * g.Wx + qx) * 32 + lane) * MFP + j];
+                                for (int j = 0; j < MF; ++j) sy[j] = spy[((size_t)qx * 32 + lane) * MFP + j];
                             } else {
-                                if (ps == 0) wait_progress(P.progress + (int64_t)(task - per_gy) * 8 + qx, r + 1);
-                                const double *ysrc = P.ybuf + (((((int64_t)(task - per_gy) * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                                PDG_CHECK_IDX((int64_t)(task - per_gy) * 8 + qx, (int64_t)g.ntasks * 8, "lattice progress");
+                                wait_progress(P.progress + (int64_t)(task - per_gy) * 8 + qx, r + 1);
+                                const int64_t yo = ((((int64_t)(task - per_gy) * g.rcap + r) * g.Wx + qx) * 32 + lane) * MFP;
+                                PDG_CHECK_IDX(yo + MFP - 1, P.ybuf_elems, "lattice y trace (plain)");
+                                const double *ysrc = P.ybuf + yo;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) sy[j] = __ldcg(ysrc + j);
                             }
@@ -670,7 +648,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                             for (int j = 0; j < MF; ++j) sy[j] = 0.0;
                             if (valid) ghost_face<D, N, ACT, 1>(P, V, ucell, sy);
                         }
-                        if (PFA > 0 && ps == NPASS - 1) prefetch(r + 1);  // overlaps the rest of the row
+                        if (PFA > 0) prefetch(r + 1);  // overlaps the rest of the row
                     }
                     // x in-trace of the warp (lane 0's cell): previous x warp, previous x CTA or the ghost
                     double s0[XA ? MF : 1];
@@ -679,12 +657,11 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     if constexpr (XA) {
                         if (qx > 0) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) s0[j] = xs[ps][(t - 1) % XR][warp - 1][j];
+                            for (int j = 0; j < MF; ++j) s0[j] = xs[(t - 1) % XR][warp - 1][j];
                         } else if (gx > 0) {
                             // only lane 0 enters the x in-trace into the scan
                             if (lane == 0)
-                                ll_take<MF>(xll + ((((int64_t)(task - 1) * g.rcap + r) * NPASS + ps) * g.Wy + wy) * 2 * MF, s0,
-                                            (uint32_t)r + 1u);
+                                ll_take<MF>(xll + xlslot(task - 1, r), s0, (uint32_t)r + 1u);
                         } else if (lane == 0 && valid) {
 #pragma unroll
                             for (int j = 0; j < MF; ++j) s0[j] = 2.0 * gxs[wy][r % RING][j];
@@ -721,10 +698,9 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         // the warp's x out-trace (lane 31's inclusive value) for the next x warp / CTA
                         if (lane == 31) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) xs[ps][t % XR][warp][j] = a[j];
+                            for (int j = 0; j < MF; ++j) xs[t % XR][warp][j] = a[j];
                             if (qx == g.Wx - 1 && gx < g.ngx - 1)
-                                ll_put<MF>(xll + ((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wy + wy) * 2 * MF, a,
-                                           (uint32_t)r + 1u);
+                                ll_put<MF>(xll + xlslot(task, r), a, (uint32_t)r + 1u);
                         }
                     };
                     PDG_TMARK(2);
@@ -741,7 +717,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         for (int q = 0; q < NB; ++q) {
                             double v = 2.0 * fsrc[ro(q, lane)];
                             if ((q / ipow(N, TC)) % N == 0)  // chain in-face node
-                                v = fma(g.kw[TC], sc[ps][(q % ipow(N, TC)) + (q / ipow(N, TC + 1)) * ipow(N, TC)], v);
+                                v = fma(g.kw[TC], sc[(q % ipow(N, TC)) + (q / ipow(N, TC + 1)) * ipow(N, TC)], v);
                             if constexpr (PIPE) {
                                 if ((q / ipow(N, TY)) % N == 0)  // pipe in-face node
                                     v = fma(g.kw[TY], sy[(q % ipow(N, TY)) + (q / ipow(N, TY + 1)) * ipow(N, TY)], v);
@@ -822,7 +798,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         auto rhs = [&](int c) -> double {
                             double v = 2.0 * fold(c);
                             if ((c / ipow(N, TC)) % N == 0)  // chain in-face node
-                                v = fma(g.kw[TC], sc[ps][(c % ipow(N, TC)) + (c / ipow(N, TC + 1)) * ipow(N, TC)], v);
+                                v = fma(g.kw[TC], sc[(c % ipow(N, TC)) + (c / ipow(N, TC + 1)) * ipow(N, TC)], v);
                             if constexpr (PIPE) {
                                 if ((c / ipow(N, TY)) % N == 0)  // pipe in-face node
                                     v = fma(g.kw[TY], sy[(c % ipow(N, TY)) + (c / ipow(N, TY + 1)) * ipow(N, TY)], v);
@@ -859,7 +835,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
 #pragma unroll
                     for (int j = 0; j < MF; ++j) {
                         const int q = (j % ipow(N, TC)) + (j / ipow(N, TC)) * ipow(N, TC + 1) + (N - 1) * ipow(N, TC);
-                        sc[ps][j] = fold(q) + fn[q];
+                        sc[j] = fold(q) + fn[q];
                     }
                     if constexpr (PIPE) {
                         double ty[MF];
@@ -870,28 +846,30 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         }
                         if (warp < nys) {
 #pragma unroll
-                            for (int j = 0; j < MF; ++j) YS(ps, t & 1, warp, lane)[j] = ty[j];
+                            for (int j = 0; j < MF; ++j) YS(t & 1, warp, lane)[j] = ty[j];
                         }
-                        if (wy == g.Wy - 1 && crank == CS - 1 && gy < g.ngy - 1) {
+                        if (wy == g.Wy - 1 && gy < g.ngy - 1) {
                             if constexpr (YLL) {
-                                ll_put<MF>(yll + ylslot(task, r, ps), ty, (uint32_t)r + 1u);
+                                ll_put<MF>(yll + ylslot(task, r), ty, (uint32_t)r + 1u);
                             } else {
-                                double *dst = P.ybuf + (((((int64_t)task * g.rcap + r) * NPASS + ps) * g.Wx + qx) * 32 + lane) * MFP;
+                                const int64_t yo = ((((int64_t)task * g.rcap + r) * g.Wx + qx) * 32 + lane) * MFP;
+                                PDG_CHECK_IDX(yo + MFP - 1, P.ybuf_elems, "lattice y trace (plain)");
+                                double *dst = P.ybuf + yo;
 #pragma unroll
                                 for (int j = 0; j < MF; ++j) __stcg(dst + j, ty[j]);
                                 // the producing warp publishes its own row progress: __syncwarp orders
                                 // the lanes' stores before lane 0's release (cumulative at gpu scope)
                                 __syncwarp();
+                                PDG_CHECK_IDX((int64_t)task * 8 + qx, (int64_t)g.ntasks * 8, "lattice progress");
                                 if (lane == 0) st_release(P.progress + (int64_t)task * 8 + qx, r + 1);
                             }
                         }
                     }
-#pragma unroll
-                    for (int q = 0; q < NB; ++q) fprev[q] = fn[q];
                 }
                 PDG_TMARK(5);
                 // the last halo rows of the next segment: wait until it has read their old values
                 if (!hclear && r0 + r >= r1 - g.halo) {
+                    PDG_CHECK_IDX(task + per_seg, g.ntasks, "lattice halo flag");
                     if (lane == 0) wait_progress(P.hdone + task + per_seg, 1);
                     __syncwarp();
                     hclear = true;
@@ -902,7 +880,8 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                         int64_t off = 0;
 #pragma unroll
                         for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
-                        __stcs(P.f + ub + off, fprev[q]);
+                        PDG_CHECK_IDX(ub + off, P.f_elems, "lattice row store f");
+                        __stcs(P.f + ub + off, fn[q]);
                     }
                 }
             }
@@ -911,6 +890,7 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             // every warp has read the halo rows (cp.async waited): release them to the previous segment
             if (rs > r0 && t == rs - r0 - 1 + maxskew) {
                 __syncthreads();
+                PDG_CHECK_IDX(task, g.ntasks, "lattice halo flag");
                 if (threadIdx.x == 0) st_release(P.hdone + task, 1);
             }
         }
@@ -1022,44 +1002,6 @@ __device__ __forceinline__ void lbm_local_ops(double (&fv)[NV], double (&w)[D + 
     }
 }
 
-// Memory-level parallelism: the kernel needs ~100 KB of loads in flight per SM to saturate HBM; with
-// one node per thread that is NV x 8 B x resident threads, so D3Q15 runs 3 CTAs per SM (80
-// registers: 2.37 -> 2.09 ms per pass on 128^3, 0.87 -> 0.99 of HBM); D3Q19 spilled at 3 (slower)
-template <int D, int NV>
-__global__ void __launch_bounds__(256, (D == 3 && NV <= 15) ? 3 : 2) relax_lbm_kernel(double *__restrict__ f, int64_t nnodes,
-                                                        const __grid_constant__ LbmParams L, const LocalOps op)
-{
-    // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
-    // instead of being hoisted into registers)
-    {
-        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (x >= nnodes) return;
-        double fv[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) fv[i] = __ldcs(f + (int64_t)i * nnodes + x);
-        double w[D + 1];
-        lbm_moments<D, NV>(fv, L, w);
-        // lbm_local_ops, with every velocity stored as soon as it is updated (fewer live registers)
-        double gs[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            gs[d] = w[0] * L.G[d] * L.inv_c2;
-            w[1 + d] = fma(op.hs1 * w[0], L.G[d], w[1 + d]);
-        }
-        const double hg = fma(op.ca, op.hs1, op.hs2);
-        const LbmNode<D> nd(w, L);
-        const double cb = op.cb;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            double vg = 0.0;
-#pragma unroll
-            for (int d = 0; d < D; ++d) vg = fma(L.v[i][d], gs[d], vg);
-            const double fs = fma(hg * L.wgt[i], vg, op.ca * fv[i]);
-            __stcs(f + (int64_t)i * nnodes + x, (cb != 0.0) ? fma(cb, nd.feq(i, L), fs) : fs);
-        }
-    }
-}
-
 __device__ __forceinline__ double ld_l1(const double *p)
 {
     double v;
@@ -1067,10 +1009,12 @@ __device__ __forceinline__ double ld_l1(const double *p)
     return v;
 }
 
-// Two-phase variant for the 3-D sets: the moments from a first read of the node's NV values
-// (short live ranges), then each value read again -- an L1 hit: the CTA's values were just loaded
-// -- for its update.  ~60 registers instead of 92-128, so more threads per SM keep loads in flight
-// without the spills of a register cap.  Same arithmetic, same results as relax_lbm_kernel.
+// Two phases: the moments from a first read of the node's NV values (short live ranges), then each
+// value read again -- an L1 hit: the CTA's values were just loaded -- for its update.  ~60 registers
+// instead of the 92-128 of a one-read kernel, so more threads per SM keep loads in flight without
+// the spills of a register cap (one node per thread: no grid-stride loop, so the velocity constants
+// stay constant-bank operands; the one-read kernel measured 0.90-0.99 of HBM against 1.01-1.03,
+// DESIGN.md §12).
 template <int D, int NV>
 __global__ void __launch_bounds__(256, 4) relax_lbm2_kernel(double *__restrict__ f, int64_t nnodes,
                                                            const __grid_constant__ LbmParams L, const LocalOps op)

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdg.so")
+# PDG_CHECKED=1 selects the bounds-checked build of the same library (build.py --checked)
+LIB_PATH = os.path.join(_HERE, "libpdg_checked.so" if os.environ.get("PDG_CHECKED") == "1" else "libpdg.so")
 
 # status codes (include/pdg.h)
 PDG_OK = 0
@@ -67,6 +68,7 @@ class pdg_problem(ctypes.Structure):
         ("decomposition", ctypes.c_int32), ("slabs_per_rank", ctypes.c_int32),
         ("source", ctypes.c_int32), ("source_params", ctypes.POINTER(ctypes.c_double)),
         ("n_source_params", ctypes.c_int32),
+        ("lattice_cta", ctypes.c_int32 * 2), ("lattice_segment", ctypes.c_int32),
     ]
 
 
@@ -148,7 +150,8 @@ def version() -> str:
 
 def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, tau=0.0, scheme=PDG_SCHEME_M2,
                  rank=0, nranks=1, nccl_id=None, stream=None, flags=0, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
-                 decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1, gravity=None):
+                 decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1, gravity=None, lattice_cta=(0, 0),
+                 lattice_segment=0):
     """Build a pdg_problem; the returned object keeps its host arrays alive."""
     pb = pdg_problem()
     pb.dim = dim
@@ -177,6 +180,8 @@ def make_problem(dim, ncell, degree, m, vel, comp, lam, flux, flux_params, dt, t
     pb.flags = flags
     pb.decomposition = decomposition
     pb.slabs_per_rank = slabs_per_rank
+    pb.lattice_cta[0], pb.lattice_cta[1] = int(lattice_cta[0]), int(lattice_cta[1])
+    pb.lattice_segment = int(lattice_segment)
     if gravity:
         pb._src = (ctypes.c_double * len(gravity))(*gravity)
         pb.source = PDG_SOURCE_GRAVITY
@@ -336,10 +341,11 @@ class Solver:
 
 
 def problem_from_config(cfg, tau=0.0, scheme=PDG_SCHEME_M2, rank=0, nranks=1, nccl_id=None, flags=0, stream=None,
-                        decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1):
+                        decomposition=PDG_DECOMP_VELOCITY, slabs_per_rank=1, lattice_cta=(0, 0), lattice_segment=0):
     """pdg_problem for a pdg_inputs.Config (the seeded workload descriptions)."""
     vel, comp = cfg.velocities()
     return make_problem(cfg.dim, cfg.N, cfg.p, cfg.m, vel, comp, cfg.lam, cfg.flux, list(cfg.flux_params()), cfg.dt,
                         tau=tau, scheme=scheme, rank=rank, nranks=nranks, nccl_id=nccl_id, flags=flags,
                         stream=stream, lo=cfg.lo, hi=cfg.hi, decomposition=decomposition,
-                        slabs_per_rank=slabs_per_rank, gravity=getattr(cfg, "gravity", None) or None)
+                        slabs_per_rank=slabs_per_rank, gravity=getattr(cfg, "gravity", None) or None,
+                        lattice_cta=lattice_cta, lattice_segment=lattice_segment)

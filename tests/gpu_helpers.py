@@ -59,9 +59,14 @@ def full_grid_to_planes(cfg, full: np.ndarray, plane_stride: int, v_begin: int =
     return out
 
 
+# Launch plan of the lattice sweeps forced by a test (pdg_problem.lattice_cta / lattice_segment;
+# zeros: the library's default plan).  Set through the `warps` / `seglen` fixtures.
+LATTICE_PLAN = {"lattice_cta": (0, 0), "lattice_segment": 0}
+
+
 def make_solver(cfg, **kw):
     from paper_1702_00169_b200 import pdg
-    pb = pdg.problem_from_config(cfg, **kw)
+    pb = pdg.problem_from_config(cfg, **{**LATTICE_PLAN, **kw})
     return pdg.Solver(pb)
 
 

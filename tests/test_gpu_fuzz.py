@@ -108,16 +108,15 @@ def test_fuzz_backward_steps(seed):
 
 
 # --------------------------------------------------------------------------
-# Protocol fuzz: lattice sets with the cross-CTA hand-overs, chain segments and the fused
-# two-sweep variant forced on through the plan knobs, on boxes large enough for
-# several CTAs and segments.  PDG_FUZZ_SEEDS widens the sweep (default 24 seeds).
+# Protocol fuzz: lattice sets with the cross-CTA hand-overs and chain segments, with random
+# CTA shapes forced through the launch plan (pdg_problem.lattice_cta / lattice_segment, DESIGN.md
+# §12), on boxes large enough for several CTAs and segments.  PDG_FUZZ_SEEDS widens the sweep (default 24 seeds).
 # --------------------------------------------------------------------------
 N_PROTO = int(__import__("os").environ.get("PDG_FUZZ_SEEDS", "24"))
 
 
 @pytest.mark.parametrize("seed", range(N_PROTO))
 def test_fuzz_lattice_protocols(seed):
-    import os
     from paper_1702_00169_b200 import pdg
     from pdg_inputs import lattice
     rng = np.random.default_rng(5000 + seed)
@@ -130,16 +129,14 @@ def test_fuzz_lattice_protocols(seed):
     h = 1.0 / ncell[0]
     hi = [ncell[d] * h for d in range(dim)] + [1.0] * (3 - dim)  # square cells: equal kappas
     dt = 2.0 * kappa * h
-    env = {"PDG_LATTICE_WARPS": str(rng.choice(["1,1", "2,2", "1,2", "2,1", "4,2"])),
-           "PDG_LATTICE_SEG": str(int(rng.choice([0, 12, 16, 20, 30]))),
-           "PDG_LATTICE_FUSE": str(int(rng.choice([0, 104])))}
+    cta = [(1, 1), (2, 2), (1, 2), (2, 1), (4, 2)][int(rng.integers(0, 5))]
+    seg = int(rng.choice([-1, 12, 16, 20, 30]))
+    plan = {"lattice_cta": cta, "lattice_segment": seg}
     vel, wts = lattice(name, 1.0)
     fparams = [1.0 / math.sqrt(3.0)] + list(wts)
-    old = {k: os.environ.get(k) for k in env}
-    try:
-        os.environ.update(env)
+    if True:  # (indentation kept from the env-knob version)
         pb = pdg.make_problem(dim, ncell, p, dim + 1, vel, [0] * len(vel), 1.0, pdg.PDG_FLUX_LBM, fparams, dt,
-                              hi=tuple(hi))
+                              hi=tuple(hi), **plan)
         S = pdg.Solver(pb)
         ob = O.Problem(dim, ncell, p, vel, [0] * len(vel), dim + 1, 1.0, 3, fparams, dt, hi=hi)
         shape = ob.grid_shape()
@@ -156,12 +153,6 @@ def test_fuzz_lattice_protocols(seed):
         S.step(2)
         got = to_np(S.get_state(), f.shape)
         S.destroy()
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
     ref = O.scheme_run(ob, f, fb, 2, "m2")
     err = rel_maxnorm(got, ref)
-    assert err <= 1e-12, (seed, name, dim, ncell, p, kappa, env, err)
+    assert err <= 1e-12, (seed, name, dim, ncell, p, kappa, plan, err)

@@ -5,17 +5,16 @@ The oracle assembles the full eq DG_reduit blocks of each velocity, orders cells
 Kahn's algorithm on the dependency graph and solves every cell with a
 dense LU; the CUDA path applies the pre-inverted dense (p+1)^d block along diagonal
 wavefronts (pdg_lattice.cuh).  Bar: <= 1e-13 for one operator, <= 1e-12 for M2 steps
-(relative max-norm, reading C17).  PDG_LATTICE_WARPS forces one warp per CTA so that
-the cross-CTA hand-over (global traces + progress flags) runs on small grids.
+(relative max-norm, reading C17).  pdg_problem.lattice_cta forces small CTAs (one warp per
+CTA) so that the cross-CTA hand-over (global traces + progress flags) runs on small grids.
 """
-import os
-
 import numpy as np
 import pytest
 import torch
 
 from oracle import oracle as O
 from pdg_inputs import lbm_config, random_state, w0_grid, wb_grid
+import gpu_helpers
 from gpu_helpers import lattice_planes, make_solver, oracle_problem, rel_maxnorm, to_dev, to_np
 
 pytestmark = pytest.mark.gpu
@@ -24,18 +23,16 @@ TOL_OP = 1e-13
 TOL_STEP = 1e-12
 
 
+def _cta(warps):
+    return tuple(int(x) for x in warps.split(",")) if warps else (0, 0)
+
+
 @pytest.fixture
 def warps(request):
-    old = os.environ.get("PDG_LATTICE_WARPS")
-    if request.param:
-        os.environ["PDG_LATTICE_WARPS"] = request.param
-    else:
-        os.environ.pop("PDG_LATTICE_WARPS", None)
+    """Forced CTA shape "wx,wy" (pdg_problem.lattice_cta) for the solvers the test creates."""
+    gpu_helpers.LATTICE_PLAN["lattice_cta"] = _cta(request.param)
     yield request.param
-    if old is None:
-        os.environ.pop("PDG_LATTICE_WARPS", None)
-    else:
-        os.environ["PDG_LATTICE_WARPS"] = old
+    gpu_helpers.LATTICE_PLAN["lattice_cta"] = (0, 0)
 
 
 def cases():
@@ -115,7 +112,8 @@ def test_lbm_scheme_parity(lat, N, p, scheme):
     w0 = w0_grid(cfg)
     wb = wb_grid(cfg, w0)
     sch = {"m2": pdg.PDG_SCHEME_M2, "m2kin": pdg.PDG_SCHEME_M2KIN, "m4": pdg.PDG_SCHEME_M4}[scheme]
-    tau = 0.0 if scheme == "m2" else 0.3 * cfg.dt
+    # M4's middle substep is negative (g2 = 1 - 2 g1 < 0): tau > 0 needs 2 tau + g2 dt/2 > 0
+    tau = {"m2": 0.0, "m2kin": 0.3 * cfg.dt, "m4": 0.6 * cfg.dt}[scheme]
     S = make_solver(cfg, scheme=sch, tau=tau)
     S.set_equilibrium(w0.reshape(-1).cuda(), wb.reshape(-1).cuda())
     S.step(cfg.steps)
@@ -318,7 +316,7 @@ def _aniso(lat, ncell, p, lam=1.0, hi=(1.0, 1.0, 1.0)):
     h = min(hi[d] / ncell[d] for d in range(dim))
     dt = 0.7 * h / lam
     pb = pdg.make_problem(dim, list(ncell), p, dim + 1, vel, [0] * len(vel), lam, pdg.PDG_FLUX_LBM, fparams, dt,
-                          hi=tuple(hi))
+                          hi=tuple(hi), **gpu_helpers.LATTICE_PLAN)
     ob = O.Problem(dim, list(ncell), p, vel, [0] * len(vel), dim + 1, lam, 3, fparams, dt, hi=list(hi))
     return pb, ob, dt
 
@@ -407,17 +405,13 @@ def test_lattice_host_pointer_paths():
 # Chain segments: a class without a pipe axis is cut along its chain into
 # segments swept concurrently, each starting `halo` rows early from a zero chain trace, the
 # halo taken from the norm bound of the chain operator (pdg_tables.hpp lattice_chain_halo).
-# PDG_LATTICE_SEG forces the segment length so that small grids run several segments.
+# pdg_problem.lattice_segment forces the segment length so that small grids run several segments.
 # --------------------------------------------------------------------------
 @pytest.fixture
 def seglen(request):
-    old = os.environ.get("PDG_LATTICE_SEG")
-    os.environ["PDG_LATTICE_SEG"] = str(request.param)
+    gpu_helpers.LATTICE_PLAN["lattice_segment"] = int(request.param)
     yield request.param
-    if old is None:
-        os.environ.pop("PDG_LATTICE_SEG", None)
-    else:
-        os.environ["PDG_LATTICE_SEG"] = old
+    gpu_helpers.LATTICE_PLAN["lattice_segment"] = 0
 
 
 def _d2q9_box(ncell, p, dt, lam=1.0, hi=(1.0, 1.0, 1.0)):
@@ -426,7 +420,8 @@ def _d2q9_box(ncell, p, dt, lam=1.0, hi=(1.0, 1.0, 1.0)):
     import math
     vel, wts = lattice("D2Q9", lam)
     fparams = [lam / math.sqrt(3.0)] + list(wts)
-    pb = pdg.make_problem(2, list(ncell), p, 3, vel, [0] * len(vel), lam, pdg.PDG_FLUX_LBM, fparams, dt, hi=tuple(hi))
+    pb = pdg.make_problem(2, list(ncell), p, 3, vel, [0] * len(vel), lam, pdg.PDG_FLUX_LBM, fparams, dt, hi=tuple(hi),
+                          **gpu_helpers.LATTICE_PLAN)
     ob = O.Problem(2, list(ncell), p, vel, [0] * len(vel), 3, lam, 3, fparams, dt, hi=list(hi))
     return pb, ob
 
@@ -488,52 +483,14 @@ def test_lattice_chain_segments_match_unsegmented(N):
     agree to the last bits: the truncated trace differs by <= 2^-64 of the true one."""
     cfg = lbm_config("D2Q9", N, nu=2.0)
     outs = []
-    for seg in ("0", None):
-        old = os.environ.get("PDG_LATTICE_SEG")
-        if seg is None:
-            os.environ.pop("PDG_LATTICE_SEG", None)
-        else:
-            os.environ["PDG_LATTICE_SEG"] = seg
-        try:
-            S = make_solver(cfg)
-        finally:
-            if old is None:
-                os.environ.pop("PDG_LATTICE_SEG", None)
-            else:
-                os.environ["PDG_LATTICE_SEG"] = old
+    for seg in (-1, 0):  # never segmented, the default plan
+        S = make_solver(cfg, lattice_segment=seg)
         S.set_equilibrium(w0_grid(cfg, device="cuda").reshape(-1))
         S.step(2)
         outs.append(S.get_state().clone())
         S.destroy()
     err = float((outs[0] - outs[1]).abs().max() / outs[0].abs().max())
     assert err <= 1e-15, err
-
-
-@pytest.mark.parametrize("lat,N,p", [("D3Q19", 6, 2), ("D3Q27", 5, 1), ("D3Q19", 4, 3), ("D3Q27", 33, 2)])
-def test_lattice_fused_two_sweeps_parity(lat, N, p):
-    """PDG_LATTICE_FUSE=104 (axis masks 3, 5, 6): the 3-D two-axis classes apply the trailing and the
-    leading T2(dt/2) of consecutive steps in one launch (NPASS = 2, off by default) == the oracle."""
-    old = os.environ.get("PDG_LATTICE_FUSE")
-    os.environ["PDG_LATTICE_FUSE"] = "104"
-    try:
-        from paper_1702_00169_b200 import pdg
-        cfg = lbm_config(lat, N, p=p, steps=3)
-        w0 = w0_grid(cfg)
-        wb = wb_grid(cfg, w0)
-        S = make_solver(cfg)
-        S.set_equilibrium(w0.reshape(-1).cuda(), wb.reshape(-1).cuda())
-        S.step(cfg.steps)
-        got = to_np(S.get_state(), (cfg.nv,) + cfg.grid_shape)
-        S.destroy()
-    finally:
-        if old is None:
-            os.environ.pop("PDG_LATTICE_FUSE", None)
-        else:
-            os.environ["PDG_LATTICE_FUSE"] = old
-    pb = oracle_problem(cfg)
-    f0, fb = O.initial_data(pb, w0.numpy(), wb.numpy())
-    ref = O.scheme_run(pb, f0, fb, cfg.steps, "m2")
-    assert rel_maxnorm(got, ref) <= TOL_STEP
 
 
 @pytest.mark.parametrize("lat,N,warps", [("D2Q9", 1024, None), ("D2Q9", 300, "1,1"), ("D3Q27", 48, None),
@@ -571,11 +528,11 @@ def test_lattice_sweeps_bitwise_deterministic(lat, N, warps):
         assert torch.equal(o, outs[0])
 
 
-@pytest.mark.parametrize("seglen,fuse", [(16, None), (40, "104")])
-def test_lattice_chain_segments_3d_two_axis_classes(seglen, fuse):
+@pytest.mark.parametrize("seglen", [16, 40])
+def test_lattice_chain_segments_3d_two_axis_classes(seglen):
     """Chain segments on the 3-D classes without a pipe axis (x,y and x,z active: D3Q19's face
-    diagonals), one sweep per launch (halo H) and two sweeps per launch (PDG_LATTICE_FUSE, halo 2H),
-    against the oracle: one T2 and two M2 steps on a box whose chains span several segments."""
+    diagonals) against the oracle: one T2 and two M2 steps on a box whose chains span several
+    segments."""
     from paper_1702_00169_b200 import pdg
     from pdg_inputs import lattice
     import math
@@ -586,15 +543,9 @@ def test_lattice_chain_segments_3d_two_axis_classes(seglen, fuse):
     dtp = kappa * h
     vel, wts = lattice("D3Q19", 1.0)
     fparams = [1.0 / math.sqrt(3.0)] + list(wts)
-    env = {"PDG_LATTICE_SEG": str(seglen), "PDG_LATTICE_FUSE": fuse}
-    old = {k: os.environ.get(k) for k in env}
-    try:
-        for k, v in env.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
-        pb = pdg.make_problem(3, list(ncell), 2, 4, vel, [0] * len(vel), 1.0, pdg.PDG_FLUX_LBM, fparams, 2.0 * dtp, hi=hi)
+    if True:  # (indentation kept from the env-knob version)
+        pb = pdg.make_problem(3, list(ncell), 2, 4, vel, [0] * len(vel), 1.0, pdg.PDG_FLUX_LBM, fparams, 2.0 * dtp, hi=hi,
+                              lattice_segment=seglen)
         S = pdg.Solver(pb)
         ob = O.Problem(3, list(ncell), 2, vel, [0] * len(vel), 4, 1.0, 3, fparams, 2.0 * dtp, hi=list(hi))
         shape = ob.grid_shape()
@@ -611,11 +562,5 @@ def test_lattice_chain_segments_3d_two_axis_classes(seglen, fuse):
         S.step(2)
         got2 = to_np(S.get_state(), f.shape)
         S.destroy()
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
     ref2 = O.m2_run(ob, ob.cells_to_grid(fc), fb_full, 2)
     assert rel_maxnorm(got2, ref2) <= TOL_STEP
