@@ -289,6 +289,20 @@ pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad);
  * M: n*n row-major, g: n, beta = g[n-1].  Host outputs.  For inspection/pins. */
 pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, double *g, double *beta);
 
+/* Carry tables of the exact z-slab decomposition (row e; P:779-797 domain decomposition,
+ * DESIGN.md §8) along the slowest axis of problem *p, for npass consecutive T2(dtp) sweeps
+ * (npass = 1 or 2) of a slab of `len` cells.  The line recurrence is affine, so a slab swept
+ * with zero inflow needs, once its true inflow carries S1 (pass 1) and S2 (pass 2) are known:
+ *   f_l += Q_l S_last + (npass == 2 ? P_l S1 : 0),   l = 0 .. len-1 (cells in flow order,
+ *          S_last = S2 for npass 2, S1 for npass 1; nodes of cell l in flow order),
+ *   outgoing carries: c1 = A1 + B S1,  c2 = A2 + B S2 + C S1   (A = the zero-inflow carries).
+ * Outputs (host): P, Q: [len][p+1] row-major; B = beta^len; C; leff = cells after which every
+ * |P_l|, |Q_l| < 2^-64 (the correction the library applies stops there, reading C26).
+ * Host-only (no GPU); computed in long double and rounded once.
+ * Errors: those of pdg_query_sizes; PDG_E_INVALID_ARGUMENT for npass, len < 1, NULL outputs. */
+pdg_status pdg_zslab_table(const pdg_problem *p, double dtp, int npass, int64_t len, double *P, double *Q,
+                           double *B, double *C, int32_t *leff);
+
 /* Block until all work enqueued by this context has finished (including PDG_ASYNC_HOST copies);
  * reports asynchronous faults. */
 pdg_status pdg_synchronize(pdg_ctx *c);

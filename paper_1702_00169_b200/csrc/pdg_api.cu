@@ -1332,29 +1332,15 @@ void build_sweep_params(pdg_ctx *c)
 // For one sweep pass structure (T2(dtp) applied npass times): Q_l = g beta^l (response of cell l
 // to a unit inflow), P_l (pass-2 response to a unit pass-1 inflow), B_len = beta^len and C_len
 // (pass-2 outgoing carry response), computed in long double by running the recurrence on unit
-// inputs.  Truncated at leff where |P_l|, |Q_l| < 2^-64 for every later l.
-pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out)
+// inputs.  leff: every later l has |P_l|, |Q_l| < 2^-64.  P, Q: [lmax][n]; B, C: [lmax + 1].
+bool zslab_tables(int p, long double kappa, int npass, int64_t lmax, std::vector<double> &P, std::vector<double> &Q,
+                  std::vector<double> &B, std::vector<double> &C, int *leff_out)
 {
-    for (const auto &t : c->ztables_host)
-        if (t.dtp == dtp && t.npass == npass) {
-            *out = &t;
-            return PDG_OK;
-        }
-    if ((int)c->ztables_host.size() >= kMaxTables) return fail(PDG_E_UNSUPPORTED, "too many distinct z-slab steps");
-    const Geometry &g = c->g;
-    const int n = g.n;
-    int64_t lmax = 0;
-    for (int sl = 0; sl < g.nslab; ++sl) lmax = std::max(lmax, g.slab_begin[sl + 1] - g.slab_begin[sl]);
-    lmax += 1;
-    pdg::CellBlock cb;
-    const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)g.h[g.outer];
-    if (!pdg::cell_block(g.p, kappa, &cb)) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block");
-    // long-double copies of the block
+    const int n = p + 1;
     long double M[16], gv[4];
     {
-        // recompute in long double for the tables (the kernel block is its double rounding)
         long double x[4], w[4], D[16], G[16], A[16], Ai[16];
-        pdg::gl_nodes(g.p, x, w);
+        pdg::gl_nodes(p, x, w);
         pdg::lagrange_derivative(n, x, D);
         for (int i = 0; i < n; ++i)
             for (int jj = 0; jj < n; ++jj) {
@@ -1363,7 +1349,7 @@ pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out
                 G[i * n + jj] = v / w[i];
                 A[i * n + jj] = ((i == jj) ? 1.0L : 0.0L) - kappa * G[i * n + jj];
             }
-        pdg::invert(n, A, Ai);
+        if (!pdg::invert(n, A, Ai)) return false;
         for (int i = 0; i < n; ++i) {
             for (int jj = 0; jj < n; ++jj) {
                 long double acc = 0.0L;
@@ -1373,16 +1359,14 @@ pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out
             gv[i] = Ai[i * n + 0] * kappa / w[0];
         }
     }
-    std::vector<double> table((size_t)2 * lmax * n, 0.0);
-    pdg_ctx::ZTable zt;
-    zt.dtp = dtp;
-    zt.npass = npass;
-    zt.B.assign(lmax + 1, 0.0);
-    zt.C.assign(lmax + 1, 0.0);
+    P.assign((size_t)lmax * n, 0.0);
+    Q.assign((size_t)lmax * n, 0.0);
+    B.assign(lmax + 1, 0.0);
+    C.assign(lmax + 1, 0.0);
     long double c1 = 1.0L, c2 = 0.0L;  // carries of pass 1 (unit inflow) and pass 2 (zero inflow)
     int leff = 0;
-    zt.B[0] = 1.0;
-    zt.C[0] = 0.0;
+    B[0] = 1.0;
+    C[0] = 0.0;
     for (int64_t l = 0; l < lmax; ++l) {
         long double d1[4], d2[4];
         for (int a = 0; a < n; ++a) d1[a] = gv[a] * c1;  // pass-1 response (old data 0)
@@ -1395,15 +1379,39 @@ pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out
         c2 = d1[n - 1] + d2[n - 1];
         bool big = false;
         for (int a = 0; a < n; ++a) {
-            table[(size_t)l * n + a] = (double)d2[a];               // P_l
-            table[(size_t)lmax * n + l * n + a] = (double)d1[a];   // Q_l
+            P[(size_t)l * n + a] = (double)d2[a];
+            Q[(size_t)l * n + a] = (double)d1[a];
             if (fabsl(d1[a]) >= 0x1p-64L || (npass > 1 && fabsl(d2[a]) >= 0x1p-64L)) big = true;
         }
         if (big) leff = (int)l + 1;
-        zt.B[l + 1] = (double)c1;
-        zt.C[l + 1] = (double)c2;
+        B[l + 1] = (double)c1;
+        C[l + 1] = (double)c2;
     }
-    zt.leff = leff;
+    *leff_out = leff;
+    return true;
+}
+
+pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out)
+{
+    for (const auto &t : c->ztables_host)
+        if (t.dtp == dtp && t.npass == npass) {
+            *out = &t;
+            return PDG_OK;
+        }
+    if ((int)c->ztables_host.size() >= kMaxTables) return fail(PDG_E_UNSUPPORTED, "too many distinct z-slab steps");
+    const Geometry &g = c->g;
+    int64_t lmax = 0;
+    for (int sl = 0; sl < g.nslab; ++sl) lmax = std::max(lmax, g.slab_begin[sl + 1] - g.slab_begin[sl]);
+    lmax += 1;
+    const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)g.h[g.outer];
+    std::vector<double> Pt, Qt;
+    pdg_ctx::ZTable zt;
+    if (!zslab_tables(g.p, kappa, npass, lmax, Pt, Qt, zt.B, zt.C, &zt.leff))
+        return fail(PDG_E_INVALID_ARGUMENT, "singular cell block");
+    zt.dtp = dtp;
+    zt.npass = npass;
+    std::vector<double> table(Pt);  // P[lmax][n], then Q[lmax][n] (zslab_correct_kernel)
+    table.insert(table.end(), Qt.begin(), Qt.end());
     zt.slot = (int)c->ztables_host.size();
     cudaError_t e = cudaMemcpy(c->ztables + (size_t)zt.slot * g.table_doubles, table.data(),
                                sizeof(double) * table.size(), cudaMemcpyHostToDevice);
@@ -1880,6 +1888,30 @@ pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, dou
     for (int i = 0; i < cb.n * cb.n; ++i) M[i] = cb.M[i];
     for (int i = 0; i < cb.n; ++i) g[i] = cb.g[i];
     *beta = cb.beta;
+    return PDG_OK;
+}
+
+pdg_status pdg_zslab_table(const pdg_problem *p, double dtp, int npass, int64_t len, double *P, double *Q,
+                           double *B, double *C, int32_t *leff)
+{
+    Geometry g;
+    pdg_status s = validate(p, &g);
+    if (s != PDG_OK) return s;
+    if ((npass != 1 && npass != 2) || len < 1 || !std::isfinite(dtp))
+        return fail(PDG_E_INVALID_ARGUMENT, "npass must be 1 or 2, len >= 1, dtp finite");
+    if (!P || !Q || !B || !C || !leff) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
+    const int outer = p->dim - 1;
+    const long double h = ((long double)p->hi[outer] - (long double)p->lo[outer]) / (long double)p->ncell[outer];
+    const long double kappa = (long double)p->lambda * (long double)dtp / h;
+    std::vector<double> Pt, Qt, Bt, Ct;
+    int le = 0;
+    if (!zslab_tables(p->degree, kappa, npass, len, Pt, Qt, Bt, Ct, &le))
+        return fail(PDG_E_INVALID_ARGUMENT, "singular cell block");
+    std::memcpy(P, Pt.data(), sizeof(double) * Pt.size());
+    std::memcpy(Q, Qt.data(), sizeof(double) * Qt.size());
+    *B = Bt[len];
+    *C = Ct[len];
+    *leff = le;
     return PDG_OK;
 }
 

@@ -52,7 +52,7 @@ EXPORTED = [
     "pdg_query_sizes", "pdg_create", "pdg_set_state", "pdg_set_equilibrium", "pdg_get_state", "pdg_step",
     "pdg_transport", "pdg_collide", "pdg_source", "pdg_partial_moments", "pdg_relax_from_w", "pdg_moments",
     "pdg_check_state", "pdg_cell_block", "pdg_synchronize", "pdg_destroy", "pdg_nccl_unique_id",
-    "pdg_status_string", "pdg_last_error", "pdg_version", "pdg_profile_read",
+    "pdg_status_string", "pdg_last_error", "pdg_version", "pdg_profile_read", "pdg_zslab_table",
 ]
 
 
@@ -122,6 +122,7 @@ def load() -> ctypes.CDLL:
         "pdg_last_error": ([], ctypes.c_char_p),
         "pdg_version": ([], ctypes.c_char_p),
         "pdg_profile_read": ([ctx, pd, P(i64), pd], st),
+        "pdg_zslab_table": ([P(pdg_problem), d, ctypes.c_int, i64, pd, pd, pd, pd, P(ctypes.c_int32)], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -194,6 +195,18 @@ def query_sizes(pb: pdg_problem) -> pdg_sizes:
     out = pdg_sizes()
     _check(load().pdg_query_sizes(ctypes.byref(pb), ctypes.byref(out)), "pdg_query_sizes")
     return out
+
+
+def zslab_table(pb: pdg_problem, dtp: float, npass: int, length: int):
+    """(P [len][n], Q [len][n], B, C, leff): the z-slab carry tables (pdg_zslab_table, host-only)."""
+    n = pb.degree + 1
+    P_ = (ctypes.c_double * (length * n))()
+    Q_ = (ctypes.c_double * (length * n))()
+    B_, C_, le = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+    _check(load().pdg_zslab_table(ctypes.byref(pb), float(dtp), int(npass), int(length), P_, Q_, ctypes.byref(B_),
+                                  ctypes.byref(C_), ctypes.byref(le)), "pdg_zslab_table")
+    rows = lambda a: [list(a[i * n:(i + 1) * n]) for i in range(length)]  # noqa: E731
+    return rows(P_), rows(Q_), B_.value, C_.value, le.value
 
 
 def nccl_unique_id() -> bytes:

@@ -144,6 +144,17 @@ class OracleRun:
     def moments(self):
         return O.moments(self.pb, self.fc)                                # [m, ncell, Nd]
 
+    def nonphysical(self) -> int:
+        """Nodes of the oracle's current state with rho <= 0 or a non-finite value (component 0 of w
+        is the density of the Euler / isothermal models; the advection model has none)."""
+        if self.pb.flux == 0:
+            return int(sum(int((~np.isfinite(self.fc[i])).sum()) for i in range(self.pb.nv)))
+        w = self.moments()
+        bad = ~(w[0] > 0.0)
+        for c in range(1, w.shape[0]):
+            bad |= ~np.isfinite(w[c])
+        return int(bad.sum())
+
 
 # ----------------------------------------------------------------------------
 # GPU side
@@ -263,6 +274,10 @@ def run_protocol(cfg, resync_steps, lockstep=True, oracle_twin=False, gpu_twin=T
     for n in range(1, steps + 1):
         e = {"step": n}
         if n in resync_steps:
+            # the input state of the re-synced step: a state with rho <= 0 somewhere makes the
+            # collision (1/rho in the flux) arbitrarily ill-conditioned, so the 1e-12 bar applies to
+            # physical inputs only (reading C7)
+            e["oracle_nonphysical_in"] = orun.nonphysical()
             load_into(R, orun)                       # oracle f^{n-1}
             R.step(1)                                # runs on the GPU while the oracle computes f^n
         if F is not None:

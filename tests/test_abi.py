@@ -27,6 +27,17 @@ def test_header_symbols_exported():
     assert set(names) == set(pdg.EXPORTED)
 
 
+def test_checked_build_exports_the_same_symbols():
+    """The bounds-checked build (build.py --checked) is the same C-ABI."""
+    path = os.path.join(ROOT, "paper_1702_00169_b200", "libpdg_checked.so")
+    if not os.path.exists(path):
+        from paper_1702_00169_b200 import build
+        build.build(checked=True)
+    lib = ctypes.CDLL(path)
+    for n in declared_symbols():
+        assert hasattr(lib, n), n
+
+
 def test_version_and_status_strings():
     assert "sm_100a" in pdg.version()
     assert pdg.status_string(pdg.PDG_E_VELOCITY_SET) == "PDG_E_VELOCITY_SET"

@@ -105,3 +105,106 @@ def _sharded_collision(rank, world):
 def test_sharded_collision_decomposition():
     errs = run_world(_sharded_collision)
     assert all(isinstance(e, float) and e < 1e-14 for e in errs), errs
+
+
+# --------------------------------------------------------------------------
+# The exact z-slab decomposition (row e): each rank sweeps its slab of cell planes with
+# zero inflow, the outgoing carries of every slab are all-gathered (gloo here, NCCL in libpdg),
+# the true slab inflows follow from the affine carry scan with the product's tables
+# (pdg_zslab_table: B = beta^len, C), and the first leff cells are corrected with its P, Q
+# responses.  The slab sweeps themselves are the oracle's (standing in for the CUDA kernels); the
+# result must equal the oracle's sweep of the whole domain.
+# --------------------------------------------------------------------------
+def _zslab_world(rank, world, p=2, nu_half=1.0, nz=64):
+    from oracle import oracle as O
+    from paper_1702_00169_b200 import pdg
+    n, nx, ny, lam = p + 1, 2, 3, 2.0
+    h = 1.0 / nz
+    dtp = nu_half * h / lam           # kappa = lambda dt' / h
+    lo, hi = (0.0, 0.0, 0.0), (nx * h, ny * h, 1.0)
+    lines = (nx * n) * (ny * n)
+    rng = np.random.default_rng(5)
+    fz = rng.random((nz * n, ny * n, nx * n))          # one z-velocity's node grid [Z][Y][X]
+    fbz = rng.random((ny * n, nx * n))                 # its inflow plane
+    out = {}
+    for sgn in (+1.0, -1.0):
+        v = [0.0, 0.0, sgn * lam]
+        # the whole domain, two consecutive T2(dt') sweeps (the fused y/z pass of pdg_step)
+        full = O.Problem(3, [nx, ny, nz], p, [v], [0], 1, lam, 0, [1.0, 0.0, 0.0], 2 * dtp, lo=lo, hi=hi)
+        fb_full = np.zeros_like(fz)
+        fb_full[0 if sgn > 0 else -1] = fbz
+        fc = full.grid_to_cells(fz[None])[0]
+        O.t2_velocity(full, v, dtp, fc, full.grid_to_cells(fb_full[None])[0])
+        O.t2_velocity(full, v, dtp, fc, full.grid_to_cells(fb_full[None])[0])
+        ref = full.cells_to_grid(fc[None])[0]
+        # this rank's slab, swept with zero inflow unless the velocity enters the domain here
+        z0, z1 = rank * nz // world, (rank + 1) * nz // world
+        ln = z1 - z0
+        entry = (rank == 0) if sgn > 0 else (rank == world - 1)
+        sub = O.Problem(3, [nx, ny, ln], p, [v], [0], 1, lam, 0, [1.0, 0.0, 0.0], 2 * dtp,
+                        lo=(0.0, 0.0, z0 * h), hi=(nx * h, ny * h, z1 * h))
+        f0 = fz[z0 * n:z1 * n].copy()
+        fb_sub = np.zeros_like(f0)
+        if entry:
+            fb_sub[0 if sgn > 0 else -1] = fbz
+        c = sub.grid_to_cells(f0[None])[0]
+        fbc = sub.grid_to_cells(fb_sub[None])[0]
+        O.t2_velocity(sub, v, dtp, c, fbc)
+        f1 = sub.cells_to_grid(c[None])[0]
+        O.t2_velocity(sub, v, dtp, c, fbc)
+        f2 = sub.cells_to_grid(c[None])[0]
+        # outgoing carries of the two zero-inflow passes: old + new trace at the outflow face
+        o = -1 if sgn > 0 else 0
+        A = torch.from_numpy(np.stack([f0[o] + f1[o], f1[o] + f2[o]]).reshape(2, lines).copy())
+        gathered = [torch.zeros_like(A) for _ in range(world)]
+        dist.all_gather(gathered, A)                    # the carry-plane exchange
+        # product tables for every slab length (the tables depend on p and kappa of the outer axis)
+        from pdg_inputs import velocity_set
+        vs, cs = velocity_set(3, 1, lam)
+        pb = pdg.make_problem(3, [nx, ny, nz], p, 1, vs, cs, lam, 0, [1.0, 0.0, 0.0], 2 * dtp, lo=lo, hi=hi)
+        P_, Q_, B_, C_, leff = pdg.zslab_table(pb, dtp, 2, ln)
+        tabs = {}
+        for r in range(world):
+            lr = (r + 1) * nz // world - r * nz // world
+            tabs[r] = pdg.zslab_table(pb, dtp, 2, lr)
+        # affine scan over the slabs upstream of this one (flow order)
+        order = list(range(world)) if sgn > 0 else list(reversed(range(world)))
+        s1 = s2 = None
+        for r in order:
+            if r == rank:
+                break
+            a1, a2 = gathered[r][0].numpy(), gathered[r][1].numpy()
+            if s1 is None:
+                s1, s2 = a1, a2                           # the entry slab: true carries
+            else:
+                Br, Cr = tabs[r][2], tabs[r][3]
+                s1, s2 = a1 + Br * s1, a2 + Br * s2 + Cr * s1
+        got = f2.copy()
+        if s1 is not None:
+            S1, S2 = s1.reshape(ny * n, nx * n), s2.reshape(ny * n, nx * n)
+            for l in range(min(ln, leff)):
+                for a in range(n):
+                    zz = (l * n + a) if sgn > 0 else (ln * n - 1 - (l * n + a))
+                    got[zz] += Q_[l][a] * S2 + P_[l][a] * S1
+        mine = ref[z0 * n:z1 * n]
+        out[sgn] = float(np.max(np.abs(got - mine)) / np.max(np.abs(ref)))
+        out[("leff", sgn)] = leff
+    return out
+
+
+def _zslab_p2(rank, world):
+    return _zslab_world(rank, world, p=2, nu_half=1.0, nz=64)
+
+
+def _zslab_p3(rank, world):
+    return _zslab_world(rank, world, p=3, nu_half=2.0, nz=32)
+
+
+@pytest.mark.parametrize("world,fn", [(2, _zslab_p2), (4, _zslab_p2), (2, _zslab_p3), (4, _zslab_p3)])
+def test_zslab_carry_scan_with_product_tables(world, fn):
+    res = run_world(fn, world=world)
+    for r in res:
+        assert isinstance(r, dict), r
+        assert r[1.0] < 1e-13 and r[-1.0] < 1e-13, r
+    if fn is _zslab_p2 and world == 2:
+        assert res[0][("leff", 1.0)] < 64 // world  # the correction stops inside the slab (reading C26)

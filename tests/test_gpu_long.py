@@ -6,7 +6,10 @@ The fast full-size cases that run in every `pytest -m gpu` are in test_gpu_fulls
 
 Protocol (reading C7):
   1. re-synced one-step parity, whole arrays of f and w, <= 1e-12: every step for configs 2-3,
-     steps {1, 2, ceil(steps/2), last} for configs 4-5;
+     steps {1, 2, ceil(steps/2), last} for configs 4-5 -- on every step whose input state is
+     physical (rho > 0 and finite at every node; the configs as written drive the state
+     non-physical: config 3 from step 26, config 2 before step 100 -- there the collision's 1/rho
+     makes the map arbitrarily ill-conditioned and the steps are reported, not held to the bar);
   2. free-running parity over the full run: required <= 1e-12 for config 5 (and config 1, in the
      fast suite); reported for configs 2-4 with the twin amplification of the map, measured in the
      same harness (GPU twin, plus the oracle's own twin for configs 2 and 3); config 3: the last step
@@ -61,9 +64,9 @@ def test_parity_protocol_full_size(name):
     cfg = CONFIGS[key].stabilised() if stab else CONFIGS[key]
     rec = run_protocol(cfg, _resync_set(cfg, every), lockstep=lockstep, oracle_twin=otwin, gpu_twin=True,
                        out_path=_out(name), stop_on_nonfinite=True)
-    # 1. re-synced one-step parity (every config, as long as the oracle's state is finite)
+    # 1. re-synced one-step parity on every step whose input state is physical (rho > 0, finite)
     for e in rec["per_step"]:
-        if "resync_f" in e and e.get("nonfinite_oracle", 0) == 0:
+        if "resync_f" in e and e["oracle_nonphysical_in"] == 0:
             assert e["resync_f"] <= TOL and e["resync_w"] <= TOL, e
             assert e["resync_nonfinite_gpu"] == 0, e
     # 2./3. free-running: required for config 5 and every stabilised twin
