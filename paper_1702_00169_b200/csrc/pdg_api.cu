@@ -54,6 +54,7 @@ struct NvtxRange {
     } while (0)
 
 constexpr int kMaxSlabs = 64;
+constexpr int kMaxChunks = 8;  // node chunks of the pipelined sharded collision
 
 struct Geometry {
     int dim = 0, p = 0, n = 0, m = 0, nv = 0, nvl = 0, v0 = 0;
@@ -468,6 +469,8 @@ struct pdg_ctx {
     pdg::SweepParams yz_params{};       // velocities along y / z
     pdg::SweepParams all_params{};      // every local velocity (inflow initialisation)
     pdg::NcclComm comm;
+    cudaStream_t comm_stream = nullptr;                // NCCL sums of the pipelined sharded collision
+    cudaEvent_t ev_pm[kMaxChunks] = {}, ev_ar[kMaxChunks] = {};  // per chunk: partial moments written, summed
     int device = 0;
     Profiler prof;
     int sms = 148;
@@ -936,24 +939,25 @@ void launch_relax_t(pdg_ctx *c, double ca, double cb)
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
 }
 
+// the sharded collision's halves on the node chunk [x0, x0 + cnt) (velocity / component stride nnodes)
 template <int DIM, int MODEL>
-void launch_partial_t(pdg_ctx *c)
+void launch_partial_t(pdg_ctx *c, int64_t x0, int64_t cnt)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const int grid = grid_for(cnt, 256);
     const int e = prof_begin(c);
     pdg::partial_moments_kernel<DIM, MODEL>
-        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl);
-    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)c->g.nnodes);
+        <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl);
+    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)cnt);
 }
 
 template <int DIM, int MODEL>
-void launch_relax_from_w_t(pdg_ctx *c, double ca, double cb)
+void launch_relax_from_w_t(pdg_ctx *c, int64_t x0, int64_t cnt, double ca, double cb)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const int grid = grid_for(cnt, 256);
     const int e = prof_begin(c);
     pdg::relax_from_w_kernel<DIM, MODEL>
-        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp, ca, cb);
-    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)c->g.nnodes);
+        <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl, c->mp, ca, cb);
+    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)cnt);
 }
 
 template <int DIM, int MODEL>
@@ -996,23 +1000,23 @@ void launch_relax_lbm_t(pdg_ctx *c, pdg::LocalOps op)
 }
 
 template <int D, int NV>
-void launch_partial_lbm_t(pdg_ctx *c)
+void launch_partial_lbm_t(pdg_ctx *c, int64_t x0, int64_t cnt)
 {
-    const unsigned grid = grid_all(c->g.nnodes, 256);
+    const unsigned grid = grid_all(cnt, 256);
     const int e = prof_begin(c);
     pdg::partial_moments_lbm_kernel<D, NV>
-        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm);
-    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)c->g.nnodes);
+        <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl, c->lbm);
+    prof_end(c, e, PDG_K_PARTIAL, 8.0 * (double)(c->g.nvl + c->g.m) * (double)cnt);
 }
 
 template <int D, int NV>
-void launch_relax_from_w_lbm_t(pdg_ctx *c, pdg::LocalOps op)
+void launch_relax_from_w_lbm_t(pdg_ctx *c, int64_t x0, int64_t cnt, pdg::LocalOps op)
 {
-    const unsigned grid = grid_all(c->g.nnodes, 256);
+    const unsigned grid = grid_all(cnt, 256);
     const int e = prof_begin(c);
     pdg::relax_from_w_lbm_kernel<D, NV>
-        <<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->lbm, op);
-    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)c->g.nnodes);
+        <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl, c->lbm, op);
+    prof_end(c, e, PDG_K_RELAX_W, 8.0 * (double)(2 * c->g.nvl + c->g.m) * (double)cnt);
 }
 
 // f = f^eq(w) (f_only) or, additionally, the inflow planes fb from f^eq(wb)
@@ -1073,23 +1077,66 @@ void wait_w_download(pdg_ctx *c)
     if (c->copy_stream) cudaStreamWaitEvent(c->stream, c->d2h_done, 0);
 }
 
-pdg_status partial_and_reduce(pdg_ctx *c)
+// Node chunks of the pipelined sharded collision: at most kMaxChunks, at least 2^20 nodes each.
+int collision_chunks(const pdg_ctx *c)
+{
+    if (!c->comm_stream) return 1;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, c->g.nnodes >> 20));
+}
+
+// The sharded collision (velocity decomposition, row a4), pipelined over node chunks (SURVEY §8(e)
+// mitigation 2): the partial moments of chunk k on the context stream; the NCCL sum of chunk k (one
+// call per moment field: w is [m][nodes]) on the communicator stream as soon as they are written;
+// then, if `relax` is given, the relaxation of chunk k on the context stream once its sum has
+// arrived.  The sum of chunk k overlaps the partial moments of the later chunks and the relaxation
+// of the earlier ones.  Every chunk's sum is joined back into the context stream (graph-capturable
+// fork/join).  Without a communicator (shard contexts for tests) only the partial moments run.
+template <class Relax>
+pdg_status sharded_collision(pdg_ctx *c, Relax relax)
 {
     wait_w_download(c);
-    if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
-    else PDG_DISPATCH(launch_partial_t, c);
+    const int64_t nn = c->g.nnodes;
+    const int K = collision_chunks(c);
+    auto chunk = [&](int k, int64_t *x0, int64_t *cnt) {
+        *x0 = nn * k / K;
+        *cnt = nn * (k + 1) / K - *x0;
+    };
+    for (int k = 0; k < K; ++k) {
+        int64_t x0, cnt;
+        chunk(k, &x0, &cnt);
+        if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c, x0, cnt);
+        else PDG_DISPATCH(launch_partial_t, c, x0, cnt);
+        if (K > 1) PDG_CUDA_TRY(cudaEventRecord(c->ev_pm[k], c->stream));
+    }
     pdg_status s = post_launch(c, "partial_moments");
     if (s != PDG_OK) return s;
-    if (sharded(c)) {
-        std::string err;
-        if (!c->comm.comm) return fail(PDG_E_NCCL, "communicator-less shard context: reduce w_dev yourself "
-                                                   "between pdg_partial_moments and pdg_relax_from_w");
-        const int e = prof_begin(c);
-        if (!c->comm.allreduce_sum(c->w, (size_t)c->g.m * (size_t)c->g.nnodes, c->stream, &err))
-            return fail(PDG_E_NCCL, err);
-        prof_end(c, e, PDG_K_ALLREDUCE, 8.0 * (double)c->g.m * (double)c->g.nnodes);
+    if (!sharded(c)) return PDG_OK;
+    if (!c->comm.comm) return fail(PDG_E_NCCL, "communicator-less shard context: reduce w_dev yourself "
+                                               "between pdg_partial_moments and pdg_relax_from_w");
+    std::string err;
+    cudaStream_t cs = (K > 1) ? c->comm_stream : c->stream;
+    for (int k = 0; k < K; ++k) {
+        int64_t x0, cnt;
+        chunk(k, &x0, &cnt);
+        if (K > 1) PDG_CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_pm[k], 0));
+        const int e = prof_begin(c, cs);
+        for (int m = 0; m < c->g.m; ++m)
+            if (!c->comm.allreduce_sum(c->w + (int64_t)m * nn + x0, (size_t)cnt, cs, &err)) return fail(PDG_E_NCCL, err);
+        prof_end(c, e, PDG_K_ALLREDUCE, 8.0 * (double)c->g.m * (double)cnt, cs);
+        if (K > 1) PDG_CUDA_TRY(cudaEventRecord(c->ev_ar[k], cs));
     }
-    return PDG_OK;
+    for (int k = 0; k < K; ++k) {
+        int64_t x0, cnt;
+        chunk(k, &x0, &cnt);
+        if (K > 1) PDG_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_ar[k], 0));
+        relax(x0, cnt);
+    }
+    return post_launch(c, "relax_from_w");
+}
+
+pdg_status partial_and_reduce(pdg_ctx *c)
+{
+    return sharded_collision(c, [](int64_t, int64_t) {});
 }
 
 // One pass of the local operators of a lattice set: S2(hs1), C2(dt) (if with_c), S2(hs2).
@@ -1106,10 +1153,7 @@ pdg_status local_pass_lbm(pdg_ctx *c, double hs1, bool with_c, double dt, double
         PDG_LBM_DISPATCH(launch_relax_lbm_t, c, op);
         return post_launch(c, "relax");
     }
-    pdg_status s = partial_and_reduce(c);
-    if (s != PDG_OK) return s;
-    PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, op);
-    return post_launch(c, "relax_from_w");
+    return sharded_collision(c, [&](int64_t x0, int64_t cnt) { PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, x0, cnt, op); });
 }
 
 pdg_status collide(pdg_ctx *c, double dt)
@@ -1122,10 +1166,7 @@ pdg_status collide(pdg_ctx *c, double dt)
         PDG_DISPATCH(launch_relax_t, c, ca, cb);
         return post_launch(c, "relax");
     }
-    pdg_status s = partial_and_reduce(c);
-    if (s != PDG_OK) return s;
-    PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
-    return post_launch(c, "relax_from_w");
+    return sharded_collision(c, [&](int64_t x0, int64_t cnt) { PDG_DISPATCH(launch_relax_from_w_t, c, x0, cnt, ca, cb); });
 }
 
 // C2(dt) followed by npass sweeps T2(dtp) of the x-velocities, in one pass over f.
@@ -1657,6 +1698,16 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
             pdg_destroy(c);
             return fail(PDG_E_NCCL, err);
         }
+        int prio = 0;
+        cudaStreamGetPriority(c->stream, &prio);
+        bool ok = cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio) == cudaSuccess;
+        for (int k = 0; k < kMaxChunks && ok; ++k)
+            ok = cudaEventCreateWithFlags(&c->ev_pm[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_ar[k], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            pdg_destroy(c);
+            return fail(PDG_E_CUDA, "cannot create the communicator stream");
+        }
     }
     *out = c;
     return PDG_OK;
@@ -1794,8 +1845,8 @@ pdg_status pdg_partial_moments(pdg_ctx *c)
     DeviceGuard dg(c);
     if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
     wait_w_download(c);  // PDG_ASYNC_HOST: a pending pdg_moments download may still read w_dev
-    if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c);
-    else PDG_DISPATCH(launch_partial_t, c);
+    if (c->g.lattice) PDG_LBM_DISPATCH(launch_partial_lbm_t, c, 0, c->g.nnodes);
+    else PDG_DISPATCH(launch_partial_t, c, 0, c->g.nnodes);
     return post_launch(c, "partial_moments");
 }
 
@@ -1809,9 +1860,9 @@ pdg_status pdg_relax_from_w(pdg_ctx *c, double dt)
     collision_coeffs(c, dt, &ca, &cb);
     if (c->g.lattice) {
         pdg::LocalOps op{0.0, ca, cb, 0.0};
-        PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, op);
+        PDG_LBM_DISPATCH(launch_relax_from_w_lbm_t, c, 0, c->g.nnodes, op);
     } else {
-        PDG_DISPATCH(launch_relax_from_w_t, c, ca, cb);
+        PDG_DISPATCH(launch_relax_from_w_t, c, 0, c->g.nnodes, ca, cb);
     }
     return post_launch(c, "relax_from_w");
 }
@@ -1939,6 +1990,14 @@ void pdg_destroy(pdg_ctx *c)
     }
     for (cudaEvent_t ev : {c->w_ready, c->d2h_done, c->stage_free, c->stage_full})
         if (ev) cudaEventDestroy(ev);
+    if (c->comm_stream) {
+        cudaStreamSynchronize(c->comm_stream);
+        cudaStreamDestroy(c->comm_stream);
+    }
+    for (int k = 0; k < kMaxChunks; ++k) {
+        if (c->ev_pm[k]) cudaEventDestroy(c->ev_pm[k]);
+        if (c->ev_ar[k]) cudaEventDestroy(c->ev_ar[k]);
+    }
     c->comm.destroy();
     for (auto st : c->lat_streams)
         if (st) cudaStreamDestroy(st);

@@ -623,15 +623,16 @@ __global__ void __launch_bounds__(256) relax_kernel(double *__restrict__ f, int6
 
 // Partial moments of the local velocity block [v0, v0 + nvl): w_c = sum of local f_i in c.
 // Velocity loops run over the compile-time n_v with a range test, so every index is static
-// (no local-memory arrays).
+// (no local-memory arrays).  f and w point at the first node of a chunk of `count` nodes;
+// nnodes is the velocity / component stride (chunks pipeline the NCCL sum, pdg_api.cu).
 template <int DIM, int MODEL>
 __global__ void __launch_bounds__(256) partial_moments_kernel(const double *__restrict__ f, double *__restrict__ w,
-                                                              int64_t nnodes, int v0, int nvl)
+                                                              int64_t nnodes, int64_t count, int v0, int nvl)
 {
     constexpr int M = Model<DIM, MODEL>::M;
     constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < count; x += stride) {
         double acc[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) acc[c] = 0.0;
@@ -643,17 +644,18 @@ __global__ void __launch_bounds__(256) partial_moments_kernel(const double *__re
     }
 }
 
-// Collision of the local velocities from reduced moments w (sharded path, row a4).
+// Collision of the local velocities from reduced moments w (sharded path, row a4), on a chunk of
+// `count` nodes (f, w at its first node; nnodes is the stride).
 template <int DIM, int MODEL>
 __global__ void __launch_bounds__(256) relax_from_w_kernel(double *__restrict__ f, const double *__restrict__ w,
-                                                           int64_t nnodes, int v0, int nvl, ModelParams P,
+                                                           int64_t nnodes, int64_t count, int v0, int nvl, ModelParams P,
                                                            double ca, double cb)
 {
     using Md = Model<DIM, MODEL>;
     constexpr int M = Md::M;
     constexpr int NV = M * 2 * DIM;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nnodes; x += stride) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < count; x += stride) {
         double fl[NV], wl[M];
 #pragma unroll
         for (int i = 0; i < NV; ++i) fl[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;

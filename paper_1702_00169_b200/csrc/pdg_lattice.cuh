@@ -1050,14 +1050,14 @@ __global__ void __launch_bounds__(256, 4) relax_lbm2_kernel(double *__restrict__
 // Partial moments of the local velocities [v0, v0 + nvl) (sharded path, pdg_moments).
 template <int D, int NV>
 __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *__restrict__ f, double *__restrict__ w,
-                                                                  int64_t nnodes, int v0, int nvl,
+                                                                  int64_t nnodes, int64_t count, int v0, int nvl,
                                                                   const __grid_constant__ LbmParams L)
 {
     // one node per thread (no grid-stride loop: the velocity constants stay constant-bank operands
-    // instead of being hoisted into registers)
+    // instead of being hoisted into registers); a chunk of `count` nodes, stride nnodes
     {
         const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (x >= nnodes) return;
+        if (x >= count) return;
         double fv[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) fv[i] = (i >= v0 && i < v0 + nvl) ? __ldcs(f + (int64_t)(i - v0) * nnodes + x) : 0.0;
@@ -1072,11 +1072,11 @@ __global__ void __launch_bounds__(256) partial_moments_lbm_kernel(const double *
 // so every local velocity is loaded, updated and stored in turn (no per-node f array).
 template <int D, int NV>
 __global__ void __launch_bounds__(256, 2) relax_from_w_lbm_kernel(double *__restrict__ f, const double *__restrict__ w,
-                                                                  int64_t nnodes, int v0, int nvl,
+                                                                  int64_t nnodes, int64_t count, int v0, int nvl,
                                                                   const __grid_constant__ LbmParams L, const LocalOps op)
 {
     const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= nnodes) return;
+    if (x >= count) return;
     double wl[D + 1];
 #pragma unroll
     for (int c = 0; c <= D; ++c) wl[c] = __ldcs(w + (int64_t)c * nnodes + x);

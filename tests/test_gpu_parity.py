@@ -489,3 +489,20 @@ def test_async_host_mode_equals_sync():
             S.destroy()
         for a, b in zip(outs["sync"], outs["async"]):
             assert np.array_equal(a, b)
+
+
+def test_nccl_pipelined_sharded_collision_chunks():
+    """The sharded collision pipelined over node chunks (partial moments of chunk k, its NCCL sum on
+    the communicator stream, relaxation of chunk k once summed; SURVEY §8(e) mitigation 2), through
+    libpdg's own single-rank communicator on a grid large enough for several chunks (>= 2^20 nodes
+    each): equal to the oracle's M2 steps."""
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(48).stabilised()        # 144^3 = 2.99 M nodes -> 2 chunks
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg, nccl_id=pdg.nccl_unique_id(), flags=pdg.PDG_PROFILE)
+    S.step(2)
+    got = to_np(S.get_state(), f0.shape)
+    prof = S.profile_read()
+    assert prof["allreduce"][1] == 2 * 2 and prof["partial_moments"][1] == 2 * 2, prof
+    assert rel_maxnorm(got, O.m2_run(pb, f0, fbg, 2)) < TOL_STEP
+    S.destroy()
