@@ -8,8 +8,10 @@ BASELINE config 5 (3-D isothermal, 256^3 cells, p=2, D3Q6 x 4 components: 10.9 G
 node.velocity updates per step; f = 87 GB in place, far larger than L2, so no L2
 flush is needed between steps).  Multi-GPU (torchrun): the exact z-slab decomposition by
 default (--decomp zslab: slabs of cell planes, NCCL all-gather of carry planes), or
-velocity shards with one NCCL sum of the moments per collision (--decomp velocity;
-the default for --lattice workloads); strong scaling: total work fixed.
+velocity shards with one NCCL sum of the moments per collision, pipelined over node chunks
+(--decomp velocity: the north star's partition; the default for --lattice workloads); the
+line's `alt_decomposition` times the other one in the same run (--one-decomp skips it);
+strong scaling: total work fixed.
 
 The JSON line adds:
   roofline     : the dominant kernel's algorithmic bytes / its CUDA-event time (on the
@@ -402,20 +404,52 @@ def run_product(args, cfg):
         if world == 1 and rank == 0 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, args.cpu_cells)
 
+        S.destroy()
+        # several ranks: also time the other decomposition (velocity sharding is the north star's
+        # partition, the exact z-slab decomposition the scalable one; both exact)
+        alt = None
+        if world > 1 and not args.lattice and not args.one_decomp:
+            other = "velocity" if args.decomp == "zslab" else "zslab"
+            T = pdist.sharded_solver(cfg, device, flags=pdg.PDG_PROFILE, stream=stream.cuda_stream,
+                                     decomposition={"velocity": pdg.PDG_DECOMP_VELOCITY,
+                                                    "zslab": pdg.PDG_DECOMP_ZSLAB}[other],
+                                     slabs_per_rank=1)
+            fill_w0(cfg, T.w, device, T.sizes)
+            T.set_equilibrium(T.w)
+            T.step(args.warmup)
+            T.profile_read()
+            torch.cuda.synchronize(device)
+            dist.barrier()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            T.step(args.steps)
+            a1.record(stream)
+            torch.cuda.synchronize(device)
+            oms = pdist.max_over_ranks(a0.elapsed_time(a1), device=device)
+            oprof = T.profile_read()
+            T.destroy()
+            alt = {"decomposition": other, "value": cfg.updates_per_step * args.steps / (oms * 1e-3),
+                   "unit": UNIT, "ms_per_step": oms / args.steps,
+                   "parallelism": config_block(cfg, world, other, 1)["parallelism"],
+                   "kernels": {k: {"ms_total": v[0], "launches": v[1]} for k, v in oprof.items() if v[1] > 0}}
+
         if rank == 0:
             line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                     "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                     "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                     "data": "synthetic (seeded pdg_inputs recipe of the config)",
-                    "config": config_block(cfg, world, args.decomp, args.slabs_per_rank), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                    "config": config_block(cfg, world, args.decomp, args.slabs_per_rank), "roofline": roofline,
+                    "cpu_baseline": cpu, "e2e": e2e,
                     "gpu_launches": launches, "clocks": clk, "kernels": kernels, "step_roofline": step_roof,
                     "nonphysical_nodes": bad,
                     "updates_vs_48B_model": value * 48.0 / (peak * 1e9 * world),
                     "updates_vs_48B_model_note": "updates/s x 48 B (SURVEY 8(d) three-pass model) / (HBM peak x "
                                                  "GPUs); exceeds 1 because consecutive half-steps share a pass: "
                                                  "a throughput ratio, not a roofline fraction"}
+            if alt is not None:
+                line["alt_decomposition"] = alt
             print(json.dumps(line), flush=True)
-        S.destroy()
     if launched:
         dist.destroy_process_group()
 
@@ -435,6 +469,8 @@ def main():
     ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
                     help="multi-GPU decomposition (default: zslab when launched on several ranks)")
     ap.add_argument("--slabs-per-rank", type=int, default=1)
+    ap.add_argument("--one-decomp", action="store_true",
+                    help="several ranks: time only --decomp (default: also the other decomposition)")
     ap.add_argument("--lattice", default=None, choices=["D2Q9", "D3Q15", "D3Q19", "D3Q27"],
                     help="NEXT-2 workload: isothermal LBM on this lattice (replaces --config)")
     ap.add_argument("--cells", type=int, default=128, help="cells per axis of the --lattice workload")
