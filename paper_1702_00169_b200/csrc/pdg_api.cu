@@ -602,6 +602,45 @@ int strided_segments(const pdg_ctx *c, const pdg::SweepParams &sp)
     return std::max(1, nseg);
 }
 
+// Lines per tile of sweep_cols_kernel, and whether a strided batch can use it: every velocity's
+// lines tile by kColsW (inner % kColsW == 0), no outgoing carries (z-slab entries), and a tile of
+// rows fits the shared memory of two CTAs per SM.
+constexpr int kColsW = 16;
+
+int cols_K(int ncells) { return ncells <= 64 ? 2 : (ncells <= 128 ? 4 : 8); }
+
+size_t cols_smem(int n, const pdg::SweepParams &sp)
+{
+    int nc = 0;
+    for (int i = 0; i < sp.nvel; ++i) nc = std::max(nc, sp.v[i].ncells);
+    const int K = cols_K(nc);
+    return sizeof(double) * (size_t)kColsW * (size_t)(nc * n + (nc * n) / (K * n) + 1);
+}
+
+bool use_cols(const pdg_ctx *c, const pdg::SweepParams &sp)
+{
+    if (sp.nvel == 0 || cols_smem(c->g.n, sp) > 110 * 1024) return false;
+    for (int i = 0; i < sp.nvel; ++i) {
+        const pdg::SweepVel &V = sp.v[i];
+        if (V.inner % kColsW != 0 || V.cout_off >= 0 || V.ncells != sp.v[0].ncells) return false;
+    }
+    return true;
+}
+
+template <int N, int NPASS, int K>
+void launch_cols_k(pdg_ctx *c, const pdg::SweepParams &sp, int64_t maxl)
+{
+    auto kern = pdg::sweep_cols_kernel<N, NPASS, K, kColsW>;
+    const size_t smem = cols_smem(N, sp);
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
+    if (c->launch_cache.find(key) == c->launch_cache.end()) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+        c->launch_cache[key] = 1;
+    }
+    dim3 grid((unsigned)((maxl + kColsW - 1) / kColsW), (unsigned)sp.nvel);
+    kern<<<grid, 256, smem, c->stream>>>(sp);
+}
+
 template <int N, int NPASS>
 void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParams &yzp, int which)
 {
@@ -610,7 +649,13 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
         for (int i = 0; i < yzp.nvel; ++i) maxl = std::max(maxl, yzp.v[i].nlines);
         const int e = prof_begin(c);
         const int nseg = strided_segments(c, yzp);
-        if (nseg > 1) {
+        if (nseg > 1 && use_cols(c, yzp)) {
+            // few long lines (2-D grids): tiles of adjacent lines staged in shared memory
+            const int K = cols_K(yzp.v[0].ncells);
+            if (K == 2) launch_cols_k<N, NPASS, 2>(c, yzp, maxl);
+            else if (K == 4) launch_cols_k<N, NPASS, 4>(c, yzp, maxl);
+            else launch_cols_k<N, NPASS, 8>(c, yzp, maxl);
+        } else if (nseg > 1) {
             dim3 grid((unsigned)((maxl + 31) / 32), (unsigned)yzp.nvel);
             pdg::sweep_strided_seg_kernel<N, NPASS><<<grid, dim3(32, nseg), 0, c->stream>>>(yzp, nseg);
         } else {

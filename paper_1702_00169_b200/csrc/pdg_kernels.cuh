@@ -401,6 +401,57 @@ __device__ __forceinline__ void warp_line_sweep(double *row, int ncells, bool up
 }
 
 // ---------------------------------------------------------------------------
+// T2 sweep(s) along a strided axis for grids with few lines (2-D y-velocities: config 2 has
+// 6144 y-lines of 768 nodes, too few for the thread-per-line kernel): a CTA stages a tile of
+// CW adjacent lines in shared memory (each node row of the tile is CW contiguous doubles:
+// coalesced loads and stores, once per pass over f), one warp per line sweeps it with the
+// lane-segment affine scan of warp_line_sweep (NPASS sweeps in shared memory), the tile is
+// stored back.  Data move once, unlike the segmented kernel's zero-inflow re-reads.
+// Requires inner % CW == 0 (a tile's lines are adjacent in memory) and no outgoing-carry output.
+// ---------------------------------------------------------------------------
+template <int N, int K>
+__host__ __device__ constexpr int cols_row_len(int ncells)
+{
+    return ncells * N + (ncells * N) / (K * N) + 1;
+}
+
+template <int N, int NPASS, int K, int CW>
+__global__ void __launch_bounds__(256) sweep_cols_kernel(const SweepParams P)
+{
+    extern __shared__ double scol[];
+    const SweepVel V = P.v[blockIdx.y];
+    const int64_t line0 = (int64_t)blockIdx.x * CW;
+    if (line0 >= V.nlines) return;
+    constexpr int SEG = K * N;
+    const int Lk = V.ncells * N;
+    const int Lp = cols_row_len<N, K>(V.ncells);
+    const int64_t base = V.f_off + (line0 / V.inner) * (V.inner * Lk) + (line0 % V.inner);
+    double *g0 = P.f + base;  // node y of tile line c at g0 + y * inner + c
+    PDG_CHECK_IDX(base + (int64_t)(Lk - 1) * V.inner + CW - 1, P.f_elems, "sweep_cols f");
+    for (int t = threadIdx.x; t < Lk * CW; t += blockDim.x) {
+        const int y = t / CW, cc = t - y * CW;
+        scol[cc * Lp + y + y / SEG] = __ldcs(g0 + (int64_t)y * V.inner + cc);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    double M[N * N], g[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
+    for (int cc = warp; cc < CW; cc += nwarps) {
+        PDG_CHECK_IDX(V.fb_off + line0 + cc, P.fb_elems, "sweep_cols fb");
+        const double s0 = V.zero_inflow ? 0.0 : 2.0 * P.fb[V.fb_off + line0 + cc];  // ghost: f^b old + new
+        warp_line_sweep<N, NPASS, K>(scol + cc * Lp, V.ncells, V.sign > 0, M, g, s0, lane);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < Lk * CW; t += blockDim.x) {
+        const int y = t / CW, cc = t - y * CW;
+        __stcs(g0 + (int64_t)y * V.inner + cc, scol[cc * Lp + y + y / SEG]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Collision fused with the moment reduction AND the following T2 sweep(s) of the
 // x-velocities (G = 1).  One CTA per x-line (fixed y, z):
 //   phase 1: per node, w = P f, f^eq(w), f <- ca f + cb f^eq for all n_v velocities;

@@ -506,3 +506,45 @@ def test_nccl_pipelined_sharded_collision_chunks():
     assert prof["allreduce"][1] == 2 * 2 and prof["partial_moments"][1] == 2 * 2, prof
     assert rel_maxnorm(got, O.m2_run(pb, f0, fbg, 2)) < TOL_STEP
     S.destroy()
+
+
+@pytest.mark.parametrize("dim,ncell,p,flux,fparams,m", [
+    (2, (16, 16), 2, 1, (1.4,), 4),       # 2-D Euler: 48-node lines tile by 16
+    (2, (32, 32), 2, 1, (1.4,), 4),
+    (2, (20, 20), 3, 1, (1.4,), 4),       # p = 3: 80-node lines
+    (2, (40, 24), 1, 2, (1.0,), 3),       # p = 1, anisotropic
+    (3, (4, 30, 30), 3, 2, (1.0,), 4),    # 3-D with few strided lines: y and z tiles
+])
+def test_strided_tile_kernel_parity(dim, ncell, p, flux, fparams, m):
+    """sweep_cols_kernel (grids with few strided lines: tiles of 16 adjacent lines staged in shared
+    memory, warp-scan sweeps; the config-2 y-velocity path) inside free-running M2 steps (fused
+    two-sweep passes and single passes) against the oracle."""
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import velocity_set
+    lam = 3.5
+    vel, comp = velocity_set(dim, m, lam)
+    h = 1.0 / ncell[0]
+    hi = tuple(ncell[d] * h for d in range(dim)) + (1.0,) * (3 - dim)
+    dt = 2.0 * h / lam
+    pb = pdg.make_problem(dim, list(ncell), p, m, vel, comp, lam, flux, list(fparams), dt, hi=hi)
+    ob = O.Problem(dim, list(ncell), p, vel, comp, m, lam, flux, list(fparams), dt, hi=list(hi))
+    S = pdg.Solver(pb)
+    shape = ob.grid_shape()
+    rng = np.random.default_rng(sum(ncell) + p)
+    base = {1: 1.0, 2: 1.0}[flux]
+    f = base * (1.0 + 0.05 * (rng.random((ob.nv,) + shape) - 0.5)) / (2 * dim)
+    if flux == 1:
+        f[3 * 2 * dim:] *= 3.0  # energy large enough for a positive pressure
+    fb_full = base * (1.0 + 0.05 * rng.random((ob.nv,) + shape)) / (2 * dim)
+    if flux == 1:
+        fb_full[3 * 2 * dim:] *= 3.0
+
+    class _C:
+        pass
+    cv = _C()
+    cv.dim, cv.grid_shape = dim, shape
+    S.set_state(to_dev(f), to_dev(full_grid_to_planes(cv, fb_full, S.sizes.plane_stride)))
+    S.step(3)
+    got = to_np(S.get_state(), f.shape)
+    S.destroy()
+    assert rel_maxnorm(got, O.m2_run(ob, f, fb_full, 3)) < TOL_STEP
