@@ -140,6 +140,9 @@ typedef enum {
                                  by 8 m nnodes_local bytes) and pdg_moments' download runs on a library copy
                                  stream, so the upload of step k+1's input overlaps the download of step k's
                                  result (PCIe is full duplex) */
+#define PDG_NO_TMA      0x20u /* stage the line of the fused collision + x-sweep pass through registers instead of
+                                 Tensor-Memory-Accelerator bulk copies (the variant for odd line lengths;
+                                 same results; for measurement) */
 
 /* kernel kinds reported by pdg_profile_read */
 typedef enum {

@@ -934,9 +934,44 @@ size_t relax_x_smem(const pdg_ctx *c)
     return sizeof(double) * (size_t)(2 * c->g.m) * (size_t)Lp;
 }
 
+// shared memory of the TMA-staged variant: the raw line [n_v][Lx] + the x-velocity sweep rows
+size_t relax_x_tma_smem(const pdg_ctx *c) { return relax_x_smem(c) + sizeof(double) * (size_t)c->g.nvl * c->g.L[0]; }
+
+bool use_relax_x_tma(const pdg_ctx *c)
+{
+    return !(c->prob.flags & PDG_NO_TMA) && (c->g.L[0] % 2 == 0) && relax_x_tma_smem(c) <= 200 * 1024;
+}
+
+template <int DIM, int MODEL, int N, int NPASS, int K>
+void launch_relax_x_tma_k(pdg_ctx *c, const pdg::RelaxXParams &P)
+{
+    auto kern = pdg::relax_xsweep_tma_kernel<DIM, MODEL, N, NPASS, K>;
+    const size_t smem = relax_x_tma_smem(c);
+    const int lx = (int)(c->g.ncell[0] * N);
+    const int threads = std::min(256, ((lx + 31) / 32) * 32);
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), threads, smem);
+    auto it = c->launch_cache.find(key);
+    int occ = 0;  // resident CTAs on the GPU: the kernel is persistent
+    if (it != c->launch_cache.end()) occ = it->second;
+    else {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
+        cudaGetLastError();
+        occ = std::max(1, occ) * c->sms;
+        c->launch_cache[key] = occ;
+    }
+    const int64_t nlines = c->g.nnodes / (c->g.ncell[0] * N);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nlines, occ));
+    kern<<<grid, threads, smem, c->stream>>>(P, nlines);
+}
+
 template <int DIM, int MODEL, int N, int NPASS, int K>
 void launch_relax_x_k(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
 {
+    if (use_relax_x_tma(c)) {
+        launch_relax_x_tma_k<DIM, MODEL, N, NPASS, K>(c, P);
+        return;
+    }
     auto kern = pdg::relax_xsweep_kernel<DIM, MODEL, N, NPASS, K>;
     const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
     if (c->launch_cache.find(key) == c->launch_cache.end()) {  // per context: attributes are per device

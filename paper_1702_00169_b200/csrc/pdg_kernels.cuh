@@ -547,6 +547,135 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
 }
 
 // ---------------------------------------------------------------------------
+// The same fused pass with the line's raw data staged by the Tensor Memory Accelerator: a
+// persistent CTA walks lines blockIdx.x, blockIdx.x + gridDim.x, ...; one thread issues the n_v
+// bulk copies (cp.async.bulk, one per velocity row of the line, completion counted on an
+// mbarrier) of the NEXT line as soon as the collision has consumed the current one, so the
+// loads overlap the x sweeps and the stores of the current line.  Shared memory: the raw line
+// [n_v][Lx] + the padded sweep rows of the x velocities.  Requires an even Lx (16-byte aligned
+// rows).  Same arithmetic as relax_xsweep_kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// bulk copy global -> shared of `bytes` (multiple of 16, 16-byte aligned), counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int DIM, int MODEL, int N, int NPASS, int K>
+__global__ void __launch_bounds__(256) relax_xsweep_tma_kernel(const RelaxXParams P, int64_t nlines)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
+    constexpr int SEG = K * N;
+    extern __shared__ __align__(128) double sraw[];  // [NV][Lx] raw line, then [2M][Lp] sweep rows
+    __shared__ __align__(8) uint64_t bar;
+    const int Lx = P.ncx * N;
+    const int Lp = relax_x_row_len<N, K>(P.ncx);
+    double *sx = sraw + (size_t)NV * Lx;
+    const int64_t nn = P.nnodes;
+    const uint32_t row_bytes = (uint32_t)Lx * 8u;
+    auto issue = [&](int64_t line) {  // one thread: the NV velocity rows of `line`
+        mbar_arrive_expect_tx(&bar, row_bytes * NV);
+#pragma unroll 1
+        for (int i = 0; i < NV; ++i) bulk_g2s(sraw + (size_t)i * Lx, P.f + i * nn + line * Lx, row_bytes, &bar);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int64_t line = blockIdx.x;
+    if (threadIdx.x == 0 && line < nlines) issue(line);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    double Mb[N * N], gb[N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) Mb[i] = P.blk.M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) gb[i] = P.blk.g[i];
+    uint32_t parity = 0;
+    for (; line < nlines; line += gridDim.x) {
+        const int64_t base = line * Lx;
+        PDG_CHECK_IDX(base + (NV - 1) * nn + Lx - 1, P.f_elems, "relax_xsweep_tma f");
+        mbar_wait(&bar, parity);
+        parity ^= 1u;
+        // collision at every node of the line, from the staged raw rows
+        for (int X = threadIdx.x; X < Lx; X += blockDim.x) {
+            double fv[NV];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) fv[i] = sraw[(size_t)i * Lx + X];
+            double w[M];
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                double s = fv[c * 2 * DIM];
+#pragma unroll
+                for (int j = 1; j < 2 * DIM; ++j) s += fv[c * 2 * DIM + j];
+                w[c] = s;
+            }
+            double q[DIM][M];
+            Md::flux(w, q, P.mp);
+            const int xs = X + X / SEG;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const double val = fma(P.cb, feq_of<DIM, M>(i, w, q, P.mp), P.ca * fv[i]);
+                const int c = i / (2 * DIM), k = (i % (2 * DIM)) >> 1, s = i & 1;
+                if (k == 0) sx[(2 * c + s) * Lp + xs] = val;
+                else __stcs(P.f + base + X + i * nn, val);
+            }
+        }
+        __syncthreads();  // the raw rows are consumed: stage the next line behind the sweeps
+        if (threadIdx.x == 0 && line + gridDim.x < nlines) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(line + gridDim.x);
+        }
+        for (int v = warp; v < 2 * M; v += nwarps) {
+            const int c = v >> 1, s = v & 1;
+            const int i = c * 2 * DIM + s;
+            PDG_CHECK_IDX(i * P.plane_stride + line, P.fb_elems, "relax_xsweep_tma fb");
+            const double s0 = 2.0 * P.fb[i * P.plane_stride + line];  // ghost: f^b old + new
+            warp_line_sweep<N, NPASS, K>(sx + v * Lp, P.ncx, s == 0, Mb, gb, s0, lane);
+        }
+        __syncthreads();
+        for (int v = 0; v < 2 * M; ++v) {
+            const int c = v >> 1, s = v & 1;
+            const int i = c * 2 * DIM + s;
+            double *dst = P.f + base + i * nn;
+            const double *srow = sx + v * Lp;
+            for (int X = threadIdx.x; X < Lx; X += blockDim.x) __stcs(dst + X, srow[X + X / SEG]);
+        }
+        __syncthreads();  // sx is rewritten by the next line's collision
+    }
+}
+
+// ---------------------------------------------------------------------------
 // T2 sweep along x (contiguous): warp per line, lanes = cells, affine warp scan.
 // ---------------------------------------------------------------------------
 constexpr int kXsWarps = 8;

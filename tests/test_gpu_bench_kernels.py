@@ -56,7 +56,10 @@ CASES = [
 
 @pytest.mark.parametrize("nx,ny,nz,p,nu,K", CASES)
 @pytest.mark.parametrize("lam,steps", [(3.5, 4), (2.0, 3)])
-def test_bench_kernel_instantiation_vs_oracle(nx, ny, nz, p, nu, K, lam, steps):
+@pytest.mark.parametrize("tma", [True, False])
+def test_bench_kernel_instantiation_vs_oracle(nx, ny, nz, p, nu, K, lam, steps, tma):
+    """tma: the line staged by bulk copies (relax_xsweep_tma_kernel, the default for even line
+    lengths) or through registers (relax_xsweep_kernel, PDG_NO_TMA)."""
     from paper_1702_00169_b200 import pdg
     h = 1.0 / 256.0
     ncell = (nx, ny, nz)
@@ -64,7 +67,7 @@ def test_bench_kernel_instantiation_vs_oracle(nx, ny, nz, p, nu, K, lam, steps):
     dt = nu * h / lam
     vel, comp = velocity_set(3, 4, lam)
     pb = pdg.make_problem(3, list(ncell), p, 4, vel, comp, lam, FLUX_ISOTHERMAL, [1.0], dt, hi=hi,
-                          flags=pdg.PDG_PROFILE)
+                          flags=pdg.PDG_PROFILE | (0 if tma else pdg.PDG_NO_TMA))
     S = pdg.Solver(pb)
     w0 = _w0(ncell, p, h, seed=nx + 7 * p)
     wd = torch.from_numpy(w0.reshape(-1)).cuda()
