@@ -295,7 +295,7 @@ def run_product(args, cfg):
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
         decomp = {"velocity": pdg.PDG_DECOMP_VELOCITY, "zslab": pdg.PDG_DECOMP_ZSLAB}[args.decomp]
-        flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST)
+        flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST) | (pdg.PDG_NO_TMA if args.no_tma else 0)
         S = pdist.sharded_solver(cfg, device, flags=flags, stream=stream.cuda_stream,
                                  decomposition=decomp, slabs_per_rank=args.slabs_per_rank)
         fill_w0(cfg, S.w, device, S.sizes)
@@ -469,6 +469,8 @@ def main():
     ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
                     help="multi-GPU decomposition (default: zslab when launched on several ranks)")
     ap.add_argument("--slabs-per-rank", type=int, default=1)
+    ap.add_argument("--no-tma", action="store_true",
+                    help="register-staged collision + x-sweep pass instead of bulk-copy staging (PDG_NO_TMA)")
     ap.add_argument("--one-decomp", action="store_true",
                     help="several ranks: time only --decomp (default: also the other decomposition)")
     ap.add_argument("--lattice", default=None, choices=["D2Q9", "D3Q15", "D3Q19", "D3Q27"],
