@@ -73,7 +73,6 @@ struct Geometry {
     int64_t gncell_outer = 0, cell_begin = 0;
     int64_t slab_begin[kMaxSlabs + 1] = {0};  // global cell plane where slab s starts
     size_t carry_doubles = 0;                 // one carry/inflow buffer (doubles)
-    size_t table_doubles = 0;                 // one correction table (doubles)
     // lattice velocity sets (PDG_FLUX_LBM, NEXT-2)
     int async_host = 0;                       // PDG_ASYNC_HOST
     int lattice = 0;                          // 1: general velocities, fb = [nvl][dim][plane_stride]
@@ -393,7 +392,6 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     const int nvo = 2 * p->m;                         // velocities along the outer axis
     g->carry_doubles = (size_t)S * nvo * 2 * (size_t)plane;
     const int64_t lmax = (Nout + S - 1) / S + 1;
-    g->table_doubles = (size_t)(2 * lmax * g->n + 2 * (lmax + 1));
     return PDG_OK;
 }
 
@@ -402,7 +400,7 @@ size_t lat_ints_bytes(const Geometry &g) { return ((g.lat_ints * sizeof(int) + 2
 size_t work_bytes_of(const Geometry &g)
 {
     size_t b = 256;
-    if (g.zslab) b += sizeof(double) * (2 * g.carry_doubles + kMaxTables * g.table_doubles);
+    if (g.zslab) b += sizeof(double) * 2 * g.carry_doubles;  // outgoing carries, exact inflows
     if (g.lattice) b += lat_ints_bytes(g) + sizeof(double) * (g.lat_xbuf + g.lat_ybuf);
     if (g.lattice && g.n == 4 && g.dim == 3) b += sizeof(double) * kMaxLatTables * kLatBigTableDoubles;
     b = ((b + 255) / 256) * 256;
@@ -476,10 +474,10 @@ struct pdg_ctx {
     int sms = 148;
     // z-slab decomposition
     std::vector<pdg::SweepVel> outer_entries;  // per (outer velocity, local slab)
-    double *zcarry = nullptr, *zinflow = nullptr, *ztables = nullptr;
+    double *zcarry = nullptr, *zinflow = nullptr;
     struct ZTable {
         double dtp;
-        int npass, slot, leff;
+        int npass, leff, lpre;     // lpre: cells the carry pre-pass reads (zslab_tables)
         std::vector<double> B, C;  // by slab length
     };
     std::vector<ZTable> ztables_host;
@@ -502,6 +500,7 @@ struct pdg_ctx {
 namespace {
 
 pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass);
+pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out);
 
 // Every entry point taking a context runs on the context's device (the caller's current
 // device may differ) and restores the caller's device on exit.
@@ -622,7 +621,7 @@ bool use_cols(const pdg_ctx *c, const pdg::SweepParams &sp)
     if (sp.nvel == 0 || cols_smem(c->g.n, sp) > 110 * 1024) return false;
     for (int i = 0; i < sp.nvel; ++i) {
         const pdg::SweepVel &V = sp.v[i];
-        if (V.inner % kColsW != 0 || V.cout_off >= 0 || V.ncells != sp.v[0].ncells) return false;
+        if (V.inner % kColsW != 0 || V.cout_off >= 0 || V.cin_off >= 0 || V.ncells != sp.v[0].ncells) return false;
     }
     return true;
 }
@@ -897,21 +896,51 @@ pdg_status transport_pass(pdg_ctx *c, double dtp, int npass, int which = SWEEP_A
     };
     launch(xp, yzp, which);
     const bool outer = c->g.zslab && which != SWEEP_X && !c->outer_entries.empty();
-    if (outer) {
-        // slab sweeps of the outer-axis velocities, in launches of at most kMaxVel entries
-        pdg::SweepParams op = yzp;
-        pdg::SweepParams none = xp;
+    pdg_status s = post_launch(c, "sweep");
+    if (s == PDG_OK && outer) {
+        // z-slab decomposition of the outer-axis velocities: read-only carry pre-pass over the
+        // last lpre cells of every slab, carry exchange + scan, then one exact sweep per slab from
+        // its exact inflows (launches of at most kMaxVel (velocity, slab) entries)
+        const pdg_ctx::ZTable *zt = nullptr;
+        s = ztable(c, dtp, npass, &zt);
+        const size_t ne = c->outer_entries.size();
+        pdg::SweepParams op = yzp, none = xp;
         none.nvel = 0;
         op.cout = c->zcarry;
-        const size_t ne = c->outer_entries.size();
-        for (size_t b0 = 0; b0 < ne; b0 += pdg::kMaxVel) {
+        op.cin = c->zinflow;
+        for (size_t b0 = 0; b0 < ne && s == PDG_OK; b0 += pdg::kMaxVel) {
             op.nvel = (int32_t)std::min<size_t>(pdg::kMaxVel, ne - b0);
-            for (int i = 0; i < op.nvel; ++i) op.v[i] = c->outer_entries[b0 + i];
+            int64_t maxl = 0;
+            double bytes = 0.0;
+            for (int i = 0; i < op.nvel; ++i) {
+                op.v[i] = c->outer_entries[b0 + i];
+                op.v[i].cin_off = -1;
+                maxl = std::max(maxl, op.v[i].nlines);
+                bytes += 8.0 * std::min(zt->lpre, op.v[i].ncells) * n * (double)op.v[i].nlines;
+            }
+            const int e = prof_begin(c);
+            dim3 grid((unsigned)((maxl + 255) / 256), (unsigned)op.nvel);
+            if (n == 2) npass == 1 ? pdg::zslab_carry_kernel<2, 1><<<grid, 256, 0, c->stream>>>(op, zt->lpre)
+                                   : pdg::zslab_carry_kernel<2, 2><<<grid, 256, 0, c->stream>>>(op, zt->lpre);
+            else if (n == 3) npass == 1 ? pdg::zslab_carry_kernel<3, 1><<<grid, 256, 0, c->stream>>>(op, zt->lpre)
+                                        : pdg::zslab_carry_kernel<3, 2><<<grid, 256, 0, c->stream>>>(op, zt->lpre);
+            else npass == 1 ? pdg::zslab_carry_kernel<4, 1><<<grid, 256, 0, c->stream>>>(op, zt->lpre)
+                            : pdg::zslab_carry_kernel<4, 2><<<grid, 256, 0, c->stream>>>(op, zt->lpre);
+            prof_end(c, e, PDG_K_ZSLAB, bytes);
+            s = post_launch(c, "zslab_carry");
+        }
+        if (s == PDG_OK) s = zslab_resolve(c, dtp, npass);
+        for (size_t b0 = 0; b0 < ne && s == PDG_OK; b0 += pdg::kMaxVel) {
+            op.nvel = (int32_t)std::min<size_t>(pdg::kMaxVel, ne - b0);
+            for (int i = 0; i < op.nvel; ++i) {
+                op.v[i] = c->outer_entries[b0 + i];
+                op.v[i].cout_off = -1;
+                op.v[i].zero_inflow = 0;
+            }
             launch(none, op, SWEEP_YZ);
+            s = post_launch(c, "zslab sweep");
         }
     }
-    pdg_status s = post_launch(c, "sweep");
-    if (s == PDG_OK && outer) s = zslab_resolve(c, dtp, npass);
     if (lat)
         for (size_t k = 0; k < c->lat_plans.size(); ++k) PDG_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->lat_join[k], 0));
     return s;
@@ -1387,6 +1416,7 @@ void build_sweep_params(pdg_ctx *c)
         sp->f_elems = (int64_t)g.nvl * g.nnodes;
         sp->fb_elems = (int64_t)g.nvl * g.nplanes * g.plane_stride;
         sp->cout_elems = (int64_t)g.carry_doubles;
+        sp->cin_elems = (int64_t)g.carry_doubles;
     }
     if (g.lattice) {
         // lattice set: single-axis velocities take the line sweeps, diagonal ones the
@@ -1407,6 +1437,7 @@ void build_sweep_params(pdg_ctx *c)
             V.axis = k;
             V.vel = i;
             V.cout_off = -1;
+            V.cin_off = -1;
             V.zero_inflow = 0;
             if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
             else c->yz_params.v[c->yz_params.nvel++] = V;
@@ -1428,6 +1459,7 @@ void build_sweep_params(pdg_ctx *c)
         V.axis = k;
         V.vel = i;
         V.cout_off = -1;
+        V.cin_off = -1;
         V.zero_inflow = 0;
         c->all_params.v[c->all_params.nvel++] = V;
         if (k == 0) c->x_params.v[c->x_params.nvel++] = V;
@@ -1441,7 +1473,8 @@ void build_sweep_params(pdg_ctx *c)
                 E.f_off = (int64_t)j * g.nnodes + lb * g.n * g.stride[k];
                 E.ncells = (int32_t)(g.slab_begin[sl + 1] - g.slab_begin[sl]);
                 E.zero_inflow = (sl == (s ? g.nslab - 1 : 0)) ? 0 : 1;
-                E.cout_off = ((int64_t)sl * (2 * g.m) + jo) * 2 * V.nlines;
+                E.cout_off = ((int64_t)sl * (2 * g.m) + jo) * 2 * V.nlines;  // pre-pass carries (zcarry)
+                E.cin_off = E.zero_inflow ? E.cout_off : -1;                  // exact inflows (zinflow)
                 c->outer_entries.push_back(E);
             }
         } else
@@ -1455,7 +1488,7 @@ void build_sweep_params(pdg_ctx *c)
 // (pass-2 outgoing carry response), computed in long double by running the recurrence on unit
 // inputs.  leff: every later l has |P_l|, |Q_l| < 2^-64.  P, Q: [lmax][n]; B, C: [lmax + 1].
 bool zslab_tables(int p, long double kappa, int npass, int64_t lmax, std::vector<double> &P, std::vector<double> &Q,
-                  std::vector<double> &B, std::vector<double> &C, int *leff_out)
+                  std::vector<double> &B, std::vector<double> &C, int *leff_out, int *lpre_out = nullptr)
 {
     const int n = p + 1;
     long double M[16], gv[4];
@@ -1509,6 +1542,46 @@ bool zslab_tables(int p, long double kappa, int npass, int64_t lmax, std::vector
         C[l + 1] = (double)c2;
     }
     *leff_out = leff;
+    if (lpre_out) {
+        // pre-pass length: the outgoing carries' response to unit data in a cell followed by d
+        // cells; every cell whose response reaches 2^-64 is read (lpre = largest such d + 1)
+        int lpre = 1;
+        for (int b = 0; b < n; ++b) {
+            long double f1[4], f2[4];
+            for (int a = 0; a < n; ++a) {
+                f1[a] = M[a * n + b];
+                f2[a] = 0.0L;
+            }
+            long double e1 = 1.0L * (b == n - 1), cc1 = e1 + f1[n - 1], cc2 = 0.0L;
+            if (npass > 1) {
+                for (int a = 0; a < n; ++a) {
+                    long double acc = 0.0L;
+                    for (int q = 0; q < n; ++q) acc += M[a * n + q] * f1[q];
+                    f2[a] = acc;
+                }
+                cc2 = f1[n - 1] + f2[n - 1];
+            }
+            for (int64_t d = 0; d <= lmax; ++d) {
+                if (fabsl(cc1) >= 0x1p-64L || fabsl(cc2) >= 0x1p-64L) lpre = std::max<int>(lpre, (int)d + 1);
+                // one more cell of zero data downstream
+                long double g1[4], g2[4];
+                for (int a = 0; a < n; ++a) g1[a] = gv[a] * cc1;
+                const long double n1 = g1[n - 1];
+                long double n2 = 0.0L;
+                if (npass > 1) {
+                    for (int a = 0; a < n; ++a) {
+                        long double acc = gv[a] * cc2;
+                        for (int q = 0; q < n; ++q) acc += M[a * n + q] * g1[q];
+                        g2[a] = acc;
+                    }
+                    n2 = g1[n - 1] + g2[n - 1];
+                }
+                cc1 = n1;
+                cc2 = n2;
+            }
+        }
+        *lpre_out = lpre;
+    }
     return true;
 }
 
@@ -1527,16 +1600,10 @@ pdg_status ztable(pdg_ctx *c, double dtp, int npass, const pdg_ctx::ZTable **out
     const long double kappa = (long double)c->prob.lambda * (long double)dtp / (long double)g.h[g.outer];
     std::vector<double> Pt, Qt;
     pdg_ctx::ZTable zt;
-    if (!zslab_tables(g.p, kappa, npass, lmax, Pt, Qt, zt.B, zt.C, &zt.leff))
+    if (!zslab_tables(g.p, kappa, npass, lmax, Pt, Qt, zt.B, zt.C, &zt.leff, &zt.lpre))
         return fail(PDG_E_INVALID_ARGUMENT, "singular cell block");
     zt.dtp = dtp;
     zt.npass = npass;
-    std::vector<double> table(Pt);  // P[lmax][n], then Q[lmax][n] (zslab_correct_kernel)
-    table.insert(table.end(), Qt.begin(), Qt.end());
-    zt.slot = (int)c->ztables_host.size();
-    cudaError_t e = cudaMemcpy(c->ztables + (size_t)zt.slot * g.table_doubles, table.data(),
-                               sizeof(double) * table.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return fail(PDG_E_CUDA, std::string("z-slab table upload: ") + cudaGetErrorString(e));
     c->ztables_host.push_back(zt);
     *out = &c->ztables_host.back();
     return PDG_OK;
@@ -1561,43 +1628,21 @@ pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
     std::memset(&P, 0, sizeof(P));
     P.carry = c->zcarry;
     P.inflow = c->zinflow;
-    P.f = c->f;
-    P.f_elems = (int64_t)g.nvl * g.nnodes;
     P.carry_elems = (int64_t)g.carry_doubles;
-    P.table_elems = (int64_t)g.table_doubles;
-    P.table = c->ztables + (size_t)zt->slot * g.table_doubles;
     P.plane = g.nnodes / g.L[g.outer];
-    P.nnodes = g.nnodes;
-    P.inner = g.stride[g.outer];
     P.nslab = g.nslab;
-    P.slab0 = g.slab0;
-    P.nslab_local = g.nslab_local;
     P.nvo = 2 * g.m;
     P.npass = npass;
-    P.leff = zt->leff;
-    P.lmax = (int)(zt->B.size() - 1);
-    for (int jo = 0; jo < P.nvo; ++jo) {
-        const int comp = jo / 2, sgn = jo % 2;
-        P.vel[jo] = comp * 2 * g.dim + 2 * g.outer + sgn;
-        P.sign[jo] = sgn ? -1 : 1;
-    }
+    for (int jo = 0; jo < P.nvo; ++jo) P.sign[jo] = (jo % 2) ? -1 : 1;
     for (int sl = 0; sl < g.nslab; ++sl) {
         const int len = (int)(g.slab_begin[sl + 1] - g.slab_begin[sl]);
-        P.cells[sl] = len;
-        P.local_begin[sl] = (int)(g.slab_begin[sl] - g.cell_begin);
         P.B[sl] = zt->B[len];
         P.C[sl] = zt->C[len];
     }
     dim3 g1((unsigned)((P.plane + 255) / 256), (unsigned)P.nvo);
     pdg::zslab_scan_kernel<<<g1, 256, 0, c->stream>>>(P);
-    dim3 g2((unsigned)((P.plane + 255) / 256), (unsigned)(P.nvo * g.nslab_local));
-    if (g.n == 2) pdg::zslab_correct_kernel<2><<<g2, 256, 0, c->stream>>>(P);
-    else if (g.n == 3) pdg::zslab_correct_kernel<3><<<g2, 256, 0, c->stream>>>(P);
-    else pdg::zslab_correct_kernel<4><<<g2, 256, 0, c->stream>>>(P);
-    const double corr_bytes = 16.0 * (double)P.nvo * (double)(g.nslab_local) * (double)P.plane *
-                              (double)std::min<int64_t>(zt->leff, P.lmax) * g.n;
-    prof_end(c, e, PDG_K_ZSLAB, corr_bytes + 16.0 * (double)g.carry_doubles);
-    return post_launch(c, "zslab_resolve");
+    prof_end(c, e, PDG_K_ZSLAB, 8.0 * 3.0 * (double)g.carry_doubles);
+    return post_launch(c, "zslab_scan");
 }
 
 bool is_device_pointer(const void *p)
@@ -1690,7 +1735,6 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     if (c->g.zslab) {
         c->zcarry = reinterpret_cast<double *>(static_cast<char *>(work_dev) + 256);
         c->zinflow = c->zcarry + c->g.carry_doubles;
-        c->ztables = c->zinflow + c->g.carry_doubles;
     }
     build_sweep_params(c);
     if (!c->lat_plans.empty()) {

@@ -42,15 +42,18 @@ struct SweepVel {
     int32_t axis;
     int32_t vel;        // global velocity index
     int64_t cout_off;   // >= 0: write the outgoing carry of pass q at cout[cout_off + q*nlines + line]
-    int32_t zero_inflow;  // 1: the line starts inside the domain (z-slab): inflow carry 0, corrected later
+    int32_t zero_inflow;  // 1: the line starts inside the domain (z-slab pre-pass): inflow carry 0
     int32_t pad;
+    int64_t cin_off;    // >= 0: the inflow carry of pass q is cin[cin_off + q*nlines + line] (z-slab:
+                        // the exact slab inflow from the carry scan), else 2 f^b (or 0, zero_inflow)
 };
 
 struct SweepParams {
     double *f;
     const double *fb;
     double *cout;     // outgoing carries of slab sweeps (z-slab decomposition)
-    int64_t f_elems, fb_elems, cout_elems;  // buffer bounds (checked build)
+    const double *cin;  // exact slab inflow carries (z-slab decomposition)
+    int64_t f_elems, fb_elems, cout_elems, cin_elems;  // buffer bounds (checked build)
     DevBlock blk[3];  // per axis (kappa_k = lambda dt' / h_k)
     int32_t nvel;
     SweepVel v[kMaxVel];
@@ -163,11 +166,20 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
     for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
 
     double carry[NPASS];
-    // ghost cell: f^b old + f^b new (reading C5); a slab interior start has zero inflow
-    if (!V.zero_inflow) PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided fb");
-    const double s0 = V.zero_inflow ? 0.0 : 2.0 * P.fb[V.fb_off + line];
+    if (V.cin_off >= 0) {
+        // a z-slab that does not touch the inflow boundary: the exact inflows from the carry scan
 #pragma unroll
-    for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+        for (int q = 0; q < NPASS; ++q) {
+            PDG_CHECK_IDX(V.cin_off + q * V.nlines + line, P.cin_elems, "sweep_strided cin");
+            carry[q] = P.cin[V.cin_off + q * V.nlines + line];
+        }
+    } else {
+        // ghost cell: f^b old + f^b new (reading C5)
+        PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided fb");
+        const double s0 = 2.0 * P.fb[V.fb_off + line];
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+    }
 
     // ring of PF prefetched cells (values in flow order)
     double ring[PF][N];
@@ -244,7 +256,8 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
     if (active) {
         PDG_CHECK_IDX(p_at, P.f_elems, "sweep_strided_seg f");
         PDG_CHECK_IDX(p_at + (Lk - 1) * step, P.f_elems, "sweep_strided_seg f");
-        if (!V.zero_inflow) PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided_seg fb");
+        if (V.cin_off < 0) PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "sweep_strided_seg fb");
+        else PDG_CHECK_IDX(V.cin_off + (NPASS - 1) * V.nlines + line, P.cin_elems, "sweep_strided_seg cin");
     }
     const int ks = (V.ncells + nseg - 1) / nseg;
     const int c0 = min(V.ncells, sg * ks), c1 = min(V.ncells, c0 + ks);
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
 #pragma unroll
     for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
     const double beta = g[N - 1];
-    const double s0 = (active && !V.zero_inflow) ? 2.0 * P.fb[V.fb_off + line] : 0.0;  // ghost: f^b old + new
+    const double s0 = (active && V.cin_off < 0) ? 2.0 * P.fb[V.fb_off + line] : 0.0;  // ghost: f^b old + new
 
 #pragma unroll
     for (int q = 0; q < NPASS; ++q) {
@@ -275,7 +288,8 @@ __global__ void __launch_bounds__(1024) sweep_strided_seg_kernel(const SweepPara
         sA[sg][lane] = A;
         sB[sg][lane] = B;
         __syncthreads();
-        double s = s0;
+        // inflow of pass q: the ghost, or the exact z-slab inflow of the carry scan
+        double s = (active && V.cin_off >= 0) ? P.cin[V.cin_off + q * V.nlines + line] : s0;
         for (int j = 0; j < sg; ++j) s = fma(sB[j][lane], s, sA[j][lane]);
         if (active) {
             for (int c = c0; c < c1; ++c) {
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(256) sweep_cols_kernel(const SweepParams P)
     for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
     for (int cc = warp; cc < CW; cc += nwarps) {
         PDG_CHECK_IDX(V.fb_off + line0 + cc, P.fb_elems, "sweep_cols fb");
-        const double s0 = V.zero_inflow ? 0.0 : 2.0 * P.fb[V.fb_off + line0 + cc];  // ghost: f^b old + new
+        const double s0 = 2.0 * P.fb[V.fb_off + line0 + cc];  // ghost: f^b old + new (no z-slab entries here)
         warp_line_sweep<N, NPASS, K>(scol + cc * Lp, V.ncells, V.sign > 0, M, g, s0, lane);
     }
     __syncthreads();
@@ -916,31 +930,22 @@ __global__ void __launch_bounds__(256) check_state_kernel(const double *__restri
 }
 
 // ---------------------------------------------------------------------------
-// Z-slab decomposition: along the outer axis every slab is swept with zero
-// inflow (except the slab where the velocity enters the domain) and writes its outgoing
-// carries A_q (pass q).  The carry recurrence is affine, so the exact inflows follow from
-// the slabs upstream: with B = beta^len and C = the pass-2 carry response to a unit
-// pass-1 inflow (host tables),
+// Z-slab decomposition: along the outer axis the zero-inflow outgoing carries
+// A_q (pass q) of every slab come from a read-only pre-pass (zslab_carry_kernel; the entry slab
+// of a velocity starts from its true inflow).  The carry recurrence is affine, so the exact
+// inflows follow from the slabs upstream: with B = beta^len and C = the pass-2 carry response
+// to a unit pass-1 inflow (host tables),
 //   S1(next) = A1 + B S1,   S2(next) = A2 + C S1 + B S2.
-// The slab's values are then corrected cell by cell: f_l += P_l S1 + Q_l S2 (two passes) or
-// f_l += Q_l S1 (one pass), Q_l = g beta^l, P_l = pass-2 response (host tables, truncated
-// where |P_l|, |Q_l| < 2^-64).
+// Each slab is then swept once from its exact inflows (SweepVel::cin_off): no correction pass.
 // ---------------------------------------------------------------------------
 struct ZSlabParams {
-    const double *carry;   // [slab][vel][2][plane] outgoing carries of the slab sweeps
+    const double *carry;   // [slab][vel][2][plane] zero-inflow outgoing carries (pre-pass, all-gathered)
     double *inflow;        // [slab][vel][2][plane] exact inflows (output of the scan)
-    double *f;
-    int64_t f_elems, carry_elems, table_elems;  // buffer bounds (checked build; inflow has carry_elems)
-    const double *table;   // P[lmax][n], Q[lmax][n]
+    int64_t carry_elems;   // buffer bound (checked build; inflow has as many)
     double B[64], C[64];   // per global slab: beta^len, pass-2 carry response
     int64_t plane;         // lines per slab
-    int64_t nnodes;        // local nodes per velocity
-    int64_t inner;         // stride of the outer axis
-    int32_t nslab, slab0, nslab_local, nvo, npass, leff, lmax;
-    int32_t vel[16];       // global velocity index of outer velocity j
+    int32_t nslab, nvo, npass;
     int32_t sign[16];
-    int32_t cells[64];     // cells of global slab s
-    int32_t local_begin[64];  // first local cell plane of global slab s (valid for local slabs)
 };
 
 __global__ void __launch_bounds__(256) zslab_scan_kernel(const ZSlabParams P)
@@ -967,38 +972,61 @@ __global__ void __launch_bounds__(256) zslab_scan_kernel(const ZSlabParams P)
     }
 }
 
-template <int N>
-__global__ void __launch_bounds__(256) zslab_correct_kernel(const ZSlabParams P)
+// Z-slab carry pre-pass (read-only): the zero-inflow outgoing carries A_q of every slab
+// line, from the slab's last `lpre` cells only (flow order; data further upstream changes the
+// outgoing carries by less than 2^-64 of its size, reading C26).  A slab with fewer cells is
+// walked whole, from its true inflow if it is the entry slab.  Writes cout[cout_off + q nlines +
+// line]; the exact slab sweeps run after the carry scan with the exact inflows (cin).
+template <int N, int NPASS>
+__global__ void __launch_bounds__(256) zslab_carry_kernel(const SweepParams P, int lpre)
 {
-    const int j = blockIdx.y % P.nvo;
-    const int t = blockIdx.y / P.nvo;  // local slab
-    const int s = P.slab0 + t;
-    const bool up = P.sign[j] > 0;
-    if (s == (up ? 0 : P.nslab - 1)) return;  // the entry slab saw the true inflow
+    const SweepVel V = P.v[blockIdx.y];
     const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (line >= P.plane) return;
-    const int64_t vstride = 2 * P.plane;
-    const int64_t o = s * (int64_t)P.nvo * vstride + j * vstride + line;
-    const double S1 = P.inflow[o];
-    const double S2 = (P.npass > 1) ? P.inflow[o + P.plane] : 0.0;
-    const int ncell = P.cells[s];
-    const int lend = min(ncell, P.leff);
-    double *col = P.f + (int64_t)P.vel[j] * P.nnodes + line;  // the outer axis is the slowest: base = line
-    PDG_CHECK_IDX(o + P.plane, P.carry_elems, "zslab_correct inflow");
-    PDG_CHECK_IDX((int64_t)(lend > 0 ? lend : 1) * N - 1 + P.lmax * N, P.table_elems, "zslab_correct table");
-    const double *Pt = P.table;
-    const double *Qt = P.table + (int64_t)P.lmax * N;
-    for (int l = 0; l < lend; ++l) {
-        const int cell = P.local_begin[s] + (up ? l : ncell - 1 - l);
+    if (line >= V.nlines) return;
+    const int64_t Lk = (int64_t)V.ncells * N;
+    const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);
+    const int64_t step = (V.sign > 0) ? V.inner : -V.inner;
+    const int64_t p_at = V.f_off + base + ((V.sign > 0) ? 0 : (Lk - 1) * V.inner);
+    const double *p = P.f + p_at;
+    PDG_CHECK_IDX(p_at, P.f_elems, "zslab_carry f");
+    PDG_CHECK_IDX(p_at + (Lk - 1) * step, P.f_elems, "zslab_carry f");
+    double M[N * N], g[N];
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-            const int am = up ? a : N - 1 - a;
-            double *ptr = col + ((int64_t)cell * N + am) * P.inner;
-            PDG_CHECK_IDX(ptr - P.f, P.f_elems, "zslab_correct f");
-            double corr = Qt[l * N + a] * ((P.npass > 1) ? S2 : S1);
-            if (P.npass > 1) corr = fma(Pt[l * N + a], S1, corr);
-            *ptr += corr;
+    for (int i = 0; i < N * N; ++i) M[i] = P.blk[V.axis].M[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = P.blk[V.axis].g[i];
+    const int c0 = max(0, V.ncells - lpre);
+    double s0 = 0.0;
+    if (c0 == 0 && !V.zero_inflow) {
+        PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "zslab_carry fb");
+        s0 = 2.0 * P.fb[V.fb_off + line];
+    }
+    double carry[NPASS];
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) carry[q] = s0;
+    for (int c = c0; c < V.ncells; ++c) {
+        double fo[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) fo[a] = __ldcs(p + ((int64_t)c * N + a) * step);
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) {
+            double fn[N];
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+                double acc = g[a] * carry[q];
+#pragma unroll
+                for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
+                fn[a] = acc;
+            }
+            carry[q] = fo[N - 1] + fn[N - 1];
+#pragma unroll
+            for (int a = 0; a < N; ++a) fo[a] = fn[a];
         }
+    }
+#pragma unroll
+    for (int q = 0; q < NPASS; ++q) {
+        PDG_CHECK_IDX(V.cout_off + q * V.nlines + line, P.cout_elems, "zslab_carry cout");
+        P.cout[V.cout_off + q * V.nlines + line] = carry[q];
     }
 }
 

@@ -508,14 +508,16 @@ def test_nccl_pipelined_sharded_collision_chunks():
     S.destroy()
 
 
-@pytest.mark.parametrize("dim,ncell,p,flux,fparams,m", [
-    (2, (16, 16), 2, 1, (1.4,), 4),       # 2-D Euler: 48-node lines tile by 16
-    (2, (32, 32), 2, 1, (1.4,), 4),
-    (2, (20, 20), 3, 1, (1.4,), 4),       # p = 3: 80-node lines
-    (2, (40, 24), 1, 2, (1.0,), 3),       # p = 1, anisotropic
-    (3, (4, 30, 30), 3, 2, (1.0,), 4),    # 3-D with few strided lines: y and z tiles
+@pytest.mark.parametrize("dim,ncell,p,flux,fparams,m,nu", [
+    (2, (16, 16), 2, 1, (1.4,), 4, 2.0),       # 2-D Euler: 48-node lines tile by 16
+    (2, (32, 32), 2, 1, (1.4,), 4, 2.0),
+    (2, (20, 20), 3, 1, (1.4,), 4, 2.0),       # p = 3: 80-node lines
+    (2, (40, 24), 1, 2, (1.0,), 3, 2.0),       # p = 1, anisotropic
+    # 3-D with few strided lines: y and z tiles.  nu = 0.6: at nu = 2 this random state amplifies a
+    # one-ulp perturbation to 2.7e-11 in three steps in the oracle itself (3.0e-14 at nu = 0.6)
+    (3, (4, 30, 30), 3, 2, (1.0,), 4, 0.6),
 ])
-def test_strided_tile_kernel_parity(dim, ncell, p, flux, fparams, m):
+def test_strided_tile_kernel_parity(dim, ncell, p, flux, fparams, m, nu):
     """sweep_cols_kernel (grids with few strided lines: tiles of 16 adjacent lines staged in shared
     memory, warp-scan sweeps; the config-2 y-velocity path) inside free-running M2 steps (fused
     two-sweep passes and single passes) against the oracle."""
@@ -525,7 +527,7 @@ def test_strided_tile_kernel_parity(dim, ncell, p, flux, fparams, m):
     vel, comp = velocity_set(dim, m, lam)
     h = 1.0 / ncell[0]
     hi = tuple(ncell[d] * h for d in range(dim)) + (1.0,) * (3 - dim)
-    dt = 2.0 * h / lam
+    dt = nu * h / lam
     pb = pdg.make_problem(dim, list(ncell), p, m, vel, comp, lam, flux, list(fparams), dt, hi=hi)
     ob = O.Problem(dim, list(ncell), p, vel, comp, m, lam, flux, list(fparams), dt, hi=list(hi))
     S = pdg.Solver(pb)
