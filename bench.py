@@ -243,6 +243,35 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def oracle_config_timing(key, steps):
+    """One child process: `steps` oracle M2 steps of BASELINE config `key` at full size."""
+    from pdg_inputs import CONFIGS
+    cfg = CONFIGS[key]
+    sub, pb, fc, fbc, _ = oracle_prepare(cfg, cfg.N)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle_step(pb, fc, fbc)
+    dt = time.perf_counter() - t0
+    return {"config": cfg.name, "steps": steps, "seconds": dt, "updates_per_s": cfg.updates_per_step * steps / dt}
+
+
+def run_oracle_table(args):
+    """the oracle on configs 1-3 at full size, single-thread and on all host cores
+    (each in a child process with OMP_NUM_THREADS set), one JSON line."""
+    model, ram = host_info()
+    rows = []
+    for key, steps in ((1, 100), (2, 2), (3, 1)):
+        for threads in (1, os.cpu_count()):
+            code = ("import sys, json; sys.path.insert(0, %r); import bench; "
+                    "print(json.dumps(bench.oracle_config_timing(%d, %d)))") % (ROOT, key, steps)
+            env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+            out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=1800)
+            r = json.loads(out.stdout.strip().splitlines()[-1])
+            r["threads"] = threads
+            rows.append(r)
+    print(json.dumps({"oracle_table": rows, "cpu_model": model, "ram_gb": ram, "cores": os.cpu_count()}), flush=True)
+
+
 def config_block(cfg, G, decomp="velocity", spr=1):
     return {"workload": cfg.name, "dim": cfg.dim, "cells_per_axis": cfg.N, "degree": cfg.p, "m": cfg.m,
             "nv": cfg.nv, "lambda": cfg.lam, "dt": cfg.dt, "nodes": cfg.nnodes,
@@ -469,6 +498,8 @@ def main():
     ap.add_argument("--decomp", default=None, choices=["velocity", "zslab"],
                     help="multi-GPU decomposition (default: zslab when launched on several ranks)")
     ap.add_argument("--slabs-per-rank", type=int, default=1)
+    ap.add_argument("--oracle-table", action="store_true",
+                    help="time the CPU oracle on configs 1-3 at full size (1 thread and all cores) and exit")
     ap.add_argument("--no-tma", action="store_true",
                     help="register-staged collision + x-sweep pass instead of bulk-copy staging (PDG_NO_TMA)")
     ap.add_argument("--one-decomp", action="store_true",
@@ -487,7 +518,9 @@ def main():
         args.ref_cells = min(args.ref_cells, 16 if cfg.dim == 3 else 128)
     if args.decomp is None:  # the z-slab decomposition is implemented for axis-aligned sets only
         args.decomp = "zslab" if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not args.lattice else "velocity"
-    if args.impl == "reference":
+    if args.oracle_table:
+        run_oracle_table(args)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_product(args, cfg)
