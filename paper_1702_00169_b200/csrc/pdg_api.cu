@@ -604,7 +604,7 @@ int strided_segments(const pdg_ctx *c, const pdg::SweepParams &sp)
 // Lines per tile of sweep_cols_kernel, and whether a strided batch can use it: every velocity's
 // lines tile by kColsW (inner % kColsW == 0), no outgoing carries (z-slab entries), and a tile of
 // rows fits the shared memory of two CTAs per SM.
-constexpr int kColsW = 16;
+constexpr int kColsW = 8;
 
 int cols_K(int ncells) { return ncells <= 64 ? 2 : (ncells <= 128 ? 4 : 8); }
 
@@ -968,7 +968,11 @@ size_t relax_x_tma_smem(const pdg_ctx *c) { return relax_x_smem(c) + sizeof(doub
 
 bool use_relax_x_tma(const pdg_ctx *c)
 {
-    return !(c->prob.flags & PDG_NO_TMA) && (c->g.L[0] % 2 == 0) && relax_x_tma_smem(c) <= 200 * 1024;
+    // only where two or more CTAs fit an SM: with one CTA per SM (configs 2, 4, 5: raw lines of
+    // 98-147 KB) the next line's load cannot hide behind enough work and the register-staged
+    // kernel measured faster (config 5: 0.888 against 0.959 of HBM; config 3, 51 KB per CTA:
+    // 0.940 against 0.814; profiles/r02_bench_*)
+    return !(c->prob.flags & PDG_NO_TMA) && (c->g.L[0] % 2 == 0) && relax_x_tma_smem(c) <= 110 * 1024;
 }
 
 template <int DIM, int MODEL, int N, int NPASS, int K>

@@ -442,10 +442,13 @@ __global__ void __launch_bounds__(256) sweep_cols_kernel(const SweepParams P)
     const int64_t base = V.f_off + (line0 / V.inner) * (V.inner * Lk) + (line0 % V.inner);
     double *g0 = P.f + base;  // node y of tile line c at g0 + y * inner + c
     PDG_CHECK_IDX(base + (int64_t)(Lk - 1) * V.inner + CW - 1, P.f_elems, "sweep_cols f");
+    // every load of the tile in flight at once (LDGSTS: no register staging, no per-load wait)
     for (int t = threadIdx.x; t < Lk * CW; t += blockDim.x) {
         const int y = t / CW, cc = t - y * CW;
-        scol[cc * Lp + y + y / SEG] = __ldcs(g0 + (int64_t)y * V.inner + cc);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(scol + cc * Lp + y + y / SEG);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g0 + (int64_t)y * V.inner + cc) : "memory");
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     double M[N * N], g[N];

@@ -518,7 +518,7 @@ def test_nccl_pipelined_sharded_collision_chunks():
     (3, (4, 30, 30), 3, 2, (1.0,), 4, 0.6),
 ])
 def test_strided_tile_kernel_parity(dim, ncell, p, flux, fparams, m, nu):
-    """sweep_cols_kernel (grids with few strided lines: tiles of 16 adjacent lines staged in shared
+    """sweep_cols_kernel (grids with few strided lines: tiles of 8 adjacent lines staged in shared
     memory, warp-scan sweeps; the config-2 y-velocity path) inside free-running M2 steps (fused
     two-sweep passes and single passes) against the oracle."""
     from paper_1702_00169_b200 import pdg

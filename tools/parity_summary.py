@@ -24,8 +24,11 @@ def main(d=os.path.join(ROOT, "profiles", "r02_parity")):
         rs = [e["resync_f"] for e in ps if "resync_f" in e and e.get("oracle_nonphysical_in", 0) == 0]
         rs_bad = [e["step"] for e in ps if "resync_f" in e and e.get("oracle_nonphysical_in", 0) > 0]
         free = [e["free_f"] for e in ps if "free_f" in e]
-        twin = [e.get("gpu_twin_amplification") for e in ps if "gpu_twin_amplification" in e]
-        otw = [e.get("oracle_twin_amplification") for e in ps if "oracle_twin_amplification" in e]
+        # amplification of a 1e-13 twin perturbation up to the last step whose state is physical
+        phys = [e for e in ps if e.get("nonphysical_gpu", 0) == 0 and e.get("nonfinite_oracle", 0) == 0]
+        twin = [e.get("gpu_twin_amplification") for e in phys if "gpu_twin_amplification" in e]
+        otw = [e.get("oracle_twin_amplification") for e in phys if "oracle_twin_amplification" in e]
+        last_phys = phys[-1]["step"] if phys else None
         first_bad = next((e["step"] for e in ps if e.get("nonphysical_gpu", 0) > 0), None)
         last = ps[-1]
         rows.append([name, r["N"], r["p"], r["lambda"], r["steps"], len(rs), fmt(max(rs) if rs else None),
@@ -33,12 +36,12 @@ def main(d=os.path.join(ROOT, "profiles", "r02_parity")):
                      fmt(free[-1] if free else None), fmt(r.get("fused_free_f")),
                      r.get("last_step_finite_and_agree_1e-12"),
                      fmt(twin[-1] if twin else r.get("gpu_twin_amplification_final")),
-                     fmt(otw[-1] if otw else None), fmt(first_bad), r.get("stopped_at_step") or "—",
+                     fmt(otw[-1] if otw else None), fmt(last_phys if twin else None), fmt(first_bad), r.get("stopped_at_step") or "—",
                      f"{r['oracle_seconds'] / 60:.1f}"])
     hdr = ["case", "N", "p", "λ", "steps", "re-synced steps (physical input)", "max re-synced rel err f",
            "re-synced steps with non-physical input", "free-running rel err f (last step, lockstep)",
            "one pdg_step(steps) call rel err f", "last step free-running <= 1e-12",
-           "GPU twin amplification (last)", "oracle twin amplification (last)", "first non-physical step",
+           "GPU twin amplification", "oracle twin amplification", "at step (last physical)", "first non-physical step",
            "oracle stopped (non-finite)", "oracle min"]
     out = ["| " + " | ".join(hdr) + " |", "|" + "---|" * len(hdr)]
     out += ["| " + " | ".join(str(c) for c in r) + " |" for r in rows]
