@@ -325,8 +325,13 @@ def run_product(args, cfg):
     with torch.cuda.stream(stream):
         decomp = {"velocity": pdg.PDG_DECOMP_VELOCITY, "zslab": pdg.PDG_DECOMP_ZSLAB}[args.decomp]
         flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST) | (pdg.PDG_NO_TMA if args.no_tma else 0)
+        plan = {}
+        if args.lattice_cta:
+            plan["lattice_cta"] = tuple(int(x) for x in args.lattice_cta.split(","))
+        if args.lattice_segment:
+            plan["lattice_segment"] = args.lattice_segment
         S = pdist.sharded_solver(cfg, device, flags=flags, stream=stream.cuda_stream,
-                                 decomposition=decomp, slabs_per_rank=args.slabs_per_rank)
+                                 decomposition=decomp, slabs_per_rank=args.slabs_per_rank, **plan)
         fill_w0(cfg, S.w, device, S.sizes)
         S.set_equilibrium(S.w)
         S.step(args.warmup)
@@ -507,6 +512,9 @@ def main():
     ap.add_argument("--lattice", default=None, choices=["D2Q9", "D3Q15", "D3Q19", "D3Q27"],
                     help="NEXT-2 workload: isothermal LBM on this lattice (replaces --config)")
     ap.add_argument("--cells", type=int, default=128, help="cells per axis of the --lattice workload")
+    ap.add_argument("--lattice-cta", default=None, help="forced lattice CTA shape 'wx,wy' (pdg_problem.lattice_cta)")
+    ap.add_argument("--lattice-segment", type=int, default=0,
+                    help="forced lattice chain-segment rows (pdg_problem.lattice_segment; < 0: none)")
     ap.add_argument("--degree", type=int, default=2, help="degree p of the --lattice workload")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "product":

@@ -548,13 +548,12 @@ void prof_end(pdg_ctx *c, int i, int kind, double bytes, cudaStream_t st = nullp
     c->prof.recs.push_back({kind, i, bytes});
 }
 
-int grid_for(int64_t work, int threads)
+// grid of a grid-stride kernel: one thread per work item up to 8 resident 256-thread CTAs per SM
+// of the context's device, grid-stride beyond
+int grid_for(const pdg_ctx *c, int64_t work, int threads)
 {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = (work + threads - 1) / threads;
-    const int64_t cap = (int64_t)sms * 8;  // 8 resident 256-thread CTAs per SM, grid-stride beyond
+    const int64_t cap = (int64_t)c->sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return (int)blocks;
@@ -1046,7 +1045,7 @@ void launch_relax_x_t(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem, int n
 template <int DIM, int MODEL>
 void launch_relax_t(pdg_ctx *c, double ca, double cb)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const int grid = grid_for(c, c->g.nnodes, 256);
     const int e = prof_begin(c);
     pdg::relax_kernel<DIM, MODEL><<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->mp, ca, cb);
     prof_end(c, e, PDG_K_RELAX, 16.0 * (double)c->g.nvl * (double)c->g.nnodes);
@@ -1056,7 +1055,7 @@ void launch_relax_t(pdg_ctx *c, double ca, double cb)
 template <int DIM, int MODEL>
 void launch_partial_t(pdg_ctx *c, int64_t x0, int64_t cnt)
 {
-    const int grid = grid_for(cnt, 256);
+    const int grid = grid_for(c, cnt, 256);
     const int e = prof_begin(c);
     pdg::partial_moments_kernel<DIM, MODEL>
         <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl);
@@ -1066,7 +1065,7 @@ void launch_partial_t(pdg_ctx *c, int64_t x0, int64_t cnt)
 template <int DIM, int MODEL>
 void launch_relax_from_w_t(pdg_ctx *c, int64_t x0, int64_t cnt, double ca, double cb)
 {
-    const int grid = grid_for(cnt, 256);
+    const int grid = grid_for(c, cnt, 256);
     const int e = prof_begin(c);
     pdg::relax_from_w_kernel<DIM, MODEL>
         <<<grid, 256, 0, c->stream>>>(c->f + x0, c->w + x0, c->g.nnodes, cnt, c->g.v0, c->g.nvl, c->mp, ca, cb);
@@ -1076,7 +1075,7 @@ void launch_relax_from_w_t(pdg_ctx *c, int64_t x0, int64_t cnt, double ca, doubl
 template <int DIM, int MODEL>
 void launch_equilibrium_t(pdg_ctx *c, const double *w, const double *wb)
 {
-    const int grid = grid_for(c->g.nnodes, 256);
+    const int grid = grid_for(c, c->g.nnodes, 256);
     pdg::equilibrium_kernel<DIM, MODEL><<<grid, 256, 0, c->stream>>>(c->f, w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp);
     int64_t maxl = 0;
     for (int i = 0; i < c->all_params.nvel; ++i) maxl = std::max(maxl, c->all_params.v[i].nlines);
@@ -1906,7 +1905,7 @@ pdg_status pdg_set_equilibrium(pdg_ctx *c, const double *w, const double *wb, in
         if (s != PDG_OK) return s;
         if (wb) {
             PDG_CUDA_TRY(cudaMemcpyAsync(c->w, w, wbytes, cudaMemcpyHostToDevice, c->stream));
-            const int grid = grid_for(c->g.nnodes, 256);
+            const int grid = grid_for(c, c->g.nnodes, 256);
             const int dim = c->g.dim, mod = c->prob.flux;
 #define PDG_EQ_ONLY(D, MO) pdg::equilibrium_kernel<D, MO><<<grid, 256, 0, c->stream>>>(c->f, c->w, c->g.nnodes, c->g.v0, c->g.nvl, c->mp)
             if (dim == 2 && mod == 0) PDG_EQ_ONLY(2, pdg::MODEL_ADV);
@@ -2043,7 +2042,7 @@ pdg_status pdg_check_state(pdg_ctx *c, int64_t *n_bad)
     DeviceGuard dg(c);
     if (!c || !n_bad) return fail(PDG_E_INVALID_ARGUMENT, "NULL argument");
     PDG_CUDA_TRY(cudaMemsetAsync(c->counter, 0, sizeof(unsigned long long), c->stream));
-    const int grid = grid_for(c->g.nnodes, 256);
+    const int grid = grid_for(c, c->g.nnodes, 256);
     const int check_rho = (c->prob.flux != PDG_FLUX_LINEAR_ADVECTION && !sharded(c)) ? 1 : 0;
     const int nrho = c->g.lattice ? c->g.nv : 2 * c->g.dim;  // velocities whose sum is rho
     pdg::check_state_kernel<<<grid, 256, 0, c->stream>>>(c->f, c->g.nnodes, c->g.v0, c->g.nvl, nrho, check_rho,

@@ -56,7 +56,7 @@ def sum_over_ranks(value: float, device=None, group=None) -> float:
 
 
 def sharded_solver(cfg, device, flags=0, stream=None, tau=0.0, scheme=pdg.PDG_SCHEME_M2,
-                   decomposition=pdg.PDG_DECOMP_VELOCITY, slabs_per_rank=1):
+                   decomposition=pdg.PDG_DECOMP_VELOCITY, slabs_per_rank=1, **plan):
     """A libpdg context for this rank's share (velocity block or z-slab), with its NCCL communicator."""
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
@@ -65,5 +65,5 @@ def sharded_solver(cfg, device, flags=0, stream=None, tau=0.0, scheme=pdg.PDG_SC
     nccl_id = bootstrap_nccl_id(device=device) if dist.is_initialized() and world > 1 else None
     pb = pdg.problem_from_config(cfg, tau=tau, scheme=scheme, rank=rank, nranks=world, nccl_id=nccl_id,
                                  flags=flags, stream=stream, decomposition=decomposition,
-                                 slabs_per_rank=slabs_per_rank)
+                                 slabs_per_rank=slabs_per_rank, **plan)
     return pdg.Solver(pb, device=device)
