@@ -14,3 +14,7 @@ timeout 300 python bench.py --config 2 --steps 20 --warmup 5 --no-e2e --no-cpu-b
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"relax_xsweep|sweep_cols" -s 6 -c 2 \
     -o gpurun_out/r2f_ncu_cfg2 python bench.py --config 2 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/r2f_ncu_cfg2.log 2>&1
 echo "ncu rc=$?"
+for L in D3Q15 D3Q19 D3Q27; do
+  timeout 600 python bench.py --lattice $L --cells 128 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2f_lat_$L.json 2>&1
+done
+timeout 600 python bench.py --lattice D2Q9 --cells 1024 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2f_lat_D2Q9.json 2>&1
