@@ -8,6 +8,18 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def ranges(xs):
+    """[86, 87, 88, 90] -> '86-88, 90'"""
+    out, i = [], 0
+    while i < len(xs):
+        j = i
+        while j + 1 < len(xs) and xs[j + 1] == xs[j] + 1:
+            j += 1
+        out.append(str(xs[i]) if i == j else f"{xs[i]}–{xs[j]}")
+        i = j + 1
+    return ", ".join(out) or "—"
+
+
 def fmt(x):
     return "—" if x is None else (f"{x:.1e}" if isinstance(x, float) else str(x))
 
@@ -32,11 +44,12 @@ def main(d=os.path.join(ROOT, "profiles", "r02_parity")):
         first_bad = next((e["step"] for e in ps if e.get("nonphysical_gpu", 0) > 0), None)
         last = ps[-1]
         rows.append([name, r["N"], r["p"], r["lambda"], r["steps"], len(rs), fmt(max(rs) if rs else None),
-                     ",".join(map(str, rs_bad)) or "—",
+                     ranges(rs_bad),
                      fmt(free[-1] if free else None), fmt(r.get("fused_free_f")),
-                     r.get("last_step_finite_and_agree_1e-12"),
+                     (r.get("last_step_finite_and_agree_1e-12") if free else
+                      (r["steps"] if (r.get("fused_free_f") or 1.0) <= 1e-12 else None)),
                      fmt(twin[-1] if twin else r.get("gpu_twin_amplification_final")),
-                     fmt(otw[-1] if otw else None), fmt(last_phys if twin else None), fmt(first_bad), r.get("stopped_at_step") or "—",
+                     fmt(otw[-1] if otw else None), fmt(last_phys if twin else r["steps"]), fmt(first_bad), r.get("stopped_at_step") or "—",
                      f"{r['oracle_seconds'] / 60:.1f}"])
     hdr = ["case", "N", "p", "λ", "steps", "re-synced steps (physical input)", "max re-synced rel err f",
            "re-synced steps with non-physical input", "free-running rel err f (last step, lockstep)",
