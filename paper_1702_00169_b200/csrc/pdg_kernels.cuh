@@ -430,7 +430,7 @@ __host__ __device__ constexpr int cols_row_len(int ncells)
 }
 
 template <int N, int NPASS, int K, int CW>
-__global__ void __launch_bounds__(256, 3) sweep_cols_kernel(const SweepParams P)
+__global__ void __launch_bounds__(256) sweep_cols_kernel(const SweepParams P)
 {
     extern __shared__ double scol[];
     const SweepVel V = P.v[blockIdx.y];
@@ -495,10 +495,8 @@ __host__ __device__ constexpr int relax_x_row_len(int ncx)
     return ncx * N + (ncx * N) / (K * N) + 1;
 }
 
-// 2-D grids (config 2: f of 75 MB, half of it served from L2) are latency-bound: three CTAs per SM
-// there; the 3-D configs keep the uncapped registers (a cap spilled and measured slower, §7)
 template <int DIM, int MODEL, int N, int NPASS, int K>
-__global__ void __launch_bounds__(256, DIM == 2 ? 3 : 1) relax_xsweep_kernel(const RelaxXParams P)
+__global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
 {
     using Md = Model<DIM, MODEL>;
     constexpr int M = Md::M;
