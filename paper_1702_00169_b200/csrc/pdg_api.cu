@@ -115,9 +115,7 @@ void plan_lattice(const Geometry &g, LatPlan &P)
         // 128^3 12.32 -> 11.82 ms per step against 4 x 2; tools/gpu/bdshape.sh.  2-D diagonals:
         // 4 x-warps, 2-3 % faster than 8 with the chain segments; tools/gpu/wsweep.sh)
         P.Wx = std::min(PIPE ? 2 : (D == 2 ? 4 : 8), (P.nlane + 31) / 32);
-        // p = 2 body diagonals: 10 warps per CTA (2 x 5; 204 registers, no row prefetch, 194 KB)
-        const int wmax = (PIPE && P.d == 3 && g.n == 3) ? 10 : 8;
-        P.Wy = std::max(1, std::min(wmax / P.Wx, P.nw));
+        P.Wy = std::max(1, std::min(8 / P.Wx, P.nw));
     } else {
         // lanes over independent x nodes: spend the warps on the pipe axis (y hand-over in smem)
         P.Wy = std::max(1, std::min(8, P.nw));

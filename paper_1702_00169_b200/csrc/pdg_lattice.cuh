@@ -182,7 +182,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b)
 // the p = 3 body diagonals, whose 64-node rows would leave room for only two warps per SM.
 template <int D, int N = 0, int DA = 0>
 struct LatRing {
-    static constexpr int PFA = (D == 2) ? 3 : (DA == 3 ? 0 : 1);
+    static constexpr int PFA = (D == 2) ? 3 : ((N == 4 && DA == 3) ? 0 : 1);
     static constexpr int RING = PFA + 1;  // row buffers per warp
 };
 
@@ -347,7 +347,7 @@ __device__ __forceinline__ void ll_take(uint64_t *slot, double (&v)[MF], uint32_
 // dropped in round 1: two sweeps per launch, thread-block clusters along the pipe
 // axis, the tensor path for the two-axis classes.)
 template <int D, int N, int ACT>
-__global__ void __launch_bounds__((LatShape<D, ACT>::DA == 3 && N == 3) ? 320 : 256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
+__global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
     lattice_sweep_kernel(const __grid_constant__ LatParams<D, N, ACT> P)
 {
     using S = LatShape<D, ACT>;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__((LatShape<D, ACT>::DA == 3 && N == 3) ? 320 : 
     // x hand-over slots between the x-warps of a CTA: a ring of XR rows; with the point-to-point
     // sync of the pipe classes a producer may run XR - 1 rows ahead of its x consumer
     constexpr int XR = PIPE ? 4 : 2;
-    __shared__ double xs[XR][16][XA ? MF : 1];
+    __shared__ double xs[XR][8][XA ? MF : 1];
     __shared__ double gxs[8][RING][XA ? MF : 1];  // x inflow ghosts of the first x warp, prefetched per row
     __shared__ int s_task;
     __shared__ int s_done[16];  // point-to-point row sync: last step finished by each warp
