@@ -633,7 +633,6 @@ void launch_cols_k(pdg_ctx *c, const pdg::SweepParams &sp, int64_t maxl)
     const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
     if (c->launch_cache.find(key) == c->launch_cache.end()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // room for 3-4 CTAs
         c->launch_cache[key] = 1;
     }
     dim3 grid((unsigned)((maxl + kColsW - 1) / kColsW), (unsigned)sp.nvel);
@@ -1009,7 +1008,6 @@ void launch_relax_x_k(pdg_ctx *c, const pdg::RelaxXParams &P, size_t smem)
     const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
     if (c->launch_cache.find(key) == c->launch_cache.end()) {  // per context: attributes are per device
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         c->launch_cache[key] = 1;
     }
     const unsigned nlines = (unsigned)(c->g.nnodes / (c->g.ncell[0] * N));

@@ -510,29 +510,42 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
     const int64_t nn = P.nnodes;
     PDG_CHECK_IDX(base + (NV - 1) * nn + Lx - 1, P.f_elems, "relax_xsweep f");  // the line's last node
 
-    // phase 1: collision at every node of the line
-    for (int X = threadIdx.x; X < Lx; X += blockDim.x) {
-        const double *src = P.f + base + X;
-        double fv[NV];
+    // phase 1: collision at every node of the line.  With few velocities per node (2-D models) a
+    // thread loads U = 2 nodes before computing either, so twice the loads are in flight (the
+    // loads of the next node cannot move above this node's stores: f may alias)
+    constexpr int U = (NV <= 16) ? 2 : 1;
+    for (int X0 = threadIdx.x; X0 < Lx; X0 += U * blockDim.x) {
+        double fv[U][NV];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) fv[i] = __ldcs(src + i * nn);
-        double w[M];
+        for (int u = 0; u < U; ++u) {
+            const int X = X0 + u * blockDim.x;
+            if (X < Lx) {
 #pragma unroll
-        for (int c = 0; c < M; ++c) {
-            double s = fv[c * 2 * DIM];
-#pragma unroll
-            for (int j = 1; j < 2 * DIM; ++j) s += fv[c * 2 * DIM + j];
-            w[c] = s;
+                for (int i = 0; i < NV; ++i) fv[u][i] = __ldcs(P.f + base + X + i * nn);
+            }
         }
-        double q[DIM][M];
-        Md::flux(w, q, P.mp);
-        const int xs = X + X / SEG;
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const double val = fma(P.cb, feq_of<DIM, M>(i, w, q, P.mp), P.ca * fv[i]);
-            const int c = i / (2 * DIM), k = (i % (2 * DIM)) >> 1, s = i & 1;
-            if (k == 0) sx[(2 * c + s) * Lp + xs] = val;
-            else __stcs(P.f + base + X + i * nn, val);
+        for (int u = 0; u < U; ++u) {
+            const int X = X0 + u * blockDim.x;
+            if (X >= Lx) break;
+            double w[M];
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                double s = fv[u][c * 2 * DIM];
+#pragma unroll
+                for (int j = 1; j < 2 * DIM; ++j) s += fv[u][c * 2 * DIM + j];
+                w[c] = s;
+            }
+            double q[DIM][M];
+            Md::flux(w, q, P.mp);
+            const int xs = X + X / SEG;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const double val = fma(P.cb, feq_of<DIM, M>(i, w, q, P.mp), P.ca * fv[u][i]);
+                const int c = i / (2 * DIM), k = (i % (2 * DIM)) >> 1, s = i & 1;
+                if (k == 0) sx[(2 * c + s) * Lp + xs] = val;
+                else __stcs(P.f + base + X + i * nn, val);
+            }
         }
     }
     __syncthreads();
