@@ -119,10 +119,11 @@ typedef enum {
                                 first nv % G ranks one more) on the whole grid; one NCCL sum of the m
                                 moment fields per collision (north star) */
     PDG_DECOMP_ZSLAB = 1     /* rank r owns the cell planes [r N/G, (r+1) N/G) of the slowest axis (z in 3-D,
-                                y in 2-D) with every velocity; sweeps along that axis run per slab with zero
-                                inflow, the exact inflows follow from an affine scan of the slabs' outgoing
-                                carries (linear superposition of the carry recurrence; NCCL all-gather of
-                                carry planes) and a correction of the first cells of each slab */
+                                y in 2-D) with every velocity; for sweeps along that axis a read-only
+                                pre-pass computes each slab's zero-inflow outgoing carries (last cells
+                                only), the exact slab inflows follow from an affine scan of those carries
+                                (linear superposition of the carry recurrence; NCCL all-gather of carry
+                                planes), and every slab is swept once from its exact inflows */
 } pdg_decomposition;
 
 /* pdg_problem.flags */
@@ -154,7 +155,7 @@ typedef enum {
     PDG_K_ALLREDUCE = 5,     /* NCCL sum of w */
     PDG_K_OTHER = 6,         /* initialisation / checks */
     PDG_K_RELAX_X = 7,       /* collision fused with moments and the following x-velocity sweep(s) */
-    PDG_K_ZSLAB = 8,         /* z-slab carry scan + correction (and the carry all-gather) */
+    PDG_K_ZSLAB = 8,         /* z-slab carry pre-pass and scan (and the carry all-gather) */
     PDG_K_LATTICE = 9,       /* T2 sweeps of lattice velocities with >= 2 non-zero components (NEXT-2) */
     PDG_NUM_KERNEL_KINDS = 10
 } pdg_kernel_kind;
@@ -300,7 +301,8 @@ pdg_status pdg_cell_block(const pdg_ctx *c, int axis, double dtp, double *M, dou
  *          S_last = S2 for npass 2, S1 for npass 1; nodes of cell l in flow order),
  *   outgoing carries: c1 = A1 + B S1,  c2 = A2 + B S2 + C S1   (A = the zero-inflow carries).
  * Outputs (host): P, Q: [len][p+1] row-major; B = beta^len; C; leff = cells after which every
- * |P_l|, |Q_l| < 2^-64 (the correction the library applies stops there, reading C26).
+ * |P_l|, |Q_l| < 2^-64 (a slab's inflow no longer moves its values in fp64, reading C26).  (The
+ * library itself uses B and C for the carry scan and sweeps each slab from its exact inflows.)
  * Host-only (no GPU); computed in long double and rounded once.
  * Errors: those of pdg_query_sizes; PDG_E_INVALID_ARGUMENT for npass, len < 1, NULL outputs. */
 pdg_status pdg_zslab_table(const pdg_problem *p, double dtp, int npass, int64_t len, double *P, double *Q,
