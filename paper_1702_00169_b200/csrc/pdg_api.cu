@@ -391,7 +391,6 @@ pdg_status validate(const pdg_problem *p, Geometry *g)
     const int64_t plane = g->nnodes / g->L[outer];  // lines along the outer axis
     const int nvo = 2 * p->m;                         // velocities along the outer axis
     g->carry_doubles = (size_t)S * nvo * 2 * (size_t)plane;
-    const int64_t lmax = (Nout + S - 1) / S + 1;
     return PDG_OK;
 }
 
