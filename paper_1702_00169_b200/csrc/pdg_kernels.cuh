@@ -336,20 +336,36 @@ __device__ __forceinline__ void warp_line_sweep(double *row, int ncells, bool up
     for (int sc0 = 0; sc0 < ncells; sc0 += 32 * K) {
         const int f0 = sc0 + lane * K;
         const int cnt = max(0, min(K, ncells - f0));
+        // A full chunk whose lane segments align with the padding segments (always upward; downward
+        // when the line length is a multiple of SEG): the lane's K N nodes are contiguous in the padded
+        // row at a per-lane base, so every index is base +- a compile-time offset (no division).
+        //   up:   X = sc0 N + lane SEG + j,          X + X / SEG = base + j, base = sc0 N + lane SEG + sc0 / K + lane
+        //   down: X = SEG q - 1 - j (q = L / SEG - sc0 / K - lane),  X + X / SEG = SEG q + q - 2 - j
+        const int Lx = ncells * N;
+        const bool fast = (sc0 + 32 * K <= ncells) && (up || Lx % SEG == 0);
+        const int q0 = Lx / SEG - sc0 / K - lane;
+        const int fbase = up ? sc0 * N + lane * SEG + sc0 / K + lane : SEG * q0 + q0 - 2;
         double v[K][N];
+        if (fast) {
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-            if (kk < cnt) {
-                const int fc = f0 + kk;
-                const int mc = up ? fc : ncells - 1 - fc;
+            for (int kk = 0; kk < K; ++kk)
 #pragma unroll
-                for (int a = 0; a < N; ++a) {
-                    const int X = mc * N + (up ? a : N - 1 - a);
-                    v[kk][a] = row[X + X / SEG];
+                for (int a = 0; a < N; ++a) v[kk][a] = row[up ? fbase + kk * N + a : fbase - (kk * N + a)];
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                if (kk < cnt) {
+                    const int fc = f0 + kk;
+                    const int mc = up ? fc : ncells - 1 - fc;
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        const int X = mc * N + (up ? a : N - 1 - a);
+                        v[kk][a] = row[X + X / SEG];
+                    }
+                } else {
+#pragma unroll
+                    for (int a = 0; a < N; ++a) v[kk][a] = 0.0;
                 }
-            } else {
-#pragma unroll
-                for (int a = 0; a < N; ++a) v[kk][a] = 0.0;
             }
         }
 #pragma unroll
@@ -399,15 +415,22 @@ __device__ __forceinline__ void warp_line_sweep(double *row, int ncells, bool up
             }
             carry[q] = __shfl_sync(FULL, fma(B, carry[q], A), 31);
         }
+        if (fast) {
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-            if (kk < cnt) {
-                const int fc = f0 + kk;
-                const int mc = up ? fc : ncells - 1 - fc;
+            for (int kk = 0; kk < K; ++kk)
 #pragma unroll
-                for (int a = 0; a < N; ++a) {
-                    const int X = mc * N + (up ? a : N - 1 - a);
-                    row[X + X / SEG] = v[kk][a];
+                for (int a = 0; a < N; ++a) row[up ? fbase + kk * N + a : fbase - (kk * N + a)] = v[kk][a];
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                if (kk < cnt) {
+                    const int fc = f0 + kk;
+                    const int mc = up ? fc : ncells - 1 - fc;
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        const int X = mc * N + (up ? a : N - 1 - a);
+                        row[X + X / SEG] = v[kk][a];
+                    }
                 }
             }
         }
