@@ -589,13 +589,14 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
     }
     __syncthreads();
 
-    // phase 3: store the x-velocities
-    for (int v = 0; v < 2 * M; ++v) {
-        const int c = v >> 1, s = v & 1;
-        const int i = c * 2 * DIM + s;
-        double *dst = P.f + base + i * nn;
-        const double *srow = sx + v * Lp;
-        for (int X = threadIdx.x; X < Lx; X += blockDim.x) __stcs(dst + X, srow[X + X / SEG]);
+    // phase 3: store the x-velocities (node-outer: one padded index per node for all of them)
+    for (int X = threadIdx.x; X < Lx; X += blockDim.x) {
+        const int xs = X + X / SEG;
+#pragma unroll
+        for (int v = 0; v < 2 * M; ++v) {
+            const int i = (v >> 1) * 2 * DIM + (v & 1);
+            __stcs(P.f + base + X + i * nn, sx[v * Lp + xs]);
+        }
     }
 }
 
@@ -717,9 +718,8 @@ __global__ void __launch_bounds__(256) relax_xsweep_tma_kernel(const RelaxXParam
             warp_line_sweep<N, NPASS, K>(sx + v * Lp, P.ncx, s == 0, Mb, gb, s0, lane);
         }
         __syncthreads();
-        for (int v = 0; v < 2 * M; ++v) {
-            const int c = v >> 1, s = v & 1;
-            const int i = c * 2 * DIM + s;
+        for (int v = 0; v < 2 * M; ++v) {  // (velocity-outer measured faster here than node-outer)
+            const int i = (v >> 1) * 2 * DIM + (v & 1);
             double *dst = P.f + base + i * nn;
             const double *srow = sx + v * Lp;
             for (int X = threadIdx.x; X < Lx; X += blockDim.x) __stcs(dst + X, srow[X + X / SEG]);
