@@ -181,47 +181,65 @@ __global__ void __launch_bounds__(256) sweep_strided_kernel(const SweepParams P)
         for (int q = 0; q < NPASS; ++q) carry[q] = s0;
     }
 
-    // ring of PF prefetched cells (values in flow order)
+    // ring of PF prefetched cells (values in flow order).  The walk advances a load pointer and a
+    // store pointer by one cell (N step elements); node a of a cell is at a fixed offset a step
+    // (fewer integer instructions per node than recomputing 64-bit indices: the kernel runs under
+    // the power cap next to the fused pass)
+    const int64_t cstep = (int64_t)N * step;
+    int64_t off[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) off[a] = (int64_t)a * step;
     double ring[PF][N];
 #pragma unroll
     for (int k = 0; k < PF; ++k)
         if (k < V.ncells) {
 #pragma unroll
-            for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(p + (int64_t)(k * N + a) * step);
+            for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(p + k * cstep + off[a]);
         }
-
-    for (int c0 = 0; c0 < V.ncells; c0 += PF) {
+    const double *lp = p + PF * cstep;  // the cell PF ahead of the one being updated
+    double *sp = p;
+    auto cell = [&](double (&fo)[N]) {
+#pragma unroll
+        for (int q = 0; q < NPASS; ++q) {
+            double fn[N];
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+                double acc = g[a] * carry[q];
+#pragma unroll
+                for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
+                fn[a] = acc;
+            }
+            carry[q] = fo[N - 1] + fn[N - 1];
+#pragma unroll
+            for (int a = 0; a < N; ++a) fo[a] = fn[a];
+        }
+#pragma unroll
+        for (int a = 0; a < N; ++a) __stcs(sp + off[a], fo[a]);
+        sp += cstep;
+    };
+    const int nfull = (V.ncells / PF) * PF;
+    for (int c0 = 0; c0 < nfull; c0 += PF) {
 #pragma unroll
         for (int k = 0; k < PF; ++k) {
-            const int c = c0 + k;
-            if (c < V.ncells) {
-                double fo[N];
+            double fo[N];
 #pragma unroll
-                for (int a = 0; a < N; ++a) fo[a] = ring[k][a];
-                const int cn = c + PF;
-                if (cn < V.ncells) {
+            for (int a = 0; a < N; ++a) fo[a] = ring[k][a];
+            if (c0 + k + PF < V.ncells) {
 #pragma unroll
-                    for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(p + ((int64_t)cn * N + a) * step);
-                }
-#pragma unroll
-                for (int q = 0; q < NPASS; ++q) {
-                    double fn[N];
-#pragma unroll
-                    for (int a = 0; a < N; ++a) {
-                        double acc = g[a] * carry[q];
-#pragma unroll
-                        for (int b = 0; b < N; ++b) acc = fma(M[a * N + b], fo[b], acc);
-                        fn[a] = acc;
-                    }
-                    carry[q] = fo[N - 1] + fn[N - 1];
-#pragma unroll
-                    for (int a = 0; a < N; ++a) fo[a] = fn[a];
-                }
-#pragma unroll
-                for (int a = 0; a < N; ++a) __stcs(p + ((int64_t)c * N + a) * step, fo[a]);
+                for (int a = 0; a < N; ++a) ring[k][a] = __ldcs(lp + off[a]);
             }
+            lp += cstep;
+            cell(fo);
         }
     }
+#pragma unroll
+    for (int k = 0; k < PF; ++k)  // ragged tail: the last ncells % PF cells, already in the ring
+        if (nfull + k < V.ncells) {
+            double fo[N];
+#pragma unroll
+            for (int a = 0; a < N; ++a) fo[a] = ring[k][a];
+            cell(fo);
+        }
     if (V.cout_off >= 0) {
 #pragma unroll
         for (int q = 0; q < NPASS; ++q) {
