@@ -233,33 +233,6 @@ __device__ __forceinline__ void wait_progress(const int *p, int need)
     }
 }
 
-// Calls f(q, base + sum_t digit_t(q) dstep[t]) for the N^DA nodes q of a unit (digit t of q in base
-// N, t = 0 fastest), building the element offsets by nested partial sums (shared by the nodes that
-// agree on the slower digits) instead of a 64-bit product per node and digit.
-template <int N, int DA, class F>
-__device__ __forceinline__ void for_unit_nodes(int64_t base, const int64_t (&dstep)[3], F &&f)
-{
-    if constexpr (DA == 3) {
-#pragma unroll
-        for (int c2 = 0; c2 < N; ++c2) {
-            const int64_t b2 = base + c2 * dstep[2];
-#pragma unroll
-            for (int c1 = 0; c1 < N; ++c1) {
-                const int64_t b1 = b2 + c1 * dstep[1];
-#pragma unroll
-                for (int c0 = 0; c0 < N; ++c0) f(c0 + N * (c1 + N * c2), b1 + c0 * dstep[0]);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int c1 = 0; c1 < N; ++c1) {
-            const int64_t b1 = base + c1 * dstep[1];
-#pragma unroll
-            for (int c0 = 0; c0 < N; ++c0) f(c0 + N * c1, b1 + c0 * dstep[0]);
-        }
-    }
-}
-
 // Index of a node (given by its flow coordinates u[] on every axis) in the inflow plane of
 // axis k: the node grid with axis k removed, same order (include/pdg.h).
 template <int D>
@@ -577,10 +550,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
             if (valid && rr < nrow) {
                 const int64_t ubr = ibase + cbase + (int64_t)(r0 + rr) * cstep;
                 double *dst = wbuf + (rr % RING) * NB * 32;
-                for_unit_nodes<N, DA>(ubr, dstep, [&](int q, int64_t e) {
-                    PDG_CHECK_IDX(e, P.f_elems, "lattice row load f");
-                    cp_async8(dst + ro(q, lane), P.f + e);
-                });
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    int64_t off = 0;
+#pragma unroll
+                    for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
+                    PDG_CHECK_IDX(ubr + off, P.f_elems, "lattice row load f");
+                    cp_async8(dst + ro(q, lane), P.f + ubr + off);
+                }
                 if constexpr (XA) {  // the row's x inflow ghost (first x warp of the first x group)
                     if (gx == 0 && qx == 0 && lane == 0) {
                         int uc[3] = {ucell[0], ucell[1], ucell[2]};
@@ -898,10 +875,14 @@ __global__ void __launch_bounds__(256, LatShape<D, ACT>::DA == 3 ? 1 : 2)
                     hclear = true;
                 }
                 if (valid && r0 + r >= rs) {
-                    for_unit_nodes<N, DA>(ub, dstep, [&](int q, int64_t e) {
-                        PDG_CHECK_IDX(e, P.f_elems, "lattice row store f");
-                        __stcs(P.f + e, fn[q]);
-                    });
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) {
+                        int64_t off = 0;
+#pragma unroll
+                        for (int tt = 0; tt < DA; ++tt) off += (int64_t)((q / ipow(N, tt)) % N) * dstep[tt];
+                        PDG_CHECK_IDX(ub + off, P.f_elems, "lattice row store f");
+                        __stcs(P.f + ub + off, fn[q]);
+                    }
                 }
             }
             PDG_TMARK(6);
