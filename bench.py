@@ -439,6 +439,31 @@ def run_product(args, cfg):
             cpu = cpu_baseline(cfg, args.cpu_cells)
 
         S.destroy()
+        # --graph: the same K steps captured once in a CUDA graph (pdg_step is capturable; no
+        # per-launch profiling events) and replayed: the launch gaps of the plain call removed
+        graph = None
+        if args.graph and world == 1:
+            Gs = pdist.sharded_solver(cfg, device, flags=0, stream=stream.cuda_stream)
+            fill_w0(cfg, Gs.w, device, Gs.sizes)
+            Gs.set_equilibrium(Gs.w)
+            Gs.step(args.warmup)
+            torch.cuda.synchronize(device)
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=stream):
+                Gs.step(args.steps)
+            cg.replay()  # warm
+            torch.cuda.synchronize(device)
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            cg.replay()
+            g1.record(stream)
+            torch.cuda.synchronize(device)
+            gms = g0.elapsed_time(g1)
+            graph = {"ms_per_step": gms / args.steps, "value": cfg.updates_per_step * args.steps / (gms * 1e-3),
+                     "unit": UNIT, "call": f"one CUDA graph of pdg_step({args.steps}), replayed"}
+            del cg
+            Gs.destroy()
         # several ranks: also time the other decomposition (velocity sharding is the north star's
         # partition, the exact z-slab decomposition the scalable one; both exact)
         alt = None
@@ -483,6 +508,8 @@ def run_product(args, cfg):
                                                  "a throughput ratio, not a roofline fraction"}
             if alt is not None:
                 line["alt_decomposition"] = alt
+            if graph is not None:
+                line["graph"] = graph
             print(json.dumps(line), flush=True)
     if launched:
         dist.destroy_process_group()
@@ -505,6 +532,8 @@ def main():
     ap.add_argument("--slabs-per-rank", type=int, default=1)
     ap.add_argument("--oracle-table", action="store_true",
                     help="time the CPU oracle on configs 1-3 at full size (1 thread and all cores) and exit")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the K steps captured in one CUDA graph and replayed (key `graph`)")
     ap.add_argument("--no-tma", action="store_true",
                     help="register-staged collision + x-sweep pass instead of bulk-copy staging (PDG_NO_TMA)")
     ap.add_argument("--one-decomp", action="store_true",

@@ -1,0 +1,5 @@
+# CUDA-graph replay of pdg_step(K) against the plain call
+set -x
+for c in 1 2 3; do
+  timeout 600 python bench.py --config $c --steps 50 --warmup 5 --no-e2e --no-cpu-baseline --graph > gpurun_out/r2o_cfg$c.json 2>&1
+done
