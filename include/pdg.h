@@ -141,6 +141,8 @@ typedef enum {
                                  by 8 m nnodes_local bytes) and pdg_moments' download runs on a library copy
                                  stream, so the upload of step k+1's input overlaps the download of step k's
                                  result (PCIe is full duplex) */
+#define PDG_NO_GRAPH    0x40u /* pdg_step launches its kernels directly instead of replaying a CUDA graph of its
+                                 n-step launch sequence (same results; for measurement) */
 #define PDG_NO_TMA      0x20u /* stage the line of the fused collision + x-sweep pass through registers instead of
                                  Tensor-Memory-Accelerator bulk copies (the variant for odd line lengths;
                                  same results; for measurement) */
@@ -254,7 +256,11 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
 
 /* Advance nsteps palindromic steps (scheme of pdg_problem; nsteps == 0 is a no-op).
  * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE (lattice classes
- * run on library streams forked from and joined back into the context stream). */
+ * run on library streams forked from and joined back into the context stream).  For nsteps >= 2
+ * the launch sequence of up to 256 steps is captured once per step count into a CUDA graph and
+ * replayed (the first call of a given count pays the capture); not with PDG_PROFILE,
+ * PDG_SYNC_ERRORS, PDG_NO_GRAPH, a communicator, or while the caller's stream is being captured
+ * (then the kernels go into the caller's graph).  Capturable by the caller. */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
 
 /* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):

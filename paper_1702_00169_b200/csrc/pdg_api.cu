@@ -466,6 +466,11 @@ struct pdg_ctx {
     pdg::SweepParams yz_params{};       // velocities along y / z
     pdg::SweepParams all_params{};      // every local velocity (inflow initialisation)
     pdg::NcclComm comm;
+    // pdg_step(n) replays a CUDA graph of its n-step launch sequence (captured on cap_stream once
+    // per n, launched on the caller's stream)
+    cudaStream_t cap_stream = nullptr;
+    std::map<int64_t, cudaGraphExec_t> step_graphs;
+    bool graphs_off = false;  // a capture failed once: direct launches from then on
     cudaStream_t comm_stream = nullptr;                // NCCL sums of the pipelined sharded collision
     cudaEvent_t ev_pm[kMaxChunks] = {}, ev_ar[kMaxChunks] = {};  // per chunk: partial moments written, summed
     int device = 0;
@@ -1647,6 +1652,71 @@ pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
     return post_launch(c, "zslab_scan");
 }
 
+// ---- pdg_step as a replayed CUDA graph ---------------------------------------------------
+// A step is 2-3 dependent launches; for small grids (configs 1-2) the gaps between launches are
+// a large part of the step (config 2: 71 -> 53 us per step, config 1: 22 -> 7 us when replayed
+// from a graph; bench.py --graph).  pdg_step(n) therefore captures its n-step launch sequence
+// once per n (on a library stream, so the caller's stream may be the legacy default stream) and
+// replays it on the caller's stream.  Not used with per-launch profiling events, synchronous error
+// checks, a communicator (NCCL), PDG_NO_GRAPH, or when the caller's stream is itself being captured
+// (the launches then go into the caller's graph directly).
+constexpr int64_t kMaxGraphSteps = 256;
+constexpr size_t kMaxStepGraphs = 8;
+
+bool use_step_graph(pdg_ctx *c, int64_t nsteps)
+{
+    if (nsteps < 2 || c->graphs_off || c->comm.comm || c->prob.nranks > 1) return false;
+    if (c->prob.flags & (PDG_PROFILE | PDG_SYNC_ERRORS | PDG_NO_GRAPH)) return false;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c->stream, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return st == cudaStreamCaptureStatusNone;
+}
+
+void destroy_step_graphs(pdg_ctx *c)
+{
+    for (auto &kv : c->step_graphs)
+        if (kv.second) cudaGraphExecDestroy(kv.second);
+    c->step_graphs.clear();
+}
+
+pdg_status step_graph(pdg_ctx *c, int64_t nsteps, const std::vector<Op> &ops)
+{
+    auto it = c->step_graphs.find(nsteps);
+    cudaGraphExec_t exec = (it != c->step_graphs.end()) ? it->second : nullptr;
+    if (!exec) {
+        if (!c->cap_stream) {
+            int prio = 0;
+            cudaStreamGetPriority(c->stream, &prio);
+            PDG_CUDA_TRY(cudaStreamCreateWithPriority(&c->cap_stream, cudaStreamNonBlocking, prio));
+        }
+        if (c->step_graphs.size() >= kMaxStepGraphs) destroy_step_graphs(c);
+        cudaStream_t user = c->stream;
+        c->stream = c->cap_stream;  // every launch of execute_ops goes to the capturing stream
+        cudaGraph_t graph = nullptr;
+        pdg_status s = PDG_OK;
+        cudaError_t e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            s = execute_ops(c, ops);
+            e = cudaStreamEndCapture(c->cap_stream, &graph);
+        }
+        c->stream = user;
+        if (s == PDG_OK && e == cudaSuccess && graph) e = cudaGraphInstantiate(&exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (s != PDG_OK || e != cudaSuccess || !exec) {
+            // capture or instantiation failed: direct launches for this context from now on
+            cudaGetLastError();
+            c->graphs_off = true;
+            return execute_ops(c, ops);
+        }
+        c->step_graphs[nsteps] = exec;
+    }
+    PDG_CUDA_TRY(cudaGraphLaunch(exec, c->stream));
+    return post_launch(c, "step graph");
+}
+
 bool is_device_pointer(const void *p)
 {
     cudaPointerAttributes attr;
@@ -2001,9 +2071,15 @@ pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
     if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (nsteps == 0) return PDG_OK;
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
-    std::vector<Op> ops;
-    for (int64_t k = 0; k < nsteps; ++k) append_scheme(ops, c->prob.scheme, c->prob.dt);
-    pdg_status s = execute_ops(c, ops);
+    pdg_status s = PDG_OK;
+    for (int64_t done = 0; done < nsteps && s == PDG_OK;) {
+        // runs of at most kMaxGraphSteps steps (a longer call is the same as consecutive calls)
+        const int64_t k = use_step_graph(c, nsteps) ? std::min<int64_t>(kMaxGraphSteps, nsteps - done) : nsteps - done;
+        std::vector<Op> ops;
+        for (int64_t j = 0; j < k; ++j) append_scheme(ops, c->prob.scheme, c->prob.dt);
+        s = use_step_graph(c, k) ? step_graph(c, k, ops) : execute_ops(c, ops);
+        done += k;
+    }
     if (s != PDG_OK) return s;
     if (c->prob.flags & PDG_CHECK_STATE) {
         int64_t bad = 0;
@@ -2120,6 +2196,9 @@ void pdg_destroy(pdg_ctx *c)
         cudaStreamSynchronize(c->comm_stream);
         cudaStreamDestroy(c->comm_stream);
     }
+    cudaStreamSynchronize(c->stream);  // a replayed step graph may still run on the caller's stream
+    destroy_step_graphs(c);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     for (int k = 0; k < kMaxChunks; ++k) {
         if (c->ev_pm[k]) cudaEventDestroy(c->ev_pm[k]);
         if (c->ev_ar[k]) cudaEventDestroy(c->ev_ar[k]);

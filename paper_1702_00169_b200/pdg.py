@@ -44,6 +44,7 @@ PDG_NO_FUSION = 0x4
 PDG_PROFILE = 0x8
 PDG_ASYNC_HOST = 0x10
 PDG_NO_TMA = 0x20
+PDG_NO_GRAPH = 0x40
 KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other",
                 "relax_xsweep", "zslab", "lattice"]
 PDG_DECOMP_VELOCITY = 0

@@ -582,3 +582,28 @@ def test_velocity_sharded_steps_standin(G):
     for S in shards:
         S.destroy()
     assert rel_maxnorm(got, O.m2_run(pb, f0, fbg, 2)) < TOL_STEP
+
+
+@pytest.mark.parametrize("kind,steps", [("iso", 7), ("iso", 300), ("lbm", 5), ("zslab", 4)])
+def test_step_graph_replay_equals_direct_launches(kind, steps):
+    """pdg_step(n) replays a CUDA graph of its launch sequence (captured once per n on a library
+    stream, launched on the caller's): bit-identical to the direct launches (PDG_NO_GRAPH), on the
+    default stream, twice in a row (the second call replays the cached graph), across the 256-step
+    chunk boundary (n = 300), for a lattice set and for the emulated z-slab decomposition."""
+    from paper_1702_00169_b200 import pdg
+    from pdg_inputs import lbm_config
+    if kind == "lbm":
+        cfg = lbm_config("D3Q19", 6)
+    else:
+        cfg = CONFIGS[3].resized(4 if steps > 100 else 6).stabilised()
+    kw = dict(decomposition=pdg.PDG_DECOMP_ZSLAB, slabs_per_rank=3) if kind == "zslab" else {}
+    w0 = w0_grid(cfg).reshape(-1).cuda()
+    outs = []
+    for flags in (0, pdg.PDG_NO_GRAPH):
+        S = make_solver(cfg, flags=flags, **kw)
+        S.set_equilibrium(w0)
+        S.step(steps)
+        S.step(steps)
+        outs.append(S.get_state().clone())
+        S.destroy()
+    assert torch.equal(outs[0], outs[1])
