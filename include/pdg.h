@@ -256,9 +256,9 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
 
 /* Advance nsteps palindromic steps (scheme of pdg_problem; nsteps == 0 is a no-op).
  * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE (lattice classes
- * run on library streams forked from and joined back into the context stream).  For nsteps >= 2
- * the launch sequence of up to 256 steps is captured once per step count into a CUDA graph and
- * replayed (the first call of a given count pays the capture); not with PDG_PROFILE,
+ * run on library streams forked from and joined back into the context stream).  For 2 <= nsteps
+ * <= 1024 the launch sequence is captured once per step count into a CUDA graph and replayed (the
+ * first call of a given count pays the capture; same launches, same results); not with PDG_PROFILE,
  * PDG_SYNC_ERRORS, PDG_NO_GRAPH, a communicator, or while the caller's stream is being captured
  * (then the kernels go into the caller's graph).  Capturable by the caller. */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);

@@ -1660,12 +1660,12 @@ pdg_status zslab_resolve(pdg_ctx *c, double dtp, int npass)
 // replays it on the caller's stream.  Not used with per-launch profiling events, synchronous error
 // checks, a communicator (NCCL), PDG_NO_GRAPH, or when the caller's stream is itself being captured
 // (the launches then go into the caller's graph directly).
-constexpr int64_t kMaxGraphSteps = 256;
+constexpr int64_t kMaxGraphSteps = 1024;  // longer calls launch directly (same launches, same results)
 constexpr size_t kMaxStepGraphs = 8;
 
 bool use_step_graph(pdg_ctx *c, int64_t nsteps)
 {
-    if (nsteps < 2 || c->graphs_off || c->comm.comm || c->prob.nranks > 1) return false;
+    if (nsteps < 2 || nsteps > kMaxGraphSteps || c->graphs_off || c->comm.comm || c->prob.nranks > 1) return false;
     if (c->prob.flags & (PDG_PROFILE | PDG_SYNC_ERRORS | PDG_NO_GRAPH)) return false;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(c->stream, &st) != cudaSuccess) {
@@ -2071,15 +2071,9 @@ pdg_status pdg_step(pdg_ctx *c, int64_t nsteps)
     if (nsteps < 0) return fail(PDG_E_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (nsteps == 0) return PDG_OK;
     if (!c->state_set) return fail(PDG_E_STATE_NOT_SET, "set the state first");
-    pdg_status s = PDG_OK;
-    for (int64_t done = 0; done < nsteps && s == PDG_OK;) {
-        // runs of at most kMaxGraphSteps steps (a longer call is the same as consecutive calls)
-        const int64_t k = use_step_graph(c, nsteps) ? std::min<int64_t>(kMaxGraphSteps, nsteps - done) : nsteps - done;
-        std::vector<Op> ops;
-        for (int64_t j = 0; j < k; ++j) append_scheme(ops, c->prob.scheme, c->prob.dt);
-        s = use_step_graph(c, k) ? step_graph(c, k, ops) : execute_ops(c, ops);
-        done += k;
-    }
+    std::vector<Op> ops;
+    for (int64_t k = 0; k < nsteps; ++k) append_scheme(ops, c->prob.scheme, c->prob.dt);
+    pdg_status s = use_step_graph(c, nsteps) ? step_graph(c, nsteps, ops) : execute_ops(c, ops);
     if (s != PDG_OK) return s;
     if (c->prob.flags & PDG_CHECK_STATE) {
         int64_t bad = 0;

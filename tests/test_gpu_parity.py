@@ -588,8 +588,8 @@ def test_velocity_sharded_steps_standin(G):
 def test_step_graph_replay_equals_direct_launches(kind, steps):
     """pdg_step(n) replays a CUDA graph of its launch sequence (captured once per n on a library
     stream, launched on the caller's): bit-identical to the direct launches (PDG_NO_GRAPH), on the
-    default stream, twice in a row (the second call replays the cached graph), across the 256-step
-    chunk boundary (n = 300), for a lattice set and for the emulated z-slab decomposition."""
+    default stream, twice in a row (the second call replays the cached graph), for a long call
+    (n = 300), a lattice set and the emulated z-slab decomposition."""
     from paper_1702_00169_b200 import pdg
     from pdg_inputs import lbm_config
     if kind == "lbm":
