@@ -258,9 +258,10 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
  * Asynchronous on the context stream unless PDG_SYNC_ERRORS / PDG_CHECK_STATE (lattice classes
  * run on library streams forked from and joined back into the context stream).  For 2 <= nsteps
  * <= 1024 the launch sequence is captured once per step count into a CUDA graph and replayed (the
- * first call of a given count pays the capture; same launches, same results); not with PDG_PROFILE,
- * PDG_SYNC_ERRORS, PDG_NO_GRAPH, a communicator, or while the caller's stream is being captured
- * (then the kernels go into the caller's graph).  Capturable by the caller. */
+ * first call of a given count pays the capture; same launches, same results); not while PDG_PROFILE
+ * events are active (pdg_profile_enable), with PDG_SYNC_ERRORS, PDG_NO_GRAPH, a communicator, or
+ * while the caller's stream is being captured (then the kernels go into the caller's graph).
+ * Capturable by the caller. */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
 
 /* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):
@@ -337,6 +338,11 @@ const char *pdg_last_error(void);
  * one fp64 read + one write of every value a launch updates, plus its side inputs
  * (inflow planes, moments), i.e. the traffic of a perfect single pass. */
 pdg_status pdg_profile_read(pdg_ctx *c, double *ms, int64_t *launches, double *alg_bytes);
+
+/* (PDG_PROFILE) Pause (on = 0) or resume (on != 0) the per-launch events; while paused the context
+ * runs as without PDG_PROFILE (pdg_step may replay its CUDA graph).  PDG_E_INVALID_ARGUMENT if the
+ * context was created without PDG_PROFILE. */
+pdg_status pdg_profile_enable(pdg_ctx *c, int on);
 
 /* Library version string ("pdg-b200 <version> sm_100a"). */
 const char *pdg_version(void);

@@ -437,7 +437,8 @@ struct ProfRec {
 };
 
 struct Profiler {
-    bool on = false;
+    bool on = false;       // events allocated (PDG_PROFILE)
+    bool paused = false;   // pdg_profile_enable(c, 0)
     std::vector<cudaEvent_t> ev;
     std::vector<ProfRec> recs;
     int next = 0;
@@ -538,7 +539,7 @@ pdg_status post_launch(pdg_ctx *c, const char *what)
 // PDG_PROFILE: CUDA events bracketing each launch on the context stream.
 int prof_begin(pdg_ctx *c, cudaStream_t st = nullptr)
 {
-    if (!c->prof.on || c->prof.next + 2 > (int)c->prof.ev.size()) return -1;
+    if (!c->prof.on || c->prof.paused || c->prof.next + 2 > (int)c->prof.ev.size()) return -1;
     const int i = c->prof.next;
     c->prof.next += 2;
     cudaEventRecord(c->prof.ev[i], st ? st : c->stream);
@@ -1666,7 +1667,7 @@ constexpr size_t kMaxStepGraphs = 8;
 bool use_step_graph(pdg_ctx *c, int64_t nsteps)
 {
     if (nsteps < 2 || nsteps > kMaxGraphSteps || c->graphs_off || c->comm.comm || c->prob.nranks > 1) return false;
-    if (c->prob.flags & (PDG_PROFILE | PDG_SYNC_ERRORS | PDG_NO_GRAPH)) return false;
+    if ((c->prof.on && !c->prof.paused) || (c->prob.flags & (PDG_SYNC_ERRORS | PDG_NO_GRAPH))) return false;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(c->stream, &st) != cudaSuccess) {
         cudaGetLastError();
@@ -2237,6 +2238,14 @@ pdg_status pdg_profile_read(pdg_ctx *c, double *ms, int64_t *launches, double *a
         if (launches) launches[k] = n[k];
         if (alg_bytes) alg_bytes[k] = b[k];
     }
+    return PDG_OK;
+}
+
+pdg_status pdg_profile_enable(pdg_ctx *c, int on)
+{
+    if (!c) return fail(PDG_E_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->prof.on) return fail(PDG_E_INVALID_ARGUMENT, "the context was created without PDG_PROFILE");
+    c->prof.paused = (on == 0);
     return PDG_OK;
 }
 

@@ -55,6 +55,7 @@ EXPORTED = [
     "pdg_transport", "pdg_collide", "pdg_source", "pdg_partial_moments", "pdg_relax_from_w", "pdg_moments",
     "pdg_check_state", "pdg_cell_block", "pdg_synchronize", "pdg_destroy", "pdg_nccl_unique_id",
     "pdg_status_string", "pdg_last_error", "pdg_version", "pdg_profile_read", "pdg_zslab_table",
+    "pdg_profile_enable",
 ]
 
 
@@ -124,6 +125,7 @@ def load() -> ctypes.CDLL:
         "pdg_last_error": ([], ctypes.c_char_p),
         "pdg_version": ([], ctypes.c_char_p),
         "pdg_profile_read": ([ctx, pd, P(i64), pd], st),
+        "pdg_profile_enable": ([ctx, ctypes.c_int], st),
         "pdg_zslab_table": ([P(pdg_problem), d, ctypes.c_int, i64, pd, pd, pd, pd, P(ctypes.c_int32)], st),
     }
     for name, (args, res) in sig.items():
@@ -338,6 +340,10 @@ class Solver:
         b = (ctypes.c_double * k)()
         _check(self.lib.pdg_profile_read(self.ctx, ms, n, b), "pdg_profile_read")
         return {KERNEL_KINDS[i]: (ms[i], n[i], b[i]) for i in range(k)}
+
+    def profile_enable(self, on: bool):
+        """Pause / resume the PDG_PROFILE per-launch events (paused: graph replay allowed)."""
+        _check(self.lib.pdg_profile_enable(self.ctx, int(bool(on))), "pdg_profile_enable")
 
     def synchronize(self):
         _check(self.lib.pdg_synchronize(self.ctx), "pdg_synchronize")

@@ -607,3 +607,25 @@ def test_step_graph_replay_equals_direct_launches(kind, steps):
         outs.append(S.get_state().clone())
         S.destroy()
     assert torch.equal(outs[0], outs[1])
+
+
+def test_profile_pause_and_resume():
+    """pdg_profile_enable: paused events record nothing (and let pdg_step replay its graph), resumed
+    events count every launch again; same results either way."""
+    from paper_1702_00169_b200 import pdg
+    cfg = CONFIGS[3].resized(6).stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    S = gpu_with_state(cfg, f0, fbg, flags=pdg.PDG_PROFILE)
+    S.profile_enable(False)
+    S.step(3)
+    assert sum(v[1] for v in S.profile_read().values()) == 0
+    S.profile_enable(True)
+    S.step(3)
+    prof = S.profile_read()
+    assert prof["relax_xsweep"][1] == 3 and prof["sweep_strided"][1] == 4, prof
+    assert rel_maxnorm(to_np(S.get_state(), f0.shape), O.m2_run(pb, f0, fbg, 6)) < TOL_STEP
+    S.destroy()
+    T = make_solver(cfg)
+    with pytest.raises(pdg.PdgError):
+        T.profile_enable(True)  # created without PDG_PROFILE
+    T.destroy()
