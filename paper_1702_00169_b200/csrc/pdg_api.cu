@@ -606,8 +606,8 @@ int strided_segments(const pdg_ctx *c, const pdg::SweepParams &sp)
 }
 
 // Lines per tile of sweep_cols_kernel, and whether a strided batch can use it: every velocity's
-// lines tile by kColsW (inner % kColsW == 0), no outgoing carries (z-slab entries), and a tile of
-// rows fits the shared memory of two CTAs per SM.
+// lines tile by kColsW (inner % kColsW == 0), every velocity has the same line count and length,
+// no outgoing carries (z-slab entries), and a tile fits the shared memory of two CTAs per SM.
 constexpr int kColsW = 8;
 
 int cols_K(int ncells) { return ncells <= 64 ? 2 : (ncells <= 128 ? 4 : 8); }
@@ -625,23 +625,47 @@ bool use_cols(const pdg_ctx *c, const pdg::SweepParams &sp)
     if (sp.nvel == 0 || cols_smem(c->g.n, sp) > 110 * 1024) return false;
     for (int i = 0; i < sp.nvel; ++i) {
         const pdg::SweepVel &V = sp.v[i];
-        if (V.inner % kColsW != 0 || V.cout_off >= 0 || V.cin_off >= 0 || V.ncells != sp.v[0].ncells) return false;
+        if (V.inner % kColsW != 0 || V.cout_off >= 0 || V.cin_off >= 0 || V.ncells != sp.v[0].ncells ||
+            V.nlines != sp.v[0].nlines)
+            return false;
     }
     return true;
 }
 
-template <int N, int NPASS, int K>
-void launch_cols_k(pdg_ctx *c, const pdg::SweepParams &sp, int64_t maxl)
+template <int N, int NPASS, int K, int AX, bool AL>
+void launch_cols_t(pdg_ctx *c, const pdg::SweepParams &sp)
 {
-    auto kern = pdg::sweep_cols_kernel<N, NPASS, K, kColsW>;
+    auto kern = pdg::sweep_cols_kernel<N, NPASS, K, kColsW, AX, AL>;
     const size_t smem = cols_smem(N, sp);
-    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)0);
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, smem);
     if (c->launch_cache.find(key) == c->launch_cache.end()) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         c->launch_cache[key] = 1;
     }
-    dim3 grid((unsigned)((maxl + kColsW - 1) / kColsW), (unsigned)sp.nvel);
-    kern<<<grid, 256, smem, c->stream>>>(sp);
+    const int64_t tpv = sp.v[0].nlines / kColsW;
+    kern<<<(unsigned)(tpv * sp.nvel), pdg::kColsThreads, smem, c->stream>>>(sp, tpv);
+}
+
+template <int N, int NPASS, int K, int AX>
+void launch_cols_ax(pdg_ctx *c, const pdg::SweepParams &sp)
+{
+    if (sp.v[0].ncells % (32 * K) == 0) launch_cols_t<N, NPASS, K, AX, true>(c, sp);
+    else launch_cols_t<N, NPASS, K, AX, false>(c, sp);
+}
+
+// one launch per sweep axis present in the batch (the kernel's block is a compile-time slot)
+template <int N, int NPASS, int K>
+void launch_cols_k(pdg_ctx *c, const pdg::SweepParams &sp)
+{
+    for (int ax = 1; ax < 3; ++ax) {
+        pdg::SweepParams q = sp;
+        q.nvel = 0;
+        for (int i = 0; i < sp.nvel; ++i)
+            if (sp.v[i].axis == ax) q.v[q.nvel++] = sp.v[i];
+        if (q.nvel == 0) continue;
+        if (ax == 1) launch_cols_ax<N, NPASS, K, 1>(c, q);
+        else launch_cols_ax<N, NPASS, K, 2>(c, q);
+    }
 }
 
 template <int N, int NPASS>
@@ -655,9 +679,9 @@ void launch_sweeps(pdg_ctx *c, const pdg::SweepParams &xp, const pdg::SweepParam
         if (nseg > 1 && use_cols(c, yzp)) {
             // few long lines (2-D grids): tiles of adjacent lines staged in shared memory
             const int K = cols_K(yzp.v[0].ncells);
-            if (K == 2) launch_cols_k<N, NPASS, 2>(c, yzp, maxl);
-            else if (K == 4) launch_cols_k<N, NPASS, 4>(c, yzp, maxl);
-            else launch_cols_k<N, NPASS, 8>(c, yzp, maxl);
+            if (K == 2) launch_cols_k<N, NPASS, 2>(c, yzp);
+            else if (K == 4) launch_cols_k<N, NPASS, 4>(c, yzp);
+            else launch_cols_k<N, NPASS, 8>(c, yzp);
         } else if (nseg > 1) {
             dim3 grid((unsigned)((maxl + 31) / 32), (unsigned)yzp.nvel);
             pdg::sweep_strided_seg_kernel<N, NPASS><<<grid, dim3(32, nseg), 0, c->stream>>>(yzp, nseg);
