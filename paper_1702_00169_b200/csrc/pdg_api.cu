@@ -477,6 +477,7 @@ struct pdg_ctx {
     int device = 0;
     Profiler prof;
     int sms = 148;
+    int l2keep = 0;  // f fits in L2 (<= 70 % of it): keep it resident between passes (pdg_kernels.cuh l2_policy)
     // z-slab decomposition
     std::vector<pdg::SweepVel> outer_entries;  // per (outer velocity, local slab)
     double *zcarry = nullptr, *zinflow = nullptr;
@@ -660,6 +661,7 @@ void launch_cols_k(pdg_ctx *c, const pdg::SweepParams &sp)
     for (int ax = 1; ax < 3; ++ax) {
         pdg::SweepParams q = sp;
         q.nvel = 0;
+        q.l2keep = c->l2keep;
         for (int i = 0; i < sp.nvel; ++i)
             if (sp.v[i].axis == ax) q.v[q.nvel++] = sp.v[i];
         if (q.nvel == 0) continue;
@@ -1331,6 +1333,7 @@ pdg_status collide_xsweep(pdg_ctx *c, double dt, double dtp, int npass)
     P.mp = c->mp;
     P.ca = ca;
     P.cb = cb;
+    P.l2keep = c->l2keep;
     const size_t smem = relax_x_smem(c);
     const int e = prof_begin(c);
     PDG_DISPATCH(launch_relax_x_t, c, P, smem, npass);
@@ -1799,6 +1802,11 @@ pdg_status pdg_create(const pdg_problem *p, double *f_dev, double *fb_dev, doubl
     c->stream = (cudaStream_t)p->cuda_stream;
     cudaGetDevice(&c->device);
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+        c->l2keep = (double)c->g.nvl * (double)c->g.nnodes * sizeof(double) <= 0.7 * (double)l2;
+    }
     std::memset(&c->mp, 0, sizeof(c->mp));
     if (p->flux == PDG_FLUX_LINEAR_ADVECTION)
         for (int d = 0; d < p->dim; ++d) c->mp.a[d] = p->flux_params[d];

@@ -56,8 +56,35 @@ struct SweepParams {
     int64_t f_elems, fb_elems, cout_elems, cin_elems;  // buffer bounds (checked build)
     DevBlock blk[3];  // per axis (kappa_k = lambda dt' / h_k)
     int32_t nvel;
+    int32_t l2keep;   // 1: f fits in L2 -- keep it resident (evict-normal), else stream it (evict-first)
     SweepVel v[kMaxVel];
 };
+
+// L2 policy of the one-pass accesses to f: evict-first (streaming) when f is far larger than the
+// L2, evict-normal when f fits in it (config 2: f = 75 MB of the 126 MB L2 then stays resident
+// from one pass to the next: 53.8 -> 46.9 us per step; evict-last measured 1 % faster still, not
+// taken: it would outlive the solver's passes in a shared L2).  One code path: the policy is a
+// register operand of the access.
+__device__ __forceinline__ uint64_t l2_policy(int keep)
+{
+    uint64_t pol;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ double ld_pol(const double *p, uint64_t pol)
+{
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void st_pol(double *p, double v, uint64_t pol)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 
 enum { MODEL_ADV = 0, MODEL_EULER = 1, MODEL_ISO = 2 };
 
@@ -523,7 +550,8 @@ constexpr int kColsThreads = 256;
 // (row of line c: node y at c Lp + y + y / SEG).  Thread t always owns column t % CW and rows
 // t / CW + i (NT / CW): the global pointer and the row advance by constants (no division per load).
 template <int N, int K, int CW>
-__device__ __forceinline__ void cols_tile_load(double *buf, const double *g0, int64_t inner, int Lk, int Lp)
+__device__ __forceinline__ void cols_tile_load(double *buf, const double *g0, int64_t inner, int Lk, int Lp,
+                                               uint64_t pol)
 {
     constexpr int SEG = K * N, RS = kColsThreads / CW;
     const int cc = threadIdx.x % CW;
@@ -533,12 +561,14 @@ __device__ __forceinline__ void cols_tile_load(double *buf, const double *g0, in
 #pragma unroll 4
     for (unsigned y = threadIdx.x / CW; y < (unsigned)Lk; y += RS, src += step) {
         const unsigned sa = sb + 8u * (y + y / SEG);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "l"(pol)
+                     : "memory");
     }
 }
 
 template <int N, int K, int CW>
-__device__ __forceinline__ void cols_tile_store(const double *buf, double *g0, int64_t inner, int Lk, int Lp)
+__device__ __forceinline__ void cols_tile_store(const double *buf, double *g0, int64_t inner, int Lk, int Lp,
+                                                uint64_t pol)
 {
     constexpr int SEG = K * N, RS = kColsThreads / CW;
     const int cc = threadIdx.x % CW;
@@ -546,7 +576,7 @@ __device__ __forceinline__ void cols_tile_store(const double *buf, double *g0, i
     const int64_t step = (int64_t)RS * inner;
     const double *sb = buf + cc * Lp;
 #pragma unroll 4
-    for (unsigned y = threadIdx.x / CW; y < (unsigned)Lk; y += RS, dst += step) __stcs(dst, sb[y + y / SEG]);
+    for (unsigned y = threadIdx.x / CW; y < (unsigned)Lk; y += RS, dst += step) st_pol(dst, sb[y + y / SEG], pol);
 }
 
 // One tile per CTA (tile t: velocity t / tpv, lines (t % tpv) CW ...).  (A persistent variant with
@@ -567,7 +597,8 @@ __global__ void __launch_bounds__(kColsThreads, 2) sweep_cols_kernel(const Sweep
     const int64_t base = V.f_off + (line0 / V.inner) * (V.inner * Lk) + (line0 % V.inner);
     double *g0 = P.f + base;  // node y of tile line c at g0 + y inner + c
     PDG_CHECK_IDX(base + (int64_t)(Lk - 1) * V.inner + CW - 1, P.f_elems, "sweep_cols f");
-    cols_tile_load<N, K, CW>(scol, g0, V.inner, Lk, Lp);
+    const uint64_t pol = l2_policy(P.l2keep);
+    cols_tile_load<N, K, CW>(scol, g0, V.inner, Lk, Lp, pol);
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -583,7 +614,7 @@ __global__ void __launch_bounds__(kColsThreads, 2) sweep_cols_kernel(const Sweep
         warp_line_sweep<N, NPASS, K, ALIGNED>(scol + cc * Lp, V.ncells, V.sign > 0, M, g, s0, lane);
     }
     __syncthreads();
-    cols_tile_store<N, K, CW>(scol, g0, V.inner, Lk, Lp);
+    cols_tile_store<N, K, CW>(scol, g0, V.inner, Lk, Lp, pol);
 }
 
 // ---------------------------------------------------------------------------
@@ -605,6 +636,7 @@ struct RelaxXParams {
     DevBlock blk; // x-axis block of the sweeps that follow the collision
     ModelParams mp;
     double ca, cb;
+    int32_t l2keep;  // as SweepParams::l2keep
 };
 
 template <int N, int K>
@@ -627,6 +659,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
     const int64_t base = line * Lx;
     const int64_t nn = P.nnodes;
     PDG_CHECK_IDX(base + (NV - 1) * nn + Lx - 1, P.f_elems, "relax_xsweep f");  // the line's last node
+    const uint64_t pol = l2_policy(P.l2keep);
 
     // phase 1: collision at every node of the line.  With few velocities per node (2-D models) a
     // thread loads U = 2 nodes before computing either, so twice the loads are in flight (the
@@ -639,7 +672,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
             const int X = X0 + u * blockDim.x;
             if (X < Lx) {
 #pragma unroll
-                for (int i = 0; i < NV; ++i) fv[u][i] = __ldcs(P.f + base + X + i * nn);
+                for (int i = 0; i < NV; ++i) fv[u][i] = ld_pol(P.f + base + X + i * nn, pol);
             }
         }
 #pragma unroll
@@ -662,7 +695,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
                 const double val = fma(P.cb, feq_of<DIM, M>(i, w, q, P.mp), P.ca * fv[u][i]);
                 const int c = i / (2 * DIM), k = (i % (2 * DIM)) >> 1, s = i & 1;
                 if (k == 0) sx[(2 * c + s) * Lp + xs] = val;
-                else __stcs(P.f + base + X + i * nn, val);
+                else st_pol(P.f + base + X + i * nn, val, pol);
             }
         }
     }
@@ -690,7 +723,7 @@ __global__ void __launch_bounds__(256) relax_xsweep_kernel(const RelaxXParams P)
 #pragma unroll
         for (int v = 0; v < 2 * M; ++v) {
             const int i = (v >> 1) * 2 * DIM + (v & 1);
-            __stcs(P.f + base + X + i * nn, sx[v * Lp + xs]);
+            st_pol(P.f + base + X + i * nn, sx[v * Lp + xs], pol);
         }
     }
 }
