@@ -261,7 +261,9 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
  * first call of a given count pays the capture; same launches, same results); not while PDG_PROFILE
  * events are active (pdg_profile_enable), with PDG_SYNC_ERRORS, PDG_NO_GRAPH, a communicator, or
  * while the caller's stream is being captured (then the kernels go into the caller's graph).
- * Capturable by the caller. */
+ * Capturable by the caller.  L2 use: when f fits in 70 % of the device's L2 the passes access it
+ * with an evict-normal policy (it stays resident from one pass to the next), else evict-first
+ * (streaming); the arithmetic, and so the result, does not depend on it. */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
 
 /* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):
