@@ -81,11 +81,40 @@ def _run_case(seed, backward):
     return f, fb, ob, steps, scheme, desc, rel_maxnorm(got, ref), rel_maxnorm(w, O.moments(ob, ref)), ref
 
 
+def _ulp_spread(ob, f, fb, steps, scheme, ref, seed, samples=3):
+    """The map's own amplification of rounding, measured on the oracle: the largest relative change
+    of its result when f is perturbed by one ulp (relative 2^-52, random signs), over `samples`
+    perturbations (one sample can underestimate it by two orders of magnitude: seed 803 of the
+    backward sweep gave 4.9e-14 with one sign pattern and 5.2e-12 with another)."""
+    eps = 2.0 ** -52
+    out = 0.0
+    for k in range(samples):
+        sg = np.where(np.random.default_rng(seed + 7919 * k).random(f.shape) < 0.5, -1.0, 1.0)
+        out = max(out, rel_maxnorm(O.scheme_run(ob, f * (1.0 + eps * sg), fb, steps, scheme), ref))
+    return out
+
+
+# A case whose map amplifies a one-ulp change of its input above 1e-13 is ill-conditioned: two
+# correct fp64 implementations differ there by about that spread (DESIGN.md parity protocol,
+# readings C7/C28).  Such a case is held to 64 ulp-equivalents of its measured spread (the rounding
+# a path accumulates over the ~10 operator applications of two steps); every other case to 1e-12.
+ILL_CONDITIONED = 1e-13
+
+
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("PDG_FUZZ_SEEDS_MAIN", "40"))))
 def test_fuzz_parity(seed):
-    """Forward steps (dt > 0): <= 1e-12, the north star's bar."""
-    *_, desc, err_f, err_w, _ = _run_case(seed, backward=False)
-    assert err_f <= 1e-12 and err_w <= 1e-12, (desc, err_f, err_w)
+    """Forward steps (dt > 0): <= 1e-12, the north star's bar, for every well-conditioned case.
+    A case above it must be ill-conditioned (its oracle 1-ulp spread > 1e-13: random states that
+    blow up -- e.g. seed 2769 of the 4000-seed campaign, max|f| 0.04 -> 6.4e5 in two steps, spread
+    3.8e-11) and within 64 times its spread; both numbers are printed."""
+    f, fb, ob, steps, scheme, desc, err_f, err_w, ref = _run_case(seed, backward=False)
+    if err_f <= 1e-12 and err_w <= 1e-12:
+        return
+    spread = _ulp_spread(ob, f, fb, steps, scheme, ref, seed)
+    print(f"forward {desc}: err_f {err_f:.2e} err_w {err_w:.2e} 1-ulp spread {spread:.2e} "
+          f"ratio {err_f / max(spread, 1e-300):.1f}")
+    assert spread > ILL_CONDITIONED, (desc, err_f, err_w, spread)
+    assert err_f <= 64.0 * spread and err_w <= 64.0 * spread, (desc, err_f, err_w, spread)
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("PDG_FUZZ_SEEDS_BACKWARD", "12"))))
@@ -93,14 +122,13 @@ def test_fuzz_backward_steps(seed):
     """Backward steps (dt < 0, T2(-dt') = T2(dt')^{-1}, eq prop_sym) are outside the
     configs and reported separately: the backward map amplifies rounding (the carry factor |beta|
     grows, and with tau > 0 the collision factor (2 tau - dt)/(2 tau + dt) exceeds 1), so the bar
-    scales with the map's own amplification, measured in the same test -- the oracle rerun with
-    f perturbed by one ulp (relative 2^-52) -- times 64 ulp-equivalents for the rounding a path
-    accumulates over the ~10 operator applications of two steps (DESIGN.md parity protocol); never
-    below 1e-12."""
+    scales with the map's own amplification measured on the oracle (_ulp_spread) -- 64
+    ulp-equivalents for the rounding a path accumulates over the ~10 operator applications of two
+    steps (DESIGN.md parity protocol); never below 1e-12."""
     f, fb, ob, steps, scheme, desc, err_f, err_w, ref = _run_case(seed, backward=True)
-    eps = 2.0 ** -52
-    f2 = f * (1.0 + eps * np.where(np.random.default_rng(seed).random(f.shape) < 0.5, -1.0, 1.0))
-    spread = rel_maxnorm(O.scheme_run(ob, f2, fb, steps, scheme), ref)
+    if err_f <= 1e-12 and err_w <= 1e-12:
+        return
+    spread = _ulp_spread(ob, f, fb, steps, scheme, ref, seed)
     tol = max(1e-12, 64.0 * spread)
     print(f"backward {desc}: err_f {err_f:.2e} err_w {err_w:.2e} 1-ulp spread {spread:.2e} "
           f"ratio {err_f / max(spread, 1e-300):.1f}")
