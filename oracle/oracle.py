@@ -156,7 +156,10 @@ class Problem:
         cell_axes = [L + 2 * k for k in range(D)]      # slow..fast cell coords
         node_axes = [L + 2 * k + 1 for k in range(D)]  # slow..fast local coords
         a = a.transpose(tuple(range(L)) + tuple(cell_axes) + tuple(node_axes))
-        return np.ascontiguousarray(a.reshape(lead + (self.ncell, self.Nd)))
+        out = np.ascontiguousarray(a.reshape(lead + (self.ncell, self.Nd)))
+        # with one cell per axis the reordering is the identity and numpy returns a view: the
+        # drivers update their cell arrays in place, so the caller's grid must never be aliased
+        return out.copy() if np.may_share_memory(out, g) else out
 
     def cells_to_grid(self, c: np.ndarray) -> np.ndarray:
         lead = c.shape[:-2]
