@@ -324,7 +324,7 @@ def run_product(args, cfg):
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
         decomp = {"velocity": pdg.PDG_DECOMP_VELOCITY, "zslab": pdg.PDG_DECOMP_ZSLAB}[args.decomp]
-        flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST) | (pdg.PDG_NO_TMA if args.no_tma else 0)
+        flags = pdg.PDG_PROFILE | (0 if args.no_e2e else pdg.PDG_ASYNC_HOST) | (pdg.PDG_NO_TMA if args.no_tma else 0) | (pdg.PDG_NO_SMALL if args.no_small else 0)
         plan = {}
         if args.lattice_cta:
             plan["lattice_cta"] = tuple(int(x) for x in args.lattice_cta.split(","))
@@ -522,6 +522,8 @@ def main():
     ap.add_argument("--slabs-per-rank", type=int, default=1)
     ap.add_argument("--oracle-table", action="store_true",
                     help="time the CPU oracle on configs 1-3 at full size (1 thread and all cores) and exit")
+    ap.add_argument("--no-small", action="store_true",
+                    help="small problems: the general per-operator kernels instead of one CTA with f in shared memory (PDG_NO_SMALL)")
     ap.add_argument("--no-tma", action="store_true",
                     help="register-staged collision + x-sweep pass instead of bulk-copy staging (PDG_NO_TMA)")
     ap.add_argument("--one-decomp", action="store_true",

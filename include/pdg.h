@@ -143,6 +143,10 @@ typedef enum {
                                  result (PCIe is full duplex) */
 #define PDG_NO_GRAPH    0x40u /* pdg_step launches its kernels directly instead of replaying a CUDA graph of its
                                  n-step launch sequence (same results; for measurement) */
+#define PDG_NO_SMALL    0x80u /* small problems (f <= 64 KB, one rank, axis-aligned velocities) run pdg_step's
+                                 operators with the general per-operator kernels instead of one CTA holding f in
+                                 shared memory for up to 48 operators per launch (results agree to rounding:
+                                 the x sweeps of the general path take a warp scan; for measurement and tests) */
 #define PDG_NO_TMA      0x20u /* stage the line of the fused collision + x-sweep pass through registers instead of
                                  Tensor-Memory-Accelerator bulk copies (the variant for odd line lengths;
                                  same results; for measurement) */
@@ -159,7 +163,8 @@ typedef enum {
     PDG_K_RELAX_X = 7,       /* collision fused with moments and the following x-velocity sweep(s) */
     PDG_K_ZSLAB = 8,         /* z-slab carry pre-pass and scan (and the carry all-gather) */
     PDG_K_LATTICE = 9,       /* T2 sweeps of lattice velocities with >= 2 non-zero components (NEXT-2) */
-    PDG_NUM_KERNEL_KINDS = 10
+    PDG_K_SMALL = 10,        /* small problems: a run of operators in one CTA with f in shared memory */
+    PDG_NUM_KERNEL_KINDS = 11
 } pdg_kernel_kind;
 
 typedef struct {
@@ -263,7 +268,10 @@ pdg_status pdg_get_state(pdg_ctx *c, double *f, int on_device);
  * while the caller's stream is being captured (then the kernels go into the caller's graph).
  * Capturable by the caller.  L2 use: when f fits in 70 % of the device's L2 the passes access it
  * with an evict-normal policy (it stays resident from one pass to the next), else evict-first
- * (streaming); the arithmetic, and so the result, does not depend on it. */
+ * (streaming); the arithmetic, and so the result, does not depend on it.  Small problems (f of at
+ * most 64 KB with padded rows, one rank, axis-aligned velocities, no PDG_NO_SMALL) run the step's
+ * operators in one CTA holding f in shared memory, up to 48 operators per launch; the x sweeps then
+ * carry sequentially instead of by the warp scan (results agree to rounding). */
 pdg_status pdg_step(pdg_ctx *c, int64_t nsteps);
 
 /* One transport operator T2(dtp) on every local velocity (rows a1/a3 of the hot path):

@@ -1391,8 +1391,109 @@ void append_scheme(std::vector<Op> &ops, int scheme, double dt)
     }
 }
 
+// ---- small problems: a run of operators in one CTA (pdg_kernels.cuh small_run_kernel) ----------
+constexpr size_t kSmallBytes = 64 * 1024;  // f in shared memory
+
+int small_lp(const Geometry &g) { return (int)(g.L[0] | 1); }  // odd row stride in shared memory
+
+size_t small_smem(const Geometry &g)
+{
+    return sizeof(double) * (size_t)g.nvl * (size_t)(g.nnodes / g.L[0]) * (size_t)small_lp(g);
+}
+
+bool use_small(const pdg_ctx *c)
+{
+    const Geometry &g = c->g;
+    return !g.lattice && !g.zslab && !sharded(c) && c->prob.nranks == 1 && !(c->prob.flags & PDG_NO_SMALL) &&
+           g.nvl == c->all_params.nvel && c->all_params.nvel <= pdg::kMaxVel && small_smem(g) <= kSmallBytes;
+}
+
+template <int DIM, int MODEL, int N>
+void launch_small_n(pdg_ctx *c, const pdg::SmallParams &P, size_t smem)
+{
+    auto kern = pdg::small_run_kernel<DIM, MODEL, N>;
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), 0, (size_t)1);
+    if (c->launch_cache.find(key) == c->launch_cache.end()) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallBytes);
+        c->launch_cache[key] = 1;
+    }
+    kern<<<1, pdg::kSmallThreads, smem, c->stream>>>(P);
+}
+
+template <int DIM, int MODEL>
+void launch_small_t(pdg_ctx *c, const pdg::SmallParams &P, size_t smem)
+{
+    if (c->g.n == 2) launch_small_n<DIM, MODEL, 2>(c, P, smem);
+    else if (c->g.n == 3) launch_small_n<DIM, MODEL, 3>(c, P, smem);
+    else launch_small_n<DIM, MODEL, 4>(c, P, smem);
+}
+
+pdg_status small_run(pdg_ctx *c, const std::vector<Op> &ops)
+{
+    NvtxRange nv("pdg small run");
+    const Geometry &g = c->g;
+    pdg::SmallParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.f = c->f;
+    P.fb = c->fb;
+    P.nnodes = g.nnodes;
+    P.f_elems = (int64_t)g.nvl * g.nnodes;
+    P.fb_elems = (int64_t)g.nvl * g.nplanes * g.plane_stride;
+    P.nvel = c->all_params.nvel;
+    P.line0[0] = 0;
+    for (int i = 0; i < P.nvel; ++i) {
+        P.v[i] = c->all_params.v[i];
+        P.line0[i + 1] = P.line0[i] + (P.v[i].nlines + 31) / 32 * 32;
+    }
+    P.mp = c->mp;
+    P.L0 = (int32_t)g.L[0];
+    P.Lp = small_lp(g);
+    P.vstride = (g.nnodes / g.L[0]) * P.Lp;
+    P.sstr[0] = 1;
+    P.sstr[1] = P.Lp;
+    P.sstr[2] = (int64_t)P.Lp * g.L[1];
+    const size_t smem = small_smem(g);
+    std::vector<double> hs;  // T2 step sizes of the current launch, index = block set
+    auto flush = [&]() -> pdg_status {
+        if (P.nops == 0) return PDG_OK;
+        const int e = prof_begin(c);
+        PDG_DISPATCH(launch_small_t, c, P, smem);
+        prof_end(c, e, PDG_K_SMALL, 16.0 * (double)g.nvl * (double)g.nnodes);
+        P.nops = 0;
+        hs.clear();
+        return post_launch(c, "small_run");
+    };
+    for (const Op &o : ops) {
+        if (o.kind == 2) return fail(PDG_E_UNSUPPORTED, "source step without a lattice model");
+        int bi = -1;
+        if (o.kind == 0) {
+            for (size_t k = 0; k < hs.size(); ++k)
+                if (hs[k] == o.h) bi = (int)k;
+            if (bi < 0 && hs.size() == (size_t)pdg::kSmallMaxBlk) {
+                pdg_status s = flush();
+                if (s != PDG_OK) return s;
+            }
+            if (bi < 0) {
+                bi = (int)hs.size();
+                if (!fill_blocks(c, o.h, P.blk[bi])) return fail(PDG_E_INVALID_ARGUMENT, "singular cell block for this dt");
+                hs.push_back(o.h);
+            }
+        }
+        pdg::SmallOp &so = P.op[P.nops++];
+        so.kind = o.kind;
+        so.blk = bi;
+        if (o.kind == 1) collision_coeffs(c, o.h, &so.ca, &so.cb);
+        if (P.nops == pdg::kSmallMaxOps) {
+            pdg_status s = flush();
+            if (s != PDG_OK) return s;
+        }
+    }
+    return flush();
+}
+
 pdg_status execute_ops(pdg_ctx *c, const std::vector<Op> &ops)
 {
+    if (use_small(c)) return small_run(c, ops);
     const bool fuse = !(c->prob.flags & PDG_NO_FUSION);
     const bool fx = use_relax_x(c);
     const size_t n = ops.size();

@@ -1197,4 +1197,118 @@ __global__ void __launch_bounds__(256) zslab_carry_kernel(const SweepParams P, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Small problems (config 1: f = 18 KB): a whole pdg_step(n) is a sequence of short dependent
+// passes, each far too small to fill the GPU, so the step is bound by launch and drain latency
+// (2 launches per step in a graph replay: ~7.7 us per step).  One CTA holds f in shared memory
+// and runs the step's operator list (T2 sweeps and C2 collisions, same arithmetic as
+// sweep_strided_kernel and relax_kernel: sequential carry per line, per-node collision) with a
+// barrier between operators; f is read once and written once per launch.
+// ---------------------------------------------------------------------------
+constexpr int kSmallMaxOps = 48;   // operators per launch (longer lists take several launches)
+constexpr int kSmallMaxBlk = 6;    // distinct T2 step sizes per launch
+constexpr int kSmallThreads = 512;
+
+struct SmallOp {
+    int32_t kind;  // 0: T2 (blk = its block set), 1: C2 (f <- ca f + cb f^eq)
+    int32_t blk;
+    double ca, cb;
+};
+
+struct SmallParams {
+    double *f;
+    const double *fb;
+    int64_t nnodes;
+    int64_t f_elems, fb_elems;  // buffer bounds (checked build)
+    int32_t nvel, nops;
+    int32_t L0, Lp;      // nodes per x row in HBM and in shared memory (Lp odd: x-line walks of
+                         // neighbouring threads fall on different banks)
+    int64_t vstride;     // shared-memory elements per velocity (rows x Lp)
+    int64_t sstr[3];     // shared-memory element stride per axis (1, Lp, Lp L1)
+    int64_t line0[kMaxVel + 1];  // prefix sums of the velocities' line counts, each rounded up to a
+                                 // multiple of 32: every warp sweeps lines of one velocity, so its
+                                 // velocity record and block come from the parameter bank uniformly
+    SweepVel v[kMaxVel];
+    DevBlock blk[kSmallMaxBlk][3];
+    SmallOp op[kSmallMaxOps];
+    ModelParams mp;
+};
+
+template <int DIM, int MODEL, int N>
+__global__ void __launch_bounds__(kSmallThreads) small_run_kernel(const __grid_constant__ SmallParams P)
+{
+    using Md = Model<DIM, MODEL>;
+    constexpr int M = Md::M;
+    constexpr int NV = M * 2 * DIM;
+    extern __shared__ double sf[];  // f as [velocity][row][Lp] (HBM: [velocity][row][L0])
+    const int64_t tot = (int64_t)NV * P.nnodes;
+    PDG_CHECK_IDX(tot - 1, P.f_elems, "small_run f");
+    auto sidx = [&](int64_t g) -> int64_t { return (g / P.L0) * P.Lp + g % P.L0; };  // node -> shared
+    for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int64_t v = i / P.nnodes, x = i - v * P.nnodes;
+        sf[v * P.vstride + sidx(x)] = P.f[i];
+    }
+    __syncthreads();
+    for (int o = 0; o < P.nops; ++o) {
+        const SmallOp op = P.op[o];
+        if (op.kind == 1) {
+            for (int64_t x = threadIdx.x; x < P.nnodes; x += blockDim.x) {
+                const int64_t sx = sidx(x);
+                double fv[NV];
+#pragma unroll
+                for (int i = 0; i < NV; ++i) fv[i] = sf[(int64_t)i * P.vstride + sx];
+                double w[M];
+#pragma unroll
+                for (int c = 0; c < M; ++c) {
+                    double s = fv[c * 2 * DIM];
+#pragma unroll
+                    for (int j = 1; j < 2 * DIM; ++j) s += fv[c * 2 * DIM + j];
+                    w[c] = s;
+                }
+                double q[DIM][M];
+                Md::flux(w, q, P.mp);
+#pragma unroll
+                for (int i = 0; i < NV; ++i) sf[(int64_t)i * P.vstride + sx] = fma(op.cb, feq_of<DIM, M>(i, w, q, P.mp), op.ca * fv[i]);
+            }
+        } else {
+            const int64_t nl = P.line0[P.nvel];
+            for (int64_t t = threadIdx.x; t < nl; t += blockDim.x) {
+                int vi = 0;
+                while (t >= P.line0[vi + 1]) ++vi;
+                const SweepVel &V = P.v[vi];
+                const int64_t line = t - P.line0[vi];
+                if (line >= V.nlines) continue;
+                const DevBlock &B = P.blk[op.blk][V.axis];
+                const int64_t Lk = (int64_t)V.ncells * N;
+                const int64_t base = (line / V.inner) * (V.inner * Lk) + (line % V.inner);  // first node
+                const int64_t ss = P.sstr[V.axis];
+                const int64_t step = (V.sign > 0) ? ss : -ss;
+                double *p = sf + (V.f_off / P.nnodes) * P.vstride + sidx(base) + ((V.sign > 0) ? 0 : (Lk - 1) * ss);
+                PDG_CHECK_IDX(V.fb_off + line, P.fb_elems, "small_run fb");
+                double carry = 2.0 * P.fb[V.fb_off + line];  // ghost cell: f^b old + f^b new (reading C5)
+                for (int cl = 0; cl < V.ncells; ++cl, p += N * step) {
+                    double fo[N], fn[N];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) fo[a] = p[a * step];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) {
+                        double acc = B.g[a] * carry;
+#pragma unroll
+                        for (int b = 0; b < N; ++b) acc = fma(B.M[a * N + b], fo[b], acc);
+                        fn[a] = acc;
+                    }
+                    carry = fo[N - 1] + fn[N - 1];
+#pragma unroll
+                    for (int a = 0; a < N; ++a) p[a * step] = fn[a];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int64_t v = i / P.nnodes, x = i - v * P.nnodes;
+        P.f[i] = sf[v * P.vstride + sidx(x)];
+    }
+}
+
 }  // namespace pdg

@@ -45,8 +45,9 @@ PDG_PROFILE = 0x8
 PDG_ASYNC_HOST = 0x10
 PDG_NO_TMA = 0x20
 PDG_NO_GRAPH = 0x40
+PDG_NO_SMALL = 0x80
 KERNEL_KINDS = ["sweep_strided", "sweep_x", "relax", "partial_moments", "relax_from_w", "allreduce", "other",
-                "relax_xsweep", "zslab", "lattice"]
+                "relax_xsweep", "zslab", "lattice", "small_run"]
 PDG_DECOMP_VELOCITY = 0
 PDG_DECOMP_ZSLAB = 1
 

@@ -629,3 +629,43 @@ def test_profile_pause_and_resume():
     with pytest.raises(pdg.PdgError):
         T.profile_enable(True)  # created without PDG_PROFILE
     T.destroy()
+
+
+@pytest.mark.parametrize("key,N,scheme_name,tau,steps", [
+    (1, 8, "m2", 0.0, 10),       # config 1 as written: 30 operators, one launch
+    (1, 8, "m2", 0.0, 40),       # 120 operators: three launches (48 per launch)
+    (1, 5, "m2kin", 0.02, 7),
+    (1, 8, "m4", 0.05, 3),       # four distinct T2 step sizes in one launch, a negative one
+    (2, 3, "m2", 0.0, 6),        # 2-D Euler, 16 velocities (f = 41 KB)
+    (3, 2, "m2", 0.0, 5),        # 3-D isothermal, 24 velocities (f = 41 KB)
+    (4, 1, "m2kin", 0.01, 4),    # p = 3, one cell per axis
+])
+def test_small_problem_run(key, N, scheme_name, tau, steps):
+    """Small problems (f <= 64 KB): pdg_step runs its operators in one CTA with f in shared memory
+    (small_run_kernel) -- against the oracle, against the general per-operator kernels
+    (PDG_NO_SMALL) to rounding, and the launch count (ceil(operators / 48) per call)."""
+    from paper_1702_00169_b200 import pdg
+    code = {"m2": pdg.PDG_SCHEME_M2, "m2kin": pdg.PDG_SCHEME_M2KIN, "m4": pdg.PDG_SCHEME_M4}[scheme_name]
+    cfg = CONFIGS[key].resized(N)
+    if key != 1:
+        cfg = cfg.stabilised()
+    pb, f0, fbg = seeded_equilibrium(cfg)
+    pb.tau = tau
+    ref = O.scheme_run(pb, f0, fbg, steps, scheme_name)
+    outs = []
+    for flags in (pdg.PDG_PROFILE, pdg.PDG_PROFILE | pdg.PDG_NO_SMALL):
+        S = gpu_with_state(cfg, f0, fbg, scheme=code, tau=tau, flags=flags)
+        S.step(steps)
+        prof = S.profile_read()
+        got = to_np(S.get_state(), f0.shape)
+        S.destroy()
+        assert rel_maxnorm(got, ref) < TOL_STEP, flags
+        outs.append(got)
+        small = prof["small_run"][1]
+        if flags & pdg.PDG_NO_SMALL:
+            assert small == 0, prof
+        else:
+            nops = {"m2": 3, "m2kin": 5, "m4": 15}[scheme_name] * steps
+            assert small == -(-nops // 48), prof
+            assert sum(v[1] for k, v in prof.items() if k != "small_run") == 0, prof
+    assert rel_maxnorm(outs[0], outs[1]) < 1e-13
